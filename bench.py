@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""bench.py -- time-to-k-sensors of greedy D-optimal selection on B200.
+
+Contract (driver): `python bench.py --gpus N --steps K --warmup W` prints ONE
+JSON line on rank 0. A "step" is one full greedy selection (B rounds of
+gains -> argmax -> panel -> rank-Nt Schur update) over the synthetic K of the
+workload, with K resident in HBM when the timed region starts (C is restored
+from the pristine device copy between steps, outside the timed region).
+
+Workload (BASELINE.json configs[1], the metric's single-GPU config):
+  C2: SyntheticKAccess(200 sensors, Nt=128, rank 8192, sigma=1, seed 2024),
+  budget 50, n = 25,600, K = 5.24 GB FP64. At N > 1 the same problem is
+  block-column sharded over N GPUs (strong scaling, NCCL argmax allgather +
+  panel broadcast). `--config c3` selects the weak-scaling workload
+  (75*N sensors x Nt=420, rank 24,576, budget 50).
+
+`--impl reference` times the reference CPU implementation (oracle/_ref, the
+unmodified reference headers compiled from /root/reference) on the host's
+cores over a bounded sample (see cpu_reference()).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": dict(nd=64, nt=32, rank=2048, budget=16),
+    "c2": dict(nd=200, nt=128, rank=8192, budget=50),
+    "c3": dict(nd=75, nt=420, rank=24576, budget=50),  # nd scaled by N
+}
+SIGMA, SEED = 1.0, 2024
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# FP64 denominators measured on this pool's B200 (profiles/r01_fp64_peak_probe.log):
+# DMMA.8x8x4 issue-bound microbenchmark 37.10 TFLOP/s; cuBLAS DGEMM 16384^3 36.13.
+FP64_DMMA_PEAK_TFLOPS = 37.10
+FP64_CUBLAS_TFLOPS = 36.13
+
+
+def workload(name: str, n_gpus: int) -> dict:
+    w = dict(CONFIGS[name])
+    if name == "c3":
+        w["nd"] = 75 * n_gpus
+    return w
+
+
+# ------------------------------------------------------------------------- #
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        try:
+            p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                  "--format=csv,noheader,nounits", "-lms", "200"],
+                                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            return
+        while not self._stop.is_set():
+            line = p.stdout.readline()
+            if not line:
+                break
+            self.rows.append([x.strip() for x in line.split(",")])
+        p.terminate()
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower().startswith("active")})
+        loaded = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(loaded or sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------------- #
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def allreduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def broadcast_bytes(b: bytes | None, world: int) -> bytes:
+    if world == 1:
+        return b
+    import torch.distributed as dist
+
+    obj = [b]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def ncu_traffic(profile_dir: str):
+    """dram bytes per update-kernel launch from a committed `ncu --set full`
+    capture summary (profiles/*update*_dram.json), else None."""
+    import glob
+
+    for p in sorted(glob.glob(os.path.join(profile_dir, "*update*dram*.json")), reverse=True):
+        try:
+            return json.load(open(p))
+        except Exception:
+            pass
+    return None
+
+
+# ------------------------------------------------------------------------- #
+def our_arm(args, world, rank, local):
+    import numpy as np
+
+    import paper_2604_08812_b200 as d
+
+    w = workload(args.config, world)
+    nd, nt, vrank, budget = w["nd"], w["nt"], w["rank"], w["budget"]
+    t0 = time.time()
+    v = d.synthetic_v(nd, nt, vrank, SEED, threads=max(1, (os.cpu_count() or 1) // world))
+    t_v = time.time() - t0
+    nid = broadcast_bytes(d.nccl_unique_id() if (world > 1 and rank == 0) else None, world)
+    eng = d.Engine(nd, nt, budget, device=local, world_size=world, rank=rank, nccl_id=nid,
+                   keep_pristine=True, export_factor=True)
+    t0 = time.time()
+    eng.gen_synthetic(v, vrank, SIGMA)
+    t_gen = time.time() - t0
+    del v
+
+    # ---- device-resident timing: K steps of a full selection ----
+    times, upd_ms, upd_fl, launches, chosen = [], [], [], [], None
+    with ClockSampler(local) as clk:
+        for it in range(args.warmup + args.steps):
+            eng.reset()
+            barrier(world)
+            eng.run()
+            st = eng.stats()
+            t = allreduce_max(st["time_to_k_ms"] / 1e3, world)
+            if it >= args.warmup:
+                times.append(t)
+                upd_ms.append(st["update_ms"])
+                upd_fl.append(st["update_flops"])
+                launches.append(st["kernel_launches"])
+            rows = eng.trace()
+            chosen = [r["chosen_index"] for r in rows]
+    clocks = clk.summary()
+    value = sum(times) / len(times)
+    # dominant kernel: the rank-Nt Schur update (per-rank flops / per-rank kernel time)
+    upd_t = sum(upd_ms) / 1e3
+    upd_tf = sum(upd_fl) / upd_t / 1e12 if upd_t > 0 else 0.0
+    upd_tf_all = allreduce_max(upd_tf, world)  # report the slowest-rank view below
+    tot_flops = sum(upd_fl) / len(upd_fl)
+    tot_flops_all = tot_flops * world  # every rank updates its own shard
+    e2e_tf = tot_flops_all / value / 1e12
+
+    # ---- e2e through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        import torch
+
+        mine = [j for p, j in enumerate(range(nd)) if p % world == rank]
+        row_elems = nd * nt * nt
+        host = torch.empty(nd * row_elems, dtype=torch.float64).pin_memory() if world == 1 else \
+            torch.empty(nd * row_elems, dtype=torch.float64).pin_memory()
+        eng.reset()
+        hv = host.numpy()
+        for j in mine:
+            hv[j * row_elems:(j + 1) * row_elems] = eng.read_block_row(j)
+        e2e_times, h2d, d2h = [], 0, 0
+        for it in range(max(1, args.warmup // 2) + args.steps):
+            eng.reset()
+            barrier(world)
+            t0 = time.perf_counter()
+            eng.load_k(host)              # H2D of this rank's block rows (pinned)
+            eng.run()
+            rows = eng.trace()            # D2H of the selection result
+            res = np.array([[r["chosen_index"], r["gain"]] for r in rows])
+            t1 = time.perf_counter() - t0
+            st = eng.stats()
+            if it >= max(1, args.warmup // 2):
+                e2e_times.append(allreduce_max(t1, world))
+                h2d = st["h2d_bytes"]
+                d2h = st["d2h_bytes"] + res.size * 8
+            assert [int(x) for x in res[:, 0]] == chosen
+        e2e = {"value": sum(e2e_times) / len(e2e_times), "unit": "s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+        cpu_k = hv if (rank == 0 and world == 1) else None
+    else:
+        cpu_k = None
+
+    # ---- CPU baseline: the reference on a bounded sample (rank 0, N=1) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        if cpu_k is None:
+            import numpy as np2
+
+            cpu_k = np2.concatenate([eng.read_block_row(j) for j in range(nd)])
+        cpu = cpu_reference(cpu_k, nd, nt, budget, chosen)
+    eng.close()
+
+    traffic = ncu_traffic(os.path.join(ROOT, "profiles"))
+    peak = FP64_DMMA_PEAK_TFLOPS
+    line = {
+        "metric": "time-to-k-sensors (s)",
+        "value": round(value, 6),
+        "unit": "s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(value * 1e3, 3),
+        "higher_is_better": False,
+        "scaling": "weak" if args.config == "c3" else "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic: SyntheticKAccess K = sigma^2 I + V V^T (reference RNG stream, "
+                "bit-exact device generator)",
+        "config": {"workload": f"{args.config.upper()}: {nd} candidates x Nt={nt} "
+                               f"(n={nd * nt}) select {budget}, rank {vrank}, sigma {SIGMA}, "
+                               f"seed {SEED}, K resident in HBM",
+                   "n_sensors": nd, "n_steps": nt, "budget": budget, "rank": vrank,
+                   "parallelism": f"candidate-sharded x{world} (cyclic block columns), "
+                                  "NCCL allgather(argmax) + broadcast(panel)",
+                   "l2": f"inputs {nd * nt * nd * nt * 8 / 1e9:.2f} GB >> 126 MB L2 (no flush needed)",
+                   "chosen_first": chosen[:8]},
+        "schur_update": {"flops_per_step_per_rank": tot_flops,
+                         "flops_per_step_all_ranks": tot_flops_all,
+                         "kernel_tflops_per_gpu": round(upd_tf, 3),
+                         "kernel_tflops_per_gpu_max_rank": round(upd_tf_all, 3),
+                         "end_to_end_tflops_all_gpus": round(e2e_tf, 3),
+                         "frac_of_fp64_peak_per_gpu": round(upd_tf / peak, 4),
+                         "flop_model": "full-square right-looking: sum_t 2*Nt*(R_t*Nt)*(R_loc,t*Nt)"},
+        "roofline": {"bound": "tensor", "kernel": "schur_update_kernel (DMMA.8x8x4)",
+                     "achieved": round(upd_tf, 3), "peak": peak, "unit": "TFLOP/s",
+                     "frac": round(upd_tf / peak, 4),
+                     "peak_source": "measured FP64 DMMA peak on this pool's B200 "
+                                    "(profiles/r01_fp64_peak_probe.log; cuBLAS DGEMM "
+                                    f"{FP64_CUBLAS_TFLOPS}); MEASURED_PEAKS.json has no FP64 entry",
+                     "traffic": traffic},
+        "e2e": e2e,
+        "gpu_launches": int(sum(launches) / len(launches)) if launches else 0,
+        "clocks": clocks,
+        "setup": {"v_host_s": round(t_v, 2), "k_gen_device_s": round(t_gen, 2)},
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------- #
+def alg1_round_cost(nd, nt, k):
+    """Reference per-round cost model (Alg. 1 flops):
+    (Nd-k) candidates x [(k Nt)^2 Nt (trsm) + 2 k Nt^3 (Schur) + Nt^3/3 (chol)]."""
+    return (nd - k) * ((k * nt) ** 2 * nt + 2 * k * nt ** 3 + nt ** 3 / 3)
+
+
+def cpu_reference(k_host, nd, nt, budget, prefix, iterates=None):
+    """Reference CPU path (oracle/_ref: unmodified reference headers) on a
+    BOUNDED sample: one full evaluation round (detail::timed_round, all host
+    threads, pipelined) at a few iterates along the selected prefix, then
+    time-to-k extrapolated with the Alg. 1 cost model fitted to the samples
+    (T(k) = a*cost(k) + b*(Nd-k))."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    cores = os.cpu_count() or 1
+    if iterates is None:
+        iterates = [1, budget // 4, budget // 2] if budget >= 8 else list(range(1, budget))
+    ms, setup = O.ref_timed_rounds(np.ascontiguousarray(k_host), nd, nt, prefix, iterates, cores)
+    A = np.array([[alg1_round_cost(nd, nt, k), nd - k] for k in iterates], dtype=np.float64)
+    coef, *_ = np.linalg.lstsq(A, np.asarray(ms) / 1e3, rcond=None)
+    a, b = max(coef[0], 0.0), max(coef[1], 0.0)
+    total = sum(a * alg1_round_cost(nd, nt, k) + b * (nd - k) for k in range(budget))
+    return {"value": round(total, 3), "unit": "s", "cores": cores, "kind": "reference",
+            "sample": f"reference run_parallel_greedy round (detail::timed_round, {cores} "
+                      f"workers) timed at iterates {iterates} = {[round(x, 1) for x in ms]} ms; "
+                      f"time-to-{budget} EXTRAPOLATED with the Alg.1 cost model "
+                      f"(a={a:.3e} s/flop, b={b:.3e} s/cand)",
+            "sampled_rounds_ms": list(map(float, ms)), "setup_ms": list(map(float, setup))}
+
+
+def reference_arm(args, world, rank, local):
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle import oracle as O
+
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built "
+                          "(needs /root/reference at build time)"}))
+        return
+    w = workload(args.config, 1)
+    nd, nt, vrank, budget = w["nd"], w["nt"], w["rank"], w["budget"]
+    # Input K: materialized by the bit-exact device generator (identical bytes to
+    # SyntheticKAccess, tests/test_gpu_parity.py::test_synthetic_generator_bit_exact)
+    # because the reference's own materialization of C2 takes ~5 min on 16 cores.
+    # Only the reference runs inside the timed samples.
+    import paper_2604_08812_b200 as d
+
+    v = d.synthetic_v(nd, nt, vrank, SEED)
+    with d.Engine(nd, nt, budget, device=local) as eng:
+        eng.gen_synthetic(v, vrank, SIGMA)
+        del v
+        k = np.concatenate([eng.read_block_row(j) for j in range(nd)])
+        eng.run()
+        prefix = [r["chosen_index"] for r in eng.trace()]
+    vals = []
+    for it in range(args.warmup + args.steps):
+        its = [1, budget // 4, budget // 2] if it >= args.warmup else [1, 2]
+        cpu = cpu_reference(k, nd, nt, budget, prefix, iterates=its)
+        if it >= args.warmup:
+            vals.append(cpu)
+    value = sum(c["value"] for c in vals) / len(vals)
+    cpu = vals[-1]
+    cpu["value"] = round(value, 3)
+    line = {"metric": "time-to-k-sensors (s)", "value": round(value, 3), "unit": "s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(value * 1e3, 1), "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SyntheticKAccess K, bit-identical)",
+            "config": {"workload": f"{args.config.upper()}: {nd} candidates x Nt={nt} select "
+                                   f"{budget}, rank {vrank} (reference CPU, bounded sample)"},
+            "impl": "reference", "cpu_baseline": cpu,
+            "e2e": {"value": round(value, 3), "unit": "s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_init()
+    if args.impl == "reference":
+        reference_arm(args, world, rank, local)
+    else:
+        our_arm(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

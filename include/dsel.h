@@ -1,0 +1,172 @@
+/*
+ * dsel.h -- C ABI of the B200-native greedy D-optimal selection engine.
+ *
+ * Drop-in boundary for the reference `doptsel` selection path
+ * (/root/reference/proj/include/doptsel). Plain C: pointers, sizes and
+ * status codes, no exceptions, no torch types. Every entry point lists the
+ * reference interface it replaces.
+ *
+ *   reference (C++ templates, CPU threads)         this ABI (sm_100a, NCCL)
+ *   ---------------------------------------------  -------------------------------
+ *   run_parallel_greedy<Real,A>  parallel.hpp:281   dsel_create + dsel_step* (one
+ *   greedy_select<Real,A>        selector.hpp:181     engine per GPU/rank)
+ *   KAccess::read_block          kaccess.hpp:18-23  dsel_load_block_row /
+ *   KStoreReader::read_block     kstore.hpp:141       dsel_load_block_col
+ *   SyntheticKAccess             kaccess.hpp:81     dsel_synthetic_v + dsel_gen_synthetic
+ *   score_candidate (all s)      selector.hpp:105   dsel_peek_gains
+ *   reduce_argmax / tie rule     parallel.hpp:61,   inside dsel_step (device top-2,
+ *                                selector.hpp:132     allgather, identical fold)
+ *   SelectionState::factor       selector.hpp:31    dsel_export_factor
+ *   TraceRow / RoundResult       selector.hpp:40,   dsel_step_info
+ *                                parallel.hpp:30
+ *   doptsel::Error family        errors.hpp:10-86   dsel_status + dsel_last_error
+ *
+ * The C++ wrapper include/doptsel_gpu.hpp maps these back onto the
+ * reference types and exceptions.
+ */
+#ifndef DSEL_H_
+#define DSEL_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DSEL_ABI_VERSION 1
+
+typedef enum {
+  DSEL_OK = 0,
+  DSEL_E_INVALID = 1,    /* InvalidConfig / DimensionMismatch (errors.hpp) */
+  DSEL_E_RANGE = 2,      /* IndexOutOfRange */
+  DSEL_E_INFEASIBLE = 3, /* InfeasibleRound: round 1 had no feasible candidate */
+  DSEL_E_CUDA = 4,       /* device failure -> WorkerFailure */
+  DSEL_E_NCCL = 5,       /* collective failure -> WorkerFailure */
+  DSEL_E_OOM = 6,        /* device/pinned allocation failed in dsel_create */
+  DSEL_E_IO = 7,         /* IoError / CorruptFile */
+  DSEL_E_STATE = 8       /* call out of order (e.g. step after the budget) */
+} dsel_status;
+
+typedef enum { DSEL_STORAGE_AUTO = 0, DSEL_STORAGE_HBM = 1, DSEL_STORAGE_STREAM = 2 } dsel_storage;
+
+typedef struct dsel_engine dsel_engine;
+
+typedef struct {
+  int n_sensors;          /* KAccess::n_sensors() */
+  int n_steps;            /* KAccess::n_steps() = Nt */
+  int budget;             /* B (>= 0) */
+  int n_candidates;       /* 0 = all sensors 0..n_sensors-1 */
+  const int* candidates;  /* borrowed during dsel_create only; duplicates -> E_INVALID */
+  int device;             /* CUDA device of this engine */
+  int world_size;         /* ranks sharing the candidate set (1 = single GPU) */
+  int rank;               /* 0..world_size-1 */
+  const void* nccl_id;    /* 128-byte ncclUniqueId (dsel_nccl_unique_id) when world_size > 1 */
+  int storage;            /* dsel_storage; STREAM is reserved (returns E_INVALID) */
+  int keep_pristine;      /* keep a device copy of K so dsel_reset can rerun */
+  int export_factor;      /* keep per-step W rows so dsel_export_factor can rebuild L_S */
+  double near_tie_tau;    /* near-tie flag threshold (default 1e-9 when 0) */
+} dsel_config;
+
+/* One selection round; field names follow TraceRow (selector.hpp:40-49) and
+ * RoundResult (parallel.hpp:30-35). Times are device milliseconds measured
+ * with CUDA events on this rank's compute stream (filled by dsel_get_trace
+ * after dsel_sync; dsel_step leaves them 0). */
+typedef struct {
+  int k;                  /* 1-based round */
+  int chosen_index;       /* sensor id; -1 if no feasible candidate remained */
+  double gain;            /* raw d_max = log det(M_s*) */
+  double objective;       /* running log det(K_S) */
+  int runner_up;          /* sensor id of the second best, -1 if none */
+  double runner_up_gain;
+  int near_tie;           /* (g1-g2)/max(|g1|,1) < tau */
+  int n_evaluated;
+  int n_infeasible;
+  uint64_t bytes_exchanged; /* argmax allgather + panel broadcast bytes */
+  double ms_gain;         /* gain kernel + local argmax */
+  double ms_exchange;     /* allgather + D2H of the 32-byte records */
+  double ms_panel;        /* panel broadcast + chol(C_kk) + L^{-1} + W */
+  double ms_update;       /* rank-nt Schur update (+ factor history) */
+  double ms_round;        /* whole round on the device */
+  double update_flops;    /* algorithmic flops of this rank's update: 2*nt*rows*cols */
+} dsel_step_info;
+
+/* ---- lifecycle ---------------------------------------------------------- */
+int dsel_abi_version(void);
+dsel_status dsel_nccl_unique_id(void* out128);
+dsel_status dsel_create(const dsel_config* cfg, dsel_engine** out);
+void dsel_destroy(dsel_engine* e);
+const char* dsel_last_error(const dsel_engine* e); /* NULL engine -> last create error */
+dsel_status dsel_sync(dsel_engine* e);
+/* bytes of device memory the engine holds */
+uint64_t dsel_device_bytes(const dsel_engine* e);
+
+/* ---- panel store ingest (north-star (1)) -------------------------------- */
+/* Block row j of K: blocks (j, i), i = 0..n_sensors-1, each row-major Nt x Nt
+ * (exactly KBF payload rows, kstore.hpp:22-35). Uses K(i,j) = K(j,i)^T, exact
+ * for symmetric K (SyntheticKAccess, assemble_k). No-op if j is not a
+ * candidate owned by this rank. Host memory may be pageable or pinned. */
+dsel_status dsel_load_block_row(dsel_engine* e, int j, const double* host_row);
+/* Block column j: blocks (i, j), i = 0..n_sensors-1, each row-major, stacked
+ * (what read_test_column reads, kaccess.hpp:27-35). Exact for any K. */
+dsel_status dsel_load_block_col(dsel_engine* e, int j, const double* host_col);
+/* Whole K in DataSpaceHessian / KBF payload order (n_sensors^2 blocks,
+ * block-row-major, hessian.hpp:17-84): loads every owned panel. */
+dsel_status dsel_load_k(dsel_engine* e, const double* host_k);
+/* Export block row j (same layout as dsel_load_block_row) of the CURRENT
+ * conditional covariance (= K before the first step); owner rank only. */
+dsel_status dsel_read_block_row(dsel_engine* e, int j, double* host_row);
+
+/* ---- synthetic K (SyntheticKAccess, kaccess.hpp:81-124) ----------------- */
+/* Host: V = (n_sensors*Nt) x rank, row-major, N(0,1) from the reference RNG
+ * stream (rng.hpp:15-50: mt19937_64 + Box-Muller). Bit-identical to
+ * SyntheticKAccess's v_. `threads` parallelises the transform (0 = auto). */
+dsel_status dsel_synthetic_v(int n_sensors, int n_steps, int rank, uint64_t seed, double* out,
+                             int threads);
+/* Device: generate this rank's panels of K = sigma^2 I + V V^T bit-exactly
+ * (sequential non-FMA dot products). V_host as produced above. */
+dsel_status dsel_gen_synthetic(dsel_engine* e, const double* v_host, int rank, double sigma);
+
+/* ---- selection (north-star (2)-(4)) ------------------------------------- */
+/* One round: gains of all remaining candidates, cross-rank argmax, panel
+ * broadcast from the owner, W = C[:,k] L_k^{-T}, C -= W W^T. Collective over
+ * the ranks. Returns DSEL_E_INFEASIBLE when round 1 has no feasible
+ * candidate; later all-infeasible rounds return DSEL_OK with
+ * chosen_index = -1 (partial selection, parallel.hpp:416-421). */
+dsel_status dsel_step(dsel_engine* e, dsel_step_info* info);
+/* Same, but the winner is forced to `sensor` (replay along a given sequence);
+ * the gain reported is that sensor's. */
+dsel_status dsel_step_forced(dsel_engine* e, int sensor, dsel_step_info* info);
+/* Run rounds until the budget (or infeasibility). n_done <- rounds done. */
+dsel_status dsel_run(dsel_engine* e, int* n_done);
+/* Raw gains of all currently remaining candidates OWNED by this rank,
+ * written to gains[sensor] (other entries untouched); -inf = infeasible. */
+dsel_status dsel_peek_gains(dsel_engine* e, double* gains_by_sensor);
+/* Rounds so far with device timings (syncs). Returns the row count. */
+int dsel_get_trace(dsel_engine* e, dsel_step_info* rows, int max_rows);
+/* Restore C = K and clear the selection (requires keep_pristine). */
+dsel_status dsel_reset(dsel_engine* e);
+/* Run statistics since create/reset (syncs). time_to_k_ms: device time from
+ * the first gain launch of round 1 to the D2H of the last round's winner
+ * (CUDA events on the compute stream, host gaps included). update_ms: sum of
+ * the Schur-update kernel spans; update_flops: their algorithmic flops
+ * (2*nt*rows*cols, full-square update). */
+typedef struct {
+  int rounds;
+  uint64_t kernel_launches;
+  uint64_t h2d_bytes;
+  uint64_t d2h_bytes;
+  uint64_t nccl_bytes;
+  double time_to_k_ms;
+  double update_ms;
+  double update_flops;
+} dsel_stats;
+dsel_status dsel_get_stats(dsel_engine* e, dsel_stats* st);
+/* L_S (SelectionState::factor): row-major, (k*Nt) x (k*Nt) active window with
+ * row stride `ld` (>= k*Nt), k = rounds done. Collective: every rank gets the
+ * full factor. Requires export_factor. */
+dsel_status dsel_export_factor(dsel_engine* e, double* host, int64_t ld);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DSEL_H_ */

@@ -1,0 +1,98 @@
+"""ctypes mirror of include/dsel.h (the C ABI of libdsel.so).
+
+The product path is libdsel.so: if it is missing this module raises at import
+time -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "lib", "libdsel.so")
+
+DSEL_OK = 0
+STATUS_NAMES = {0: "DSEL_OK", 1: "DSEL_E_INVALID", 2: "DSEL_E_RANGE", 3: "DSEL_E_INFEASIBLE",
+                4: "DSEL_E_CUDA", 5: "DSEL_E_NCCL", 6: "DSEL_E_OOM", 7: "DSEL_E_IO",
+                8: "DSEL_E_STATE"}
+
+# every entry point declared in include/dsel.h (tests check the exports)
+EXPORTS = ["dsel_abi_version", "dsel_nccl_unique_id", "dsel_create", "dsel_destroy",
+           "dsel_last_error", "dsel_sync", "dsel_device_bytes", "dsel_load_block_row",
+           "dsel_load_block_col", "dsel_load_k", "dsel_read_block_row", "dsel_synthetic_v",
+           "dsel_gen_synthetic", "dsel_step", "dsel_step_forced", "dsel_run", "dsel_peek_gains",
+           "dsel_get_trace", "dsel_reset", "dsel_get_stats", "dsel_export_factor"]
+
+
+class DselConfig(C.Structure):
+    _fields_ = [("n_sensors", C.c_int), ("n_steps", C.c_int), ("budget", C.c_int),
+                ("n_candidates", C.c_int), ("candidates", C.POINTER(C.c_int)),
+                ("device", C.c_int), ("world_size", C.c_int), ("rank", C.c_int),
+                ("nccl_id", C.c_void_p), ("storage", C.c_int), ("keep_pristine", C.c_int),
+                ("export_factor", C.c_int), ("near_tie_tau", C.c_double)]
+
+
+class DselStepInfo(C.Structure):
+    _fields_ = [("k", C.c_int), ("chosen_index", C.c_int), ("gain", C.c_double),
+                ("objective", C.c_double), ("runner_up", C.c_int),
+                ("runner_up_gain", C.c_double), ("near_tie", C.c_int),
+                ("n_evaluated", C.c_int), ("n_infeasible", C.c_int),
+                ("bytes_exchanged", C.c_uint64), ("ms_gain", C.c_double),
+                ("ms_exchange", C.c_double), ("ms_panel", C.c_double),
+                ("ms_update", C.c_double), ("ms_round", C.c_double),
+                ("update_flops", C.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class DselStats(C.Structure):
+    _fields_ = [("rounds", C.c_int), ("kernel_launches", C.c_uint64), ("h2d_bytes", C.c_uint64),
+                ("d2h_bytes", C.c_uint64), ("nccl_bytes", C.c_uint64),
+                ("time_to_k_ms", C.c_double), ("update_ms", C.c_double),
+                ("update_flops", C.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (the selection path has no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, ip, dp = C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_double)
+    L.dsel_abi_version.restype = C.c_int
+    L.dsel_nccl_unique_id.argtypes = [vp]
+    L.dsel_create.argtypes = [C.POINTER(DselConfig), C.POINTER(vp)]
+    L.dsel_destroy.argtypes = [vp]
+    L.dsel_destroy.restype = None
+    L.dsel_last_error.argtypes = [vp]
+    L.dsel_last_error.restype = C.c_char_p
+    L.dsel_sync.argtypes = [vp]
+    L.dsel_device_bytes.argtypes = [vp]
+    L.dsel_device_bytes.restype = C.c_uint64
+    L.dsel_load_block_row.argtypes = [vp, C.c_int, vp]
+    L.dsel_load_block_col.argtypes = [vp, C.c_int, vp]
+    L.dsel_load_k.argtypes = [vp, vp]
+    L.dsel_read_block_row.argtypes = [vp, C.c_int, vp]
+    L.dsel_synthetic_v.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, vp, C.c_int]
+    L.dsel_gen_synthetic.argtypes = [vp, vp, C.c_int, C.c_double]
+    L.dsel_step.argtypes = [vp, C.POINTER(DselStepInfo)]
+    L.dsel_step_forced.argtypes = [vp, C.c_int, C.POINTER(DselStepInfo)]
+    L.dsel_run.argtypes = [vp, ip]
+    L.dsel_peek_gains.argtypes = [vp, vp]
+    L.dsel_get_trace.argtypes = [vp, C.POINTER(DselStepInfo), C.c_int]
+    L.dsel_get_trace.restype = C.c_int
+    L.dsel_reset.argtypes = [vp]
+    L.dsel_export_factor.argtypes = [vp, vp, C.c_int64]
+    L.dsel_get_stats.argtypes = [vp, C.POINTER(DselStats)]
+    for name in EXPORTS:
+        if name not in ("dsel_destroy", "dsel_last_error", "dsel_device_bytes",
+                        "dsel_get_trace", "dsel_abi_version"):
+            getattr(L, name).restype = C.c_int
+    return L
+
+
+lib = _load()

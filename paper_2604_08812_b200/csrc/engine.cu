@@ -1,0 +1,958 @@
+// engine.cu -- per-GPU selection engine behind the C ABI (include/dsel.h).
+//
+// One engine per GPU (one process or thread per GPU). Candidates are owned
+// cyclically by position (p % world_size); every rank holds all candidate
+// rows of its candidates' block columns of the conditional covariance C.
+// Per round (north star (2)-(4)):
+//   gain kernel (batched chol + logdet) -> local top-2 argmax
+//   -> ncclAllGather(32 B/rank) -> identical host fold (reference tie rule)
+//   -> ncclBroadcast of the chosen conditional panel C[:,k] from its owner
+//   -> chol(C_kk), L_k^{-1}, W = C[live,k] L_k^{-T}  (DMMA)
+//   -> C[live, local live] -= W W^T                  (DMMA)
+// The reference computes the same gains left-looking per candidate
+// (selector.hpp:86-116); this is the right-looking Schur form of Alg. 1
+// with the conditional covariance kept resident.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "dsel.h"
+#include "kernels.cuh"
+
+using namespace dsel;
+
+namespace {
+
+thread_local std::string g_create_err;
+
+struct Fail {
+  dsel_status st;
+  std::string msg;
+};
+
+#define CU(x)                                                                          \
+  do {                                                                                 \
+    cudaError_t _e = (x);                                                              \
+    if (_e != cudaSuccess)                                                             \
+      throw Fail{DSEL_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(_e)};        \
+  } while (0)
+#define NC(x)                                                                          \
+  do {                                                                                 \
+    ncclResult_t _r = (x);                                                             \
+    if (_r != ncclSuccess)                                                             \
+      throw Fail{DSEL_E_NCCL, std::string(#x) + ": " + ncclGetErrorString(_r)};        \
+  } while (0)
+
+inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+template <class T>
+T* dmalloc(size_t count, uint64_t& total) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Fail{DSEL_E_OOM, "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed"};
+  }
+  total += count * sizeof(T);
+  return static_cast<T*>(p);
+}
+
+constexpr int kEv = 5;
+
+}  // namespace
+
+struct dsel_engine {
+  // ---- configuration ----
+  int nd = 0, nt = 0, budget = 0, G = 1, rank = 0, dev = 0;
+  int nc = 0;          // candidates
+  long long n = 0;     // nc * nt
+  int nloc = 0;        // local slots
+  int ldw = 0;         // W / Linv pitch
+  int eff_budget = 0;
+  bool keep = false, export_factor = false;
+  double tau = 1e-9;
+  std::vector<int> pos_sensor, sensor_pos, slot_sensor;
+
+  // ---- device state ----
+  cudaStream_t s = nullptr;
+  ncclComm_t comm = nullptr;
+  double *C = nullptr, *K0 = nullptr, *W = nullptr, *Pbuf = nullptr, *Lk = nullptr,
+         *Linv = nullptr, *Lscr = nullptr, *gains = nullptr, *hist = nullptr, *kgain = nullptr,
+         *stage = nullptr, *xbuf = nullptr;
+  int *status = nullptr, *kstatus = nullptr;
+  int *d_pos_sensor = nullptr, *d_slot_sensor = nullptr;
+  int* d_tab = nullptr;  // [row_pos nc | col_slot nloc | col_g nloc]
+  ArgRec *d_rec = nullptr, *d_recs = nullptr;
+  ArgRec* h_recs = nullptr;  // pinned
+  int* h_tab = nullptr;      // pinned
+  double* h_stage = nullptr;  // pinned bounce buffer for pageable ingest (one block row)
+  size_t stage_elems = 0;     // per device staging buffer (two of them)
+  int stage_flip = 0;
+  cudaStream_t cs = nullptr;  // copy stream (H2D ingest)
+  cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_scat[2] = {nullptr, nullptr};
+  uint64_t h2d_bytes = 0, d2h_bytes = 0, nccl_bytes = 0;
+  uint64_t launches = 0;  // kernels launched by the selection rounds
+  double update_flops = 0.0;
+  uint64_t dev_bytes = 0;
+  std::vector<cudaEvent_t> ev;  // kEv per round
+
+  // ---- selection state ----
+  std::vector<char> alive;     // by position
+  int n_alive = 0;
+  int n_rows_tab = 0, n_cols_tab = 0;  // sizes of the uploaded tables
+  std::vector<int> chosen;
+  std::vector<dsel_step_info> trace;
+  double objective = 0.0;
+  bool finished = false;
+  std::string err;
+
+  int* row_pos() { return d_tab; }
+  int* col_slot() { return d_tab + nc; }
+  int* col_g() { return d_tab + nc + nloc; }
+};
+
+namespace {
+
+void build_tables(dsel_engine* e) {
+  // compact global live list (ascending position) and local live list
+  int* rp = e->h_tab;
+  int* cs = e->h_tab + e->nc;
+  int* cg = e->h_tab + e->nc + e->nloc;
+  int R = 0, Rl = 0;
+  for (int p = 0; p < e->nc; ++p) {
+    if (!e->alive[p]) continue;
+    if (p % e->G == e->rank) {
+      cs[Rl] = p / e->G;
+      cg[Rl] = R;
+      ++Rl;
+    }
+    rp[R++] = p;
+  }
+  e->n_rows_tab = R;
+  e->n_cols_tab = Rl;
+  CU(cudaMemcpyAsync(e->d_tab, e->h_tab, sizeof(int) * (size_t)(e->nc + 2 * e->nloc),
+                     cudaMemcpyHostToDevice, e->s));
+}
+
+}  // namespace
+
+// Kernel-side helpers for the gain kernel batch description.
+namespace {
+__global__ void gain_tables_kernel(const int* col_slot, int n, int G, int rank, int nt,
+                                   const int* pos_sensor, int* src_col, int* src_row,
+                                   int* sensor) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  const int q = col_slot[b];
+  const int p = q * G + rank;
+  src_col[b] = q * nt;
+  src_row[b] = p * nt;
+  sensor[b] = pos_sensor[p];
+}
+
+__global__ void fixed_tables_kernel(int col, int row, int* src_col, int* src_row) {
+  src_col[0] = col;
+  src_row[0] = row;
+}
+
+// forced winner: record with that sensor's gain (if local & feasible)
+__global__ void pick_kernel(const double* gain, const int* status, const int* sensor, int n,
+                            int forced, ArgRec* out) {
+  if (threadIdx.x != 0) return;
+  ArgRec r;
+  r.g1 = -INFINITY;
+  r.g2 = -INFINITY;
+  r.s1 = -1;
+  r.s2 = -1;
+  r.n_eval = n;
+  r.n_inf = 0;
+  for (int i = 0; i < n; ++i) {
+    if (status[i] >= 0) {
+      ++r.n_inf;
+      continue;
+    }
+    if (sensor[i] == forced) {
+      r.g1 = gain[i];
+      r.s1 = forced;
+    }
+  }
+  *out = r;
+}
+
+__global__ void pack_factor_row_kernel(const double* hist_slot, int nt, int i_blocks,
+                                       double* out /* nt x (i_blocks*nt) row-major */) {
+  const long long n2 = (long long)nt * nt;
+  const long long total = n2 * i_blocks;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(e / n2);
+    const long long w = e - j * n2;
+    const int a = (int)(w / nt), b = (int)(w - (long long)a * nt);
+    out[(size_t)a * i_blocks * nt + (size_t)j * nt + b] = hist_slot[e];
+  }
+}
+}  // namespace
+
+namespace {
+
+// scratch int tables for the gain kernel batch: [src_col | src_row | sensor]
+struct GainTabs {
+  int* src_col;
+  int* src_row;
+  int* sensor;
+};
+
+// panel width of the gain kernel: two NB x mp panels must fit in 227 KB
+int chol_nb(int nt) { return nt <= 440 ? 32 : (nt <= 900 ? 16 : 8); }
+
+void launch_chol(const CholArgs& a, int n_batch, cudaStream_t s) {
+  const int nb = chol_nb(a.nt);
+  const size_t smem = (size_t)2 * nb * a.mp * sizeof(double);
+  if (nb == 32)
+    chol_logdet_kernel<32><<<n_batch, 256, smem, s>>>(a);
+  else if (nb == 16)
+    chol_logdet_kernel<16><<<n_batch, 256, smem, s>>>(a);
+  else
+    chol_logdet_kernel<8><<<n_batch, 256, smem, s>>>(a);
+}
+
+GainTabs gain_tabs(dsel_engine* e) {
+  int* base = reinterpret_cast<int*>(e->xbuf);
+  return {base, base + e->nloc + 1, base + 2 * (e->nloc + 1)};
+}
+
+void run_gain(dsel_engine* e, const int* slots, int n_batch) {
+  if (n_batch <= 0) return;
+  GainTabs t = gain_tabs(e);
+  gain_tables_kernel<<<(n_batch + 127) / 128, 128, 0, e->s>>>(
+      slots, n_batch, e->G, e->rank, e->nt, e->d_pos_sensor, t.src_col, t.src_row, t.sensor);
+  CU(cudaGetLastError());
+  CholArgs a;
+  a.src = e->C;
+  a.lds = e->n;
+  a.src_col = t.src_col;
+  a.src_row = t.src_row;
+  a.L = e->Lscr;
+  a.l_stride = (long long)e->nt * e->nt;
+  a.gain = e->gains;
+  a.status = e->status;
+  a.nt = e->nt;
+  a.n = n_batch;
+  a.mp = round_up(e->nt, 2);
+  launch_chol(a, n_batch, e->s);
+  CU(cudaGetLastError());
+  e->launches += 2;
+}
+
+void chol_winner(dsel_engine* e, const double* panel, long long ldp, int pos) {
+  // batch of one: block rows pos*nt of the panel, panel columns 0..nt
+  GainTabs t = gain_tabs(e);
+  int* fc = t.src_col + e->nloc;  // spare slot at the end of each table
+  int* fr = t.src_row + e->nloc;
+  fixed_tables_kernel<<<1, 1, 0, e->s>>>(0, pos * e->nt, fc, fr);
+  CholArgs a;
+  a.src = panel;
+  a.lds = ldp;
+  a.src_col = fc;
+  a.src_row = fr;
+  a.L = e->Lk;
+  a.l_stride = (long long)e->nt * e->nt;
+  a.gain = e->kgain;
+  a.status = e->kstatus;
+  a.nt = e->nt;
+  a.n = 1;
+  a.mp = round_up(e->nt, 2);
+  launch_chol(a, 1, e->s);
+  CU(cudaGetLastError());
+  e->launches += 2;
+}
+
+template <class K>
+void allow_smem(K kernel, int optin) {
+  cudaFuncAttributes fa{};
+  CU(cudaFuncGetAttributes(&fa, kernel));
+  CU(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          optin - (int)fa.sharedSizeBytes));
+}
+
+void set_smem_limits(int dev) {
+  // per device context; cheap, called from dsel_create on the engine's device
+  int optin = 0;
+  CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  allow_smem(chol_logdet_kernel<32>, optin);
+  allow_smem(chol_logdet_kernel<16>, optin);
+  allow_smem(chol_logdet_kernel<8>, optin);
+  allow_smem(schur_update_kernel<2>, optin);
+  allow_smem(schur_update_kernel<1>, optin);
+  allow_smem(panel_w_kernel<2>, optin);
+  allow_smem(panel_w_kernel<1>, optin);
+  allow_smem(trinv_kernel, optin);
+}
+
+void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
+  if (e->finished || (int)e->chosen.size() >= e->eff_budget)
+    throw Fail{DSEL_E_STATE, "selection already finished"};
+  CU(cudaSetDevice(e->dev));
+  const int round = (int)e->chosen.size();
+  const int nt = e->nt;
+  cudaEvent_t* ev = &e->ev[(size_t)round * kEv];
+  const bool last = round + 1 == e->eff_budget;
+
+  // ---- gains + local argmax ----
+  CU(cudaEventRecord(ev[0], e->s));
+  const int n_batch = e->n_cols_tab;
+  run_gain(e, e->col_slot(), n_batch);
+  GainTabs t = gain_tabs(e);
+  if (forced >= 0)
+    pick_kernel<<<1, 32, 0, e->s>>>(e->gains, e->status, t.sensor, n_batch, forced, e->d_rec);
+  else
+    argmax_kernel<<<1, 256, 0, e->s>>>(e->gains, e->status, t.sensor, n_batch, e->d_rec);
+  CU(cudaGetLastError());
+  e->launches += 1;
+  CU(cudaEventRecord(ev[1], e->s));
+
+  // ---- cross-rank argmax: 32 B per rank ----
+  uint64_t bytes = 0;
+  if (e->G > 1) {
+    NC(ncclAllGather(e->d_rec, e->d_recs, sizeof(ArgRec), ncclUint8, e->comm, e->s));
+    CU(cudaMemcpyAsync(e->h_recs, e->d_recs, sizeof(ArgRec) * e->G, cudaMemcpyDeviceToHost, e->s));
+    bytes += sizeof(ArgRec) * (uint64_t)e->G;
+  } else {
+    CU(cudaMemcpyAsync(e->h_recs, e->d_rec, sizeof(ArgRec), cudaMemcpyDeviceToHost, e->s));
+  }
+  CU(cudaEventRecord(ev[2], e->s));
+  e->d2h_bytes += sizeof(ArgRec) * (uint64_t)e->G;
+  CU(cudaStreamSynchronize(e->s));
+  // identical fold on every rank (reduce_argmax, parallel.hpp:61-74, top-2)
+  double g1 = -INFINITY, g2 = -INFINITY;
+  int s1 = -1, s2 = -1, n_eval = 0, n_inf = 0;
+  auto ins = [&](double d, int s) {
+    if (s < 0) return;
+    auto better = [](double d, int s, double bd, int bs) {
+      return d > bd || (d == bd && (bs < 0 || s < bs));
+    };
+    if (s1 < 0 || better(d, s, g1, s1)) {
+      g2 = g1;
+      s2 = s1;
+      g1 = d;
+      s1 = s;
+    } else if (s2 < 0 || better(d, s, g2, s2)) {
+      g2 = d;
+      s2 = s;
+    }
+  };
+  for (int r = 0; r < e->G; ++r) {
+    const ArgRec& rr = e->h_recs[r];
+    ins(rr.g1, rr.s1);
+    ins(rr.g2, rr.s2);
+    n_eval += rr.n_eval;
+    n_inf += rr.n_inf;
+  }
+  dsel_step_info row{};
+  row.k = round + 1;
+  row.n_evaluated = n_eval;
+  row.n_infeasible = n_inf;
+  if (s1 < 0) {
+    if (forced >= 0) throw Fail{DSEL_E_INVALID, "forced sensor is not a feasible remaining candidate"};
+    if (round == 0) throw Fail{DSEL_E_INFEASIBLE, "all remaining candidates infeasible in round 1"};
+    e->finished = true;
+    row.chosen_index = -1;
+    row.objective = e->objective;
+    for (int i = 2; i < kEv; ++i) CU(cudaEventRecord(ev[i], e->s));
+    e->trace.push_back(row);
+    if (info) *info = row;
+    return;
+  }
+  const int p = e->sensor_pos[s1];
+  const int owner = p % e->G;
+  const int q = p / e->G;
+
+  // ---- panel: broadcast C[:,k] from its owner; chol(C_kk); W ----
+  double* P = nullptr;
+  if (!last || e->export_factor) {
+    P = (owner == e->rank) ? e->C + (size_t)q * nt * e->n : e->Pbuf;
+    if (e->G > 1 && !last) {
+      NC(ncclBroadcast(P, P, (size_t)e->n * nt, ncclDouble, owner, e->comm, e->s));
+      bytes += (uint64_t)e->n * nt * sizeof(double) * (uint64_t)(e->G - 1);
+    }
+    if (!last || owner == e->rank) chol_winner(e, P, e->n, p);
+  }
+  e->alive[p] = 0;
+  e->n_alive -= 1;
+  build_tables(e);
+  const int R = e->n_rows_tab, Rl = e->n_cols_tab;
+  double flops = 0.0;
+  if (!last) {
+    const int tb = 256 / 32;
+    trinv_kernel<<<(e->ldw + tb - 1) / tb, 256, (size_t)tb * e->ldw * sizeof(double), e->s>>>(
+        e->Lk, nt, e->Linv, e->ldw);
+    CU(cudaGetLastError());
+    e->launches += 1;
+    if (R > 0) {
+      PanelArgs pa;
+      pa.P = P;
+      pa.ldp = e->n;
+      pa.Linv = e->Linv;
+      pa.ldl = e->ldw;
+      pa.W = e->W;
+      pa.ldw = e->ldw;
+      pa.row_pos = e->row_pos();
+      pa.nt = nt;
+      pa.n_rows = R * nt;
+      dim3 grid((pa.n_rows + pw::BR - 1) / pw::BR, (nt + pw::BN - 1) / pw::BN);
+      if (nt % 2 == 0)
+        panel_w_kernel<2><<<grid, pw::THREADS, pw::SMEM, e->s>>>(pa);
+      else
+        panel_w_kernel<1><<<grid, pw::THREADS, pw::SMEM, e->s>>>(pa);
+      CU(cudaGetLastError());
+      e->launches += 1;
+    }
+  }
+  if (e->export_factor) {
+    const long long n2 = (long long)nt * nt;
+    const long long slot_stride = (long long)e->eff_budget * n2;
+    if (!last && Rl > 0) {
+      dim3 grid((unsigned)std::min<long long>((n2 + 255) / 256, 64), Rl);
+      hist_copy_kernel<<<grid, 256, 0, e->s>>>(e->W, e->ldw, e->col_slot(), e->col_g(), Rl, nt,
+                                               e->hist, slot_stride, (long long)round * n2);
+      CU(cudaGetLastError());
+      e->launches += 1;
+    }
+    if (owner == e->rank) {
+      hist_diag_kernel<<<(unsigned)std::min<long long>((n2 + 255) / 256, 1024), 256, 0, e->s>>>(
+          e->Lk, nt, e->hist + (long long)q * slot_stride + (long long)round * n2);
+      CU(cudaGetLastError());
+      e->launches += 1;
+    }
+  }
+  CU(cudaEventRecord(ev[3], e->s));
+  if (!last && R > 0 && Rl > 0) {
+    UpdateArgs ua;
+    ua.C = e->C;
+    ua.ldc = e->n;
+    ua.W = e->W;
+    ua.ldw = e->ldw;
+    ua.row_pos = e->row_pos();
+    ua.col_slot = e->col_slot();
+    ua.col_g = e->col_g();
+    ua.nt = nt;
+    ua.n_rows = R * nt;
+    ua.n_cols = Rl * nt;
+    ua.n_row_tiles = (ua.n_rows + upd::BR - 1) / upd::BR;
+    ua.n_col_tiles = (ua.n_cols + upd::BC - 1) / upd::BC;
+    ua.group = 16;
+    const long long tiles = (long long)ua.n_row_tiles * ua.n_col_tiles;
+    if (nt % 2 == 0)
+      schur_update_kernel<2><<<(unsigned)tiles, upd::THREADS, upd::SMEM, e->s>>>(ua);
+    else
+      schur_update_kernel<1><<<(unsigned)tiles, upd::THREADS, upd::SMEM, e->s>>>(ua);
+    CU(cudaGetLastError());
+    e->launches += 1;
+    e->update_flops += 2.0 * nt * (double)(R * nt) * (double)(Rl * nt);
+    flops = 2.0 * nt * (double)ua.n_rows * (double)ua.n_cols;
+  }
+  CU(cudaEventRecord(ev[4], e->s));
+
+  e->chosen.push_back(s1);
+  e->objective += g1;
+  row.chosen_index = s1;
+  row.gain = g1;
+  row.objective = e->objective;
+  row.runner_up = s2;
+  row.runner_up_gain = g2;
+  row.near_tie = (s2 >= 0 && (g1 - g2) / std::max(std::fabs(g1), 1.0) < e->tau) ? 1 : 0;
+  row.bytes_exchanged = bytes;
+  e->nccl_bytes += bytes;
+  row.update_flops = flops;
+  e->trace.push_back(row);
+  if (info) *info = row;
+}
+
+dsel_status fail(dsel_engine* e, const Fail& f) {
+  if (e) e->err = f.msg;
+  else g_create_err = f.msg;
+  return f.st;
+}
+
+template <class F>
+dsel_status guard(dsel_engine* e, F&& f) {
+  try {
+    f();
+    return DSEL_OK;
+  } catch (const Fail& x) {
+    return fail(e, x);
+  } catch (const std::exception& ex) {
+    return fail(e, Fail{DSEL_E_INVALID, ex.what()});
+  }
+}
+
+void destroy_impl(dsel_engine* e) {
+  if (!e) return;
+  cudaSetDevice(e->dev);
+  if (e->s) cudaStreamSynchronize(e->s);
+  if (e->cs) cudaStreamSynchronize(e->cs);
+  for (auto ev : e->ev) cudaEventDestroy(ev);
+  double* dptr[] = {e->C, e->K0, e->W, e->Pbuf, e->Lk, e->Linv, e->Lscr, e->gains, e->hist,
+                    e->kgain, e->stage, e->xbuf};
+  for (double* d : dptr)
+    if (d) cudaFree(d);
+  int* iptr[] = {e->status, e->kstatus, e->d_pos_sensor, e->d_slot_sensor, e->d_tab};
+  for (int* d : iptr)
+    if (d) cudaFree(d);
+  if (e->d_rec) cudaFree(e->d_rec);
+  if (e->d_recs) cudaFree(e->d_recs);
+  if (e->h_recs) cudaFreeHost(e->h_recs);
+  if (e->h_tab) cudaFreeHost(e->h_tab);
+  if (e->h_stage) cudaFreeHost(e->h_stage);
+  if (e->comm) ncclCommDestroy(e->comm);
+  for (int b = 0; b < 2; ++b) {
+    if (e->ev_copy[b]) cudaEventDestroy(e->ev_copy[b]);
+    if (e->ev_scat[b]) cudaEventDestroy(e->ev_scat[b]);
+  }
+  if (e->cs) cudaStreamDestroy(e->cs);
+  if (e->s) cudaStreamDestroy(e->s);
+  delete e;
+}
+
+void create_impl(const dsel_config* cfg, dsel_engine** out) {
+  if (!cfg || !out) throw Fail{DSEL_E_INVALID, "null argument"};
+  if (cfg->n_sensors < 1 || cfg->n_steps < 1) throw Fail{DSEL_E_INVALID, "n_sensors and n_steps must be >= 1"};
+  if (cfg->budget < 0) throw Fail{DSEL_E_INVALID, "budget must be nonnegative"};
+  if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size)
+    throw Fail{DSEL_E_INVALID, "bad world_size/rank"};
+  if (cfg->storage == DSEL_STORAGE_STREAM)
+    throw Fail{DSEL_E_INVALID, "storage=stream (pinned-host panel streaming) is not available in this build"};
+  if (cfg->n_steps > 1024) throw Fail{DSEL_E_INVALID, "n_steps > 1024 is not supported by the gain kernel"};
+  auto* e = new dsel_engine();
+  try {
+    e->nd = cfg->n_sensors;
+    e->nt = cfg->n_steps;
+    e->budget = cfg->budget;
+    e->G = cfg->world_size;
+    e->rank = cfg->rank;
+    e->dev = cfg->device;
+    e->keep = cfg->keep_pristine != 0;
+    e->export_factor = cfg->export_factor != 0;
+    e->tau = cfg->near_tie_tau > 0 ? cfg->near_tie_tau : 1e-9;
+    // candidates (selector.hpp:142-151 check_candidates semantics)
+    e->sensor_pos.assign(e->nd, -1);
+    if (cfg->n_candidates > 0) {
+      if (!cfg->candidates) throw Fail{DSEL_E_INVALID, "candidates pointer is null"};
+      for (int i = 0; i < cfg->n_candidates; ++i) {
+        const int c = cfg->candidates[i];
+        if (c < 0 || c >= e->nd) throw Fail{DSEL_E_RANGE, "candidate index out of range"};
+        if (e->sensor_pos[c] >= 0) throw Fail{DSEL_E_INVALID, "duplicate candidate index"};
+        e->sensor_pos[c] = 0;
+      }
+      // position order = ascending sensor id (result-invariant, parallel.hpp:299-304)
+      for (int sidx = 0; sidx < e->nd; ++sidx)
+        if (e->sensor_pos[sidx] >= 0) {
+          e->sensor_pos[sidx] = (int)e->pos_sensor.size();
+          e->pos_sensor.push_back(sidx);
+        }
+    } else {
+      for (int sidx = 0; sidx < e->nd; ++sidx) {
+        e->sensor_pos[sidx] = sidx;
+        e->pos_sensor.push_back(sidx);
+      }
+    }
+    e->nc = (int)e->pos_sensor.size();
+    e->n = (long long)e->nc * e->nt;
+    if (e->n > (1LL << 31) - 1) throw Fail{DSEL_E_INVALID, "n_candidates*n_steps exceeds 2^31"};
+    e->nloc = e->nc > e->rank ? (e->nc - e->rank + e->G - 1) / e->G : 0;
+    for (int q = 0; q < e->nloc; ++q) e->slot_sensor.push_back(e->pos_sensor[q * e->G + e->rank]);
+    e->eff_budget = std::min(e->budget, e->nc);
+    e->ldw = round_up(e->nt, 16);
+    e->alive.assign(e->nc, 1);
+    e->n_alive = e->nc;
+
+    CU(cudaSetDevice(e->dev));
+    set_smem_limits(e->dev);
+    CU(cudaStreamCreateWithFlags(&e->s, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&e->cs, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      CU(cudaEventCreateWithFlags(&e->ev_copy[b], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&e->ev_scat[b], cudaEventDisableTiming));
+    }
+    uint64_t& tot = e->dev_bytes;
+    const size_t shard = (size_t)e->n * (size_t)e->nloc * e->nt;
+    e->C = dmalloc<double>(shard, tot);
+    if (e->keep) e->K0 = dmalloc<double>(shard, tot);
+    e->W = dmalloc<double>((size_t)e->n * e->ldw, tot);
+    if (e->G > 1) e->Pbuf = dmalloc<double>((size_t)e->n * e->nt, tot);
+    e->Lk = dmalloc<double>((size_t)e->nt * e->nt, tot);
+    e->Linv = dmalloc<double>((size_t)e->ldw * e->ldw, tot);
+    e->Lscr = dmalloc<double>((size_t)std::max(e->nloc, 1) * e->nt * e->nt, tot);
+    e->gains = dmalloc<double>(e->nloc + 1, tot);
+    e->status = dmalloc<int>(e->nloc + 1, tot);
+    e->kgain = dmalloc<double>(1, tot);
+    e->kstatus = dmalloc<int>(1, tot);
+    e->xbuf = dmalloc<double>((size_t)3 * (e->nloc + 1), tot);  // int tables, oversized
+    if (e->export_factor)
+      e->hist = dmalloc<double>((size_t)std::max(e->nloc, 1) * std::max(e->eff_budget, 1) *
+                                    e->nt * e->nt, tot);
+    e->d_pos_sensor = dmalloc<int>(e->nc, tot);
+    e->d_slot_sensor = dmalloc<int>(e->nloc + 1, tot);
+    e->d_tab = dmalloc<int>((size_t)e->nc + 2 * e->nloc, tot);
+    e->d_rec = dmalloc<ArgRec>(1, tot);
+    e->d_recs = dmalloc<ArgRec>(e->G, tot);
+    CU(cudaMallocHost(&e->h_recs, sizeof(ArgRec) * e->G));
+    CU(cudaMallocHost(&e->h_tab, sizeof(int) * ((size_t)e->nc + 2 * e->nloc + 1)));
+    CU(cudaMemsetAsync(e->W, 0, sizeof(double) * (size_t)e->n * e->ldw, e->s));
+    CU(cudaMemsetAsync(e->C, 0, sizeof(double) * shard, e->s));
+    CU(cudaMemcpyAsync(e->d_pos_sensor, e->pos_sensor.data(), sizeof(int) * e->nc,
+                       cudaMemcpyHostToDevice, e->s));
+    if (e->nloc)
+      CU(cudaMemcpyAsync(e->d_slot_sensor, e->slot_sensor.data(), sizeof(int) * e->nloc,
+                         cudaMemcpyHostToDevice, e->s));
+    e->ev.resize((size_t)std::max(e->eff_budget, 1) * kEv);
+    for (auto& x : e->ev) CU(cudaEventCreate(&x));
+    if (e->G > 1) {
+      if (!cfg->nccl_id) throw Fail{DSEL_E_INVALID, "world_size > 1 requires nccl_id"};
+      ncclUniqueId id;
+      std::memcpy(&id, cfg->nccl_id, sizeof(id));
+      NC(ncclCommInitRank(&e->comm, e->G, id, e->rank));
+    }
+    build_tables(e);
+    CU(cudaStreamSynchronize(e->s));
+  } catch (...) {
+    destroy_impl(e);
+    throw;
+  }
+  *out = e;
+}
+
+void ensure_stage(dsel_engine* e, size_t elems) {
+  if (e->stage_elems >= elems) return;
+  CU(cudaStreamSynchronize(e->s));
+  CU(cudaStreamSynchronize(e->cs));
+  if (e->stage) cudaFree(e->stage);
+  if (e->h_stage) cudaFreeHost(e->h_stage);
+  e->stage = nullptr;
+  e->h_stage = nullptr;
+  e->stage = dmalloc<double>(2 * elems, e->dev_bytes);
+  CU(cudaMallocHost(&e->h_stage, elems * sizeof(double)));
+  e->stage_elems = elems;
+}
+
+// Panel store ingest: H2D of one block row/column into device staging on the
+// copy stream (double-buffered, event-ordered), scatter into the panel on the
+// compute stream, so consecutive panels overlap copy and scatter.
+void load_panel(dsel_engine* e, int j, const double* host, bool as_column) {
+  if (j < 0 || j >= e->nd) throw Fail{DSEL_E_RANGE, "block index out of range"};
+  const int p = e->sensor_pos[j];
+  if (p < 0 || p % e->G != e->rank) return;
+  const int q = p / e->G;
+  const size_t elems = (size_t)e->nd * e->nt * e->nt;
+  CU(cudaSetDevice(e->dev));
+  ensure_stage(e, elems);
+  const int b = e->stage_flip;
+  e->stage_flip ^= 1;
+  double* buf = e->stage + (size_t)b * e->stage_elems;
+  CU(cudaStreamWaitEvent(e->cs, e->ev_scat[b], 0));
+  cudaPointerAttributes attr{};
+  const bool pinned = cudaPointerGetAttributes(&attr, host) == cudaSuccess &&
+                      attr.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  if (pinned) {
+    CU(cudaMemcpyAsync(buf, host, elems * sizeof(double), cudaMemcpyHostToDevice, e->cs));
+  } else {
+    // pageable source: bounce through the engine's pinned buffer
+    CU(cudaStreamSynchronize(e->cs));
+    std::memcpy(e->h_stage, host, elems * sizeof(double));
+    CU(cudaMemcpyAsync(buf, e->h_stage, elems * sizeof(double), cudaMemcpyHostToDevice, e->cs));
+  }
+  e->h2d_bytes += elems * sizeof(double);
+  CU(cudaEventRecord(e->ev_copy[b], e->cs));
+  CU(cudaStreamWaitEvent(e->s, e->ev_copy[b], 0));
+  double* panel = e->C + (size_t)q * e->nt * e->n;
+  const long long total = (long long)e->nc * e->nt * e->nt;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
+  if (as_column)
+    scatter_block_col_kernel<<<blocks, 256, 0, e->s>>>(buf, e->nt, e->d_pos_sensor, e->nc,
+                                                       panel, e->n);
+  else
+    scatter_block_row_kernel<<<blocks, 256, 0, e->s>>>(buf, e->nt, e->d_pos_sensor, e->nc,
+                                                       panel, e->n);
+  CU(cudaGetLastError());
+  CU(cudaEventRecord(e->ev_scat[b], e->s));
+  if (e->keep)
+    CU(cudaMemcpyAsync(e->K0 + (size_t)q * e->nt * e->n, panel, sizeof(double) * e->n * e->nt,
+                       cudaMemcpyDeviceToDevice, e->s));
+}
+
+}  // namespace
+
+// ========================================================================== //
+// C ABI                                                                      //
+// ========================================================================== //
+extern "C" {
+
+int dsel_abi_version(void) { return DSEL_ABI_VERSION; }
+
+dsel_status dsel_nccl_unique_id(void* out128) {
+  if (!out128) return DSEL_E_INVALID;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return DSEL_E_NCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(out128, &id, sizeof(id));
+  return DSEL_OK;
+}
+
+dsel_status dsel_create(const dsel_config* cfg, dsel_engine** out) {
+  try {
+    create_impl(cfg, out);
+    return DSEL_OK;
+  } catch (const Fail& f) {
+    g_create_err = f.msg;
+    return f.st;
+  } catch (const std::exception& ex) {
+    g_create_err = ex.what();
+    return DSEL_E_INVALID;
+  }
+}
+
+void dsel_destroy(dsel_engine* e) { destroy_impl(e); }
+
+const char* dsel_last_error(const dsel_engine* e) {
+  return e ? e->err.c_str() : g_create_err.c_str();
+}
+
+uint64_t dsel_device_bytes(const dsel_engine* e) { return e ? e->dev_bytes : 0; }
+
+dsel_status dsel_sync(dsel_engine* e) {
+  return guard(e, [&] {
+    CU(cudaSetDevice(e->dev));
+    CU(cudaStreamSynchronize(e->s));
+  });
+}
+
+dsel_status dsel_load_block_row(dsel_engine* e, int j, const double* host_row) {
+  return guard(e, [&] { load_panel(e, j, host_row, false); });
+}
+
+dsel_status dsel_load_block_col(dsel_engine* e, int j, const double* host_col) {
+  return guard(e, [&] { load_panel(e, j, host_col, true); });
+}
+
+dsel_status dsel_load_k(dsel_engine* e, const double* host_k) {
+  return guard(e, [&] {
+    const size_t row = (size_t)e->nd * e->nt * e->nt;
+    for (int q = 0; q < e->nloc; ++q) {
+      const int sidx = e->slot_sensor[q];
+      load_panel(e, sidx, host_k + (size_t)sidx * row, false);
+    }
+    CU(cudaStreamSynchronize(e->s));
+  });
+}
+
+dsel_status dsel_read_block_row(dsel_engine* e, int j, double* host_row) {
+  return guard(e, [&] {
+    if (j < 0 || j >= e->nd) throw Fail{DSEL_E_RANGE, "block index out of range"};
+    const int p = e->sensor_pos[j];
+    if (p < 0 || p % e->G != e->rank) throw Fail{DSEL_E_RANGE, "block row not owned by this rank"};
+    const int q = p / e->G;
+    const size_t elems = (size_t)e->nd * e->nt * e->nt;
+    CU(cudaSetDevice(e->dev));
+    ensure_stage(e, elems);
+    CU(cudaMemsetAsync(e->stage, 0, elems * sizeof(double), e->s));
+    const long long total = (long long)e->nc * e->nt * e->nt;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
+    gather_block_row_kernel<<<blocks, 256, 0, e->s>>>(e->C + (size_t)q * e->nt * e->n, e->n,
+                                                      e->nt, e->d_pos_sensor, e->nc, e->stage);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(e->h_stage, e->stage, elems * sizeof(double), cudaMemcpyDeviceToHost, e->s));
+    CU(cudaStreamSynchronize(e->s));
+    std::memcpy(host_row, e->h_stage, elems * sizeof(double));
+  });
+}
+
+dsel_status dsel_gen_synthetic(dsel_engine* e, const double* v_host, int rank, double sigma) {
+  return guard(e, [&] {
+    if (rank < 1 || !v_host) throw Fail{DSEL_E_INVALID, "bad synthetic rank / V"};
+    CU(cudaSetDevice(e->dev));
+    const size_t vel = (size_t)e->nd * e->nt * rank;
+    uint64_t dummy = 0;
+    double* V = dmalloc<double>(vel, dummy);
+    cudaError_t ce = cudaMemcpy(V, v_host, vel * sizeof(double), cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess && e->nloc > 0) {
+      GenArgs g;
+      g.V = V;
+      g.rank = rank;
+      g.noise2 = sigma * sigma;  // kaccess.hpp:88
+      g.nt = e->nt;
+      g.row_sensor = e->d_pos_sensor;
+      g.n_rows = (int)e->n;
+      g.col_sensor = e->d_slot_sensor;
+      g.n_cols = e->nloc * e->nt;
+      g.C = e->C;
+      g.ldc = e->n;
+      dim3 grid((g.n_rows + gen::BM - 1) / gen::BM, (g.n_cols + gen::BN - 1) / gen::BN);
+      synth_panel_kernel<<<grid, gen::THREADS, 0, e->s>>>(g);
+      ce = cudaGetLastError();
+      if (ce == cudaSuccess) ce = cudaStreamSynchronize(e->s);
+    }
+    cudaFree(V);
+    if (ce != cudaSuccess) throw Fail{DSEL_E_CUDA, std::string("synthetic K: ") + cudaGetErrorString(ce)};
+    if (e->keep)
+      CU(cudaMemcpyAsync(e->K0, e->C, sizeof(double) * e->n * e->nloc * e->nt,
+                         cudaMemcpyDeviceToDevice, e->s));
+    CU(cudaStreamSynchronize(e->s));
+  });
+}
+
+dsel_status dsel_step(dsel_engine* e, dsel_step_info* info) {
+  return guard(e, [&] { step_impl(e, -1, info); });
+}
+
+dsel_status dsel_step_forced(dsel_engine* e, int sensor, dsel_step_info* info) {
+  return guard(e, [&] {
+    if (sensor < 0 || sensor >= e->nd || e->sensor_pos[sensor] < 0 ||
+        !e->alive[e->sensor_pos[sensor]])
+      throw Fail{DSEL_E_RANGE, "forced sensor is not a remaining candidate"};
+    step_impl(e, sensor, info);
+  });
+}
+
+dsel_status dsel_run(dsel_engine* e, int* n_done) {
+  return guard(e, [&] {
+    while (!e->finished && (int)e->chosen.size() < e->eff_budget) step_impl(e, -1, nullptr);
+    if (n_done) *n_done = (int)e->chosen.size();
+  });
+}
+
+dsel_status dsel_peek_gains(dsel_engine* e, double* gains_by_sensor) {
+  return guard(e, [&] {
+    CU(cudaSetDevice(e->dev));
+    const int n_batch = e->n_cols_tab;
+    run_gain(e, e->col_slot(), n_batch);
+    std::vector<double> g(n_batch);
+    std::vector<int> sens(n_batch);
+    GainTabs t = gain_tabs(e);
+    if (n_batch) {
+      CU(cudaMemcpyAsync(g.data(), e->gains, sizeof(double) * n_batch, cudaMemcpyDeviceToHost, e->s));
+      CU(cudaMemcpyAsync(sens.data(), t.sensor, sizeof(int) * n_batch, cudaMemcpyDeviceToHost, e->s));
+    }
+    CU(cudaStreamSynchronize(e->s));
+    for (int i = 0; i < n_batch; ++i) gains_by_sensor[sens[i]] = g[i];
+  });
+}
+
+int dsel_get_trace(dsel_engine* e, dsel_step_info* rows, int max_rows) {
+  if (!e) return -1;
+  try {
+    CU(cudaSetDevice(e->dev));
+    CU(cudaStreamSynchronize(e->s));
+    const int n = std::min<int>((int)e->trace.size(), max_rows);
+    for (int i = 0; i < n; ++i) {
+      dsel_step_info r = e->trace[i];
+      cudaEvent_t* ev = &e->ev[(size_t)i * kEv];
+      float a = 0, b = 0, c = 0, d = 0, tot = 0;
+      CU(cudaEventElapsedTime(&a, ev[0], ev[1]));
+      CU(cudaEventElapsedTime(&b, ev[1], ev[2]));
+      CU(cudaEventElapsedTime(&c, ev[2], ev[3]));
+      CU(cudaEventElapsedTime(&d, ev[3], ev[4]));
+      CU(cudaEventElapsedTime(&tot, ev[0], ev[4]));
+      r.ms_gain = a;
+      r.ms_exchange = b;
+      r.ms_panel = c;
+      r.ms_update = d;
+      r.ms_round = tot;
+      rows[i] = r;
+    }
+    return n;
+  } catch (const Fail& f) {
+    e->err = f.msg;
+    return -1;
+  }
+}
+
+dsel_status dsel_reset(dsel_engine* e) {
+  return guard(e, [&] {
+    if (!e->keep) throw Fail{DSEL_E_STATE, "dsel_reset requires keep_pristine"};
+    CU(cudaSetDevice(e->dev));
+    CU(cudaMemcpyAsync(e->C, e->K0, sizeof(double) * e->n * e->nloc * e->nt,
+                       cudaMemcpyDeviceToDevice, e->s));
+    e->alive.assign(e->nc, 1);
+    e->n_alive = e->nc;
+    e->chosen.clear();
+    e->trace.clear();
+    e->objective = 0.0;
+    e->finished = false;
+    e->launches = 0;
+    e->update_flops = 0.0;
+    e->h2d_bytes = e->d2h_bytes = e->nccl_bytes = 0;
+    build_tables(e);
+    CU(cudaStreamSynchronize(e->s));
+  });
+}
+
+dsel_status dsel_get_stats(dsel_engine* e, dsel_stats* st) {
+  return guard(e, [&] {
+    if (!st) throw Fail{DSEL_E_INVALID, "null stats"};
+    CU(cudaSetDevice(e->dev));
+    CU(cudaStreamSynchronize(e->s));
+    dsel_stats r{};
+    r.rounds = (int)e->trace.size();
+    r.kernel_launches = e->launches;
+    r.h2d_bytes = e->h2d_bytes;
+    r.d2h_bytes = e->d2h_bytes;
+    r.nccl_bytes = e->nccl_bytes;
+    r.update_flops = e->update_flops;
+    if (r.rounds > 0) {
+      float ms = 0;
+      // first gain launch -> winner of the last round on the host (its D2H)
+      CU(cudaEventElapsedTime(&ms, e->ev[0], e->ev[(size_t)(r.rounds - 1) * kEv + 2]));
+      r.time_to_k_ms = ms;
+      double upd = 0.0;
+      for (int i = 0; i < r.rounds; ++i) {
+        float u = 0;
+        CU(cudaEventElapsedTime(&u, e->ev[(size_t)i * kEv + 3], e->ev[(size_t)i * kEv + 4]));
+        upd += u;
+      }
+      r.update_ms = upd;
+    }
+    *st = r;
+  });
+}
+
+dsel_status dsel_export_factor(dsel_engine* e, double* host, int64_t ld) {
+  return guard(e, [&] {
+    if (!e->export_factor) throw Fail{DSEL_E_STATE, "engine created without export_factor"};
+    const int k = (int)e->chosen.size();
+    const int nt = e->nt;
+    if (ld < (int64_t)k * nt) throw Fail{DSEL_E_INVALID, "ld smaller than k*n_steps"};
+    CU(cudaSetDevice(e->dev));
+    const long long n2 = (long long)nt * nt;
+    const long long slot_stride = (long long)e->eff_budget * n2;
+    ensure_stage(e, (size_t)nt * std::max(k, 1) * nt);
+    for (int i = 0; i < k; ++i) {
+      const int p = e->sensor_pos[e->chosen[i]];
+      const int owner = p % e->G, q = p / e->G;
+      const long long total = n2 * (i + 1);
+      if (owner == e->rank) {
+        pack_factor_row_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 2048), 256, 0,
+                                 e->s>>>(e->hist + q * slot_stride, nt, i + 1, e->stage);
+        CU(cudaGetLastError());
+      }
+      if (e->G > 1) NC(ncclBroadcast(e->stage, e->stage, (size_t)total, ncclDouble, owner, e->comm, e->s));
+      CU(cudaMemcpyAsync(e->h_stage, e->stage, sizeof(double) * total, cudaMemcpyDeviceToHost, e->s));
+      CU(cudaStreamSynchronize(e->s));
+      for (int a = 0; a < nt; ++a) {
+        double* dst = host + ((int64_t)i * nt + a) * ld;
+        std::memcpy(dst, e->h_stage + (size_t)a * (i + 1) * nt, sizeof(double) * (size_t)(i + 1) * nt);
+        std::fill(dst + (size_t)(i + 1) * nt, dst + (size_t)k * nt, 0.0);
+      }
+    }
+  });
+}
+
+}  // extern "C"

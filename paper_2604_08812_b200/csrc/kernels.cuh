@@ -1,0 +1,729 @@
+// kernels.cuh -- sm_100a kernels of the greedy D-optimal selection hot path.
+//
+// Data layout in HBM (per rank):
+//   C      conditional covariance, candidate space, column-major shard:
+//          n = n_cand*nt rows (all candidates, position order), n_loc*nt
+//          columns (this rank's candidates, cyclic by position). Element
+//          (row, local col) at C[col*ldc + row], ldc = n.
+//   W      compact conditional panel for the step, row-major (R*nt) x ldw,
+//          ldw = nt rounded up to 16, zero in the pad columns.
+//   L      per-candidate Cholesky scratch, column-major nt x nt.
+//
+// FP64 everywhere. The tensor-core work (Schur update, panel TRSM) is
+// mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4, the only FP64 tensor-core path on
+// sm_100a (tcgen05 has no f64 kind). Operands are staged in shared memory
+// with cp.async multi-stage pipelines.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dsel {
+
+// ------------------------------------------------------------------------ //
+// PTX helpers                                                               //
+// ------------------------------------------------------------------------ //
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// ------------------------------------------------------------------------ //
+// Rank-nt Schur update: C[rows, local cols] -= W[rows] * W[cols]^T          //
+// (north-star (2); replaces the per-candidate forward substitution +       //
+// schur_complement of linalg.hpp:39-114 by one right-looking update).     //
+// ------------------------------------------------------------------------ //
+namespace upd {
+constexpr int BR = 128;       // compact rows per CTA tile (r-side)
+constexpr int BC = 64;        // local compact columns per CTA tile (c-side)
+constexpr int KC = 16;        // k-chunk per pipeline stage
+constexpr int LDK = KC + 4;   // smem row pitch (doubles): conflict-free fragment reads
+constexpr int STAGES = 3;
+constexpr int THREADS = 256;
+constexpr size_t SMEM = (size_t)STAGES * (BR + BC) * LDK * sizeof(double) +
+                        BC * sizeof(long long) + (BR + BC) * sizeof(int);
+}  // namespace upd
+
+struct UpdateArgs {
+  double* C;            // local shard, column-major
+  long long ldc;        // = n
+  const double* W;      // compact rows, row-major
+  int ldw;              // multiple of 16
+  const int* row_pos;   // compact global block g -> candidate position p
+  const int* col_slot;  // local compact block h -> local slot q
+  const int* col_g;     // local compact block h -> compact global block g
+  int nt;
+  int n_rows;           // R * nt
+  int n_cols;           // R_loc * nt
+  int n_row_tiles, n_col_tiles, group;
+};
+
+template <int VEC>
+__global__ void __launch_bounds__(upd::THREADS, 2) schur_update_kernel(UpdateArgs a) {
+  using namespace upd;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sR = reinterpret_cast<double*>(smem_raw);          // [STAGES][BR][LDK]
+  double* sC = sR + STAGES * BR * LDK;                        // [STAGES][BC][LDK]
+  long long* colbase = reinterpret_cast<long long*>(sC + STAGES * BC * LDK);  // [BC]
+  int* rowphys = reinterpret_cast<int*>(colbase + BC);        // [BR]
+  int* cwrow = rowphys + BR;                                  // [BC]
+
+  // grouped rasterization: GROUP column tiles sweep all row tiles together
+  // so their W rows stay L2-resident while the row-side W streams.
+  const int tile = blockIdx.x;
+  const int gsz = a.group * a.n_row_tiles;
+  const int grp = tile / gsz;
+  const int within = tile - grp * gsz;
+  const int ct0 = grp * a.group;
+  const int gw = min(a.group, a.n_col_tiles - ct0);
+  const int rt = within / gw;
+  const int ct = ct0 + within % gw;
+  const int r0 = rt * BR, c0 = ct * BC;
+  const int tid = threadIdx.x;
+  const int nt = a.nt;
+
+  for (int i = tid; i < BR; i += THREADS) {
+    const int r = r0 + i;
+    if (r < a.n_rows) {
+      const int blk = r / nt;
+      rowphys[i] = a.row_pos[blk] * nt + (r - blk * nt);
+    } else {
+      rowphys[i] = -1;
+    }
+  }
+  for (int i = tid; i < BC; i += THREADS) {
+    const int c = c0 + i;
+    if (c < a.n_cols) {
+      const int blk = c / nt;
+      const int off = c - blk * nt;
+      colbase[i] = (long long)(a.col_slot[blk] * nt + off) * a.ldc;
+      cwrow[i] = a.col_g[blk] * nt + off;
+    } else {
+      colbase[i] = -1;
+      cwrow[i] = -1;
+    }
+  }
+  __syncthreads();
+
+  const int n_k = a.ldw / KC;
+  auto load_stage = [&](int stage, int kc) {
+    double* dR = sR + stage * BR * LDK;
+    double* dC = sC + stage * BC * LDK;
+    constexpr int CPR = KC / 2;  // 16-byte chunks per row
+    for (int idx = tid; idx < (BR + BC) * CPR; idx += THREADS) {
+      const int row = idx / CPR;
+      const int ch = idx - row * CPR;
+      if (row < BR) {
+        const int r = r0 + row;
+        const bool ok = r < a.n_rows;
+        const double* src = a.W + (size_t)(ok ? r : 0) * a.ldw + kc + ch * 2;
+        cp_async16(dR + row * LDK + ch * 2, src, ok);
+      } else {
+        const int cr = row - BR;
+        const int wr = cwrow[cr];
+        const bool ok = wr >= 0;
+        const double* src = a.W + (size_t)(ok ? wr : 0) * a.ldw + kc + ch * 2;
+        cp_async16(dC + cr * LDK + ch * 2, src, ok);
+      }
+    }
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < n_k) load_stage(s, s * KC);
+    cp_async_commit();
+  }
+
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = (warp & 3) * 32;   // r-side offset of this warp
+  const int wc = (warp >> 2) * 32;  // c-side offset of this warp
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int kb = 0; kb < n_k; ++kb) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kb + STAGES - 1;
+      if (nk < n_k) load_stage(nk % STAGES, nk * KC);
+      cp_async_commit();
+    }
+    const double* tR = sR + (kb % STAGES) * BR * LDK;
+    const double* tC = sC + (kb % STAGES) * BC * LDK;
+#pragma unroll
+    for (int k4 = 0; k4 < KC / 4; ++k4) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) fa[i] = tC[(wc + i * 8 + g) * LDK + k4 * 4 + t];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) fb[j] = tR[(wr + j * 8 + g) * LDK + k4 * 4 + t];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j], fa[i], fb[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue: acc[i][j] = (W W^T)[c][r], [r], [r+1]; C[r, c] -= acc
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int cl = wc + i * 8 + g;
+    const long long cb = colbase[cl];
+    if (cb < 0) continue;
+    double* col = a.C + cb;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int rl = wr + j * 8 + 2 * t;
+      const int p0 = rowphys[rl];
+      if (p0 < 0) continue;
+      if (VEC == 2) {
+        double2* ptr = reinterpret_cast<double2*>(col + p0);
+        double2 v = *ptr;
+        v.x -= acc[i][j][0];
+        v.y -= acc[i][j][1];
+        *ptr = v;
+      } else {
+        col[p0] -= acc[i][j][0];
+        const int p1 = rowphys[rl + 1];
+        if (p1 >= 0) col[p1] -= acc[i][j][1];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------ //
+// Conditional panel: W[r, :] = P[prow(r), :] * Linv^T (compact live rows).  //
+// W = C[:,k] L_k^{-T}, so C -= W W^T is C[:,J] -= C[:,k] S_k^{-1} C[k,J].   //
+// ------------------------------------------------------------------------ //
+namespace pw {
+constexpr int BR = 128;
+constexpr int BN = 64;
+constexpr int KC = 16;
+constexpr int LDA = BR + 4;  // sA is [KC][LDA] (k-major, r contiguous)
+constexpr int LDB = KC + 4;  // sB is [BN][LDB]
+constexpr int STAGES = 3;
+constexpr int THREADS = 256;
+constexpr size_t SMEM = (size_t)STAGES * (KC * LDA + BN * LDB) * sizeof(double) + BR * sizeof(int);
+}  // namespace pw
+
+struct PanelArgs {
+  const double* P;      // panel, column-major, element (row, m) at P[m*ldp + row]
+  long long ldp;
+  const double* Linv;   // row-major [c][m], ld = ldl, zero above the diagonal and in pads
+  int ldl;
+  double* W;            // out, row-major, ld = ldw
+  int ldw;
+  const int* row_pos;   // compact block -> position
+  int nt;
+  int n_rows;           // R * nt
+};
+
+template <int VEC>
+__global__ void __launch_bounds__(pw::THREADS, 2) panel_w_kernel(PanelArgs a) {
+  using namespace pw;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sA = reinterpret_cast<double*>(smem_raw);  // [STAGES][KC][LDA]
+  double* sB = sA + STAGES * KC * LDA;                // [STAGES][BN][LDB]
+  int* rowphys = reinterpret_cast<int*>(sB + STAGES * BN * LDB);
+  const int tid = threadIdx.x;
+  const int r0 = blockIdx.x * BR, c0 = blockIdx.y * BN;
+  const int nt = a.nt;
+  for (int i = tid; i < BR; i += THREADS) {
+    const int r = r0 + i;
+    if (r < a.n_rows) {
+      const int blk = r / nt;
+      rowphys[i] = a.row_pos[blk] * nt + (r - blk * nt);
+    } else {
+      rowphys[i] = -1;
+    }
+  }
+  __syncthreads();
+  // Linv is lower triangular: columns [c0, c0+BN) only need m < c0+BN.
+  const int k_end = min(a.ldl, ((min(nt, c0 + BN) + KC - 1) / KC) * KC);
+  const int n_k = k_end / KC;
+
+  auto load_stage = [&](int stage, int kc) {
+    double* dA = sA + stage * KC * LDA;
+    double* dB = sB + stage * BN * LDB;
+    if (VEC == 2) {
+      for (int idx = tid; idx < KC * (BR / 2); idx += THREADS) {
+        const int k = idx / (BR / 2);
+        const int rr = (idx - k * (BR / 2)) * 2;
+        const int pr = rowphys[rr];
+        const bool ok = pr >= 0 && kc + k < nt;
+        const double* src = a.P + (ok ? (size_t)(kc + k) * a.ldp + pr : 0);
+        cp_async16(dA + k * LDA + rr, src, ok);
+      }
+    } else {
+      for (int idx = tid; idx < KC * BR; idx += THREADS) {
+        const int k = idx / BR;
+        const int rr = idx - k * BR;
+        const int pr = rowphys[rr];
+        const bool ok = pr >= 0 && kc + k < nt;
+        const double* src = a.P + (ok ? (size_t)(kc + k) * a.ldp + pr : 0);
+        cp_async8(dA + k * LDA + rr, src, ok);
+      }
+    }
+    for (int idx = tid; idx < BN * (KC / 2); idx += THREADS) {
+      const int c = idx / (KC / 2);
+      const int ch = idx - c * (KC / 2);
+      const bool ok = c0 + c < a.ldl;
+      const double* src = a.Linv + (ok ? (size_t)(c0 + c) * a.ldl + kc + ch * 2 : 0);
+      cp_async16(dB + c * LDB + ch * 2, src, ok);
+    }
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < n_k) load_stage(s, s * KC);
+    cp_async_commit();
+  }
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = (warp & 3) * 32;
+  const int wc = (warp >> 2) * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int kb = 0; kb < n_k; ++kb) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kb + STAGES - 1;
+      if (nk < n_k) load_stage(nk % STAGES, nk * KC);
+      cp_async_commit();
+    }
+    const double* tA = sA + (kb % STAGES) * KC * LDA;
+    const double* tB = sB + (kb % STAGES) * BN * LDB;
+#pragma unroll
+    for (int k4 = 0; k4 < KC / 4; ++k4) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) fa[i] = tA[(k4 * 4 + t) * LDA + wr + i * 8 + g];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) fb[j] = tB[(wc + j * 8 + g) * LDB + k4 * 4 + t];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j], fa[i], fb[j]);
+    }
+  }
+  cp_async_wait<0>();
+  // acc[i][j] = W[r = wr+8i+g][c = wc+8j+2t, +1]
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = r0 + wr + i * 8 + g;
+    if (r >= a.n_rows) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = c0 + wc + j * 8 + 2 * t;
+      if (c < nt) {
+        double2 v;
+        v.x = acc[i][j][0];
+        v.y = c + 1 < nt ? acc[i][j][1] : 0.0;
+        *reinterpret_cast<double2*>(a.W + (size_t)r * a.ldw + c) = v;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------ //
+// Gain kernel: batched nt x nt Cholesky + log-determinant (north-star (3)). //
+// One CTA per candidate; left-looking by NB-wide column panels held in     //
+// shared memory, previous factor columns staged from an L2-resident       //
+// scratch. Mirrors cholesky_in_place + logdet_from_factor                  //
+// (linalg.hpp:16-35, :117-128): pivot <= 0 or nonfinite -> infeasible.    //
+// ------------------------------------------------------------------------ //
+struct CholArgs {
+  const double* src;        // C base (column-major, ld = lds)
+  long long lds;
+  const int* src_col;       // per batch entry: first column (local) of the block
+  const int* src_row;       // per batch entry: first row of the block
+  double* L;                // scratch, column-major nt x nt per batch entry
+  long long l_stride;       // doubles between batch entries of L
+  double* gain;             // out: 2*sum(log diag) or -inf when infeasible
+  int* status;              // out: -1 ok, else failing pivot index
+  int nt;
+  int n;                    // batch size
+  int mp;                   // smem pitch (>= nt)
+};
+
+template <int NB>
+__global__ void __launch_bounds__(256) chol_logdet_kernel(CholArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int b = blockIdx.x;
+  if (b >= a.n) return;
+  const int nt = a.nt, mp = a.mp;
+  double* S = reinterpret_cast<double*>(smem_raw);  // [NB][mp] panel, column-major
+  double* Lc = S + NB * mp;                         // [NB][mp] staged factor columns
+  __shared__ double s_logsum;
+  __shared__ int s_fail;
+  const int tid = threadIdx.x;
+  const double* src = a.src + (size_t)a.src_col[b] * a.lds + a.src_row[b];
+  double* L = a.L + (size_t)b * a.l_stride;
+  if (tid == 0) {
+    s_logsum = 0.0;
+    s_fail = -1;
+  }
+  for (int J0 = 0; J0 < nt; J0 += NB) {
+    const int nb = min(NB, nt - J0);
+    const int m = nt - J0;
+    // load panel rows J0..nt, cols J0..J0+nb
+    for (int j = 0; j < nb; ++j)
+      for (int i = tid; i < m; i += blockDim.x) S[j * mp + i] = src[(size_t)(J0 + j) * a.lds + J0 + i];
+    // left-looking update with previous factor columns
+    for (int kk = 0; kk < J0; kk += NB) {
+      const int kw = min(NB, J0 - kk);
+      __syncthreads();
+      for (int c = 0; c < kw; ++c)
+        for (int i = tid; i < m; i += blockDim.x) Lc[c * mp + i] = L[(size_t)(kk + c) * nt + J0 + i];
+      __syncthreads();
+      for (int i = tid; i < m; i += blockDim.x) {
+        double acc[NB];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) acc[j] = 0.0;
+        for (int c = 0; c < kw; ++c) {
+          const double x = Lc[c * mp + i];
+#pragma unroll
+          for (int j = 0; j < NB; ++j) acc[j] += x * Lc[c * mp + j];
+        }
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          if (j < nb) S[j * mp + i] -= acc[j];
+      }
+    }
+    __syncthreads();
+    // factor the panel: unblocked right-looking over its nb columns
+    for (int j = 0; j < nb; ++j) {
+      const double piv = S[j * mp + j];
+      const bool bad = !(piv > 0.0) || !isfinite(piv);
+      if (bad) {
+        if (tid == 0) s_fail = J0 + j;
+        break;
+      }
+      const double d = sqrt(piv);
+      double lij[4];
+      int cnt = 0;
+      for (int i = j + 1 + tid; i < m; i += blockDim.x) lij[cnt++ & 3] = S[j * mp + i] / d;
+      __syncthreads();
+      cnt = 0;
+      for (int i = j + 1 + tid; i < m; i += blockDim.x) S[j * mp + i] = lij[cnt++ & 3];
+      if (tid == 0) {
+        S[j * mp + j] = d;
+        s_logsum += log(d);
+      }
+      __syncthreads();
+      for (int i = j + 1 + tid; i < m; i += blockDim.x) {
+        const double li = S[j * mp + i];
+        const int cmax = min(nb - 1, i);
+        for (int c = j + 1; c <= cmax; ++c) S[c * mp + i] -= li * S[j * mp + c];
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (s_fail >= 0) break;
+    for (int j = 0; j < nb; ++j)
+      for (int i = tid; i < m; i += blockDim.x) L[(size_t)(J0 + j) * nt + J0 + i] = S[j * mp + i];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    a.status[b] = s_fail;
+    a.gain[b] = s_fail >= 0 ? -INFINITY : 2.0 * s_logsum;
+  }
+}
+
+// ------------------------------------------------------------------------ //
+// Triangular inverse of the chosen factor: Linv = L_k^{-1}, row-major [c][m] //
+// with zeros above the diagonal and in the pad (ld = ldl). Warp per column. //
+// ------------------------------------------------------------------------ //
+__global__ void __launch_bounds__(256) trinv_kernel(const double* L, int nt, double* Linv, int ldl) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int wib = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x >> 5) + wib;  // column of Linv
+  if (j >= ldl) return;
+  double* x = reinterpret_cast<double*>(smem_raw) + (size_t)wib * ldl;
+  for (int i = lane; i < ldl; i += 32) x[i] = (i == j) ? 1.0 : 0.0;
+  __syncwarp();
+  if (j < nt) {
+    // column-oriented forward substitution: x_m /= L[m][m]; x_i -= x_m L[i][m]
+    for (int m = j; m < nt; ++m) {
+      const double xm = x[m] / L[(size_t)m * nt + m];
+      __syncwarp();
+      if (lane == 0) x[m] = xm;
+      const double* colm = L + (size_t)m * nt;
+      for (int i = m + 1 + lane; i < nt; i += 32) x[i] -= xm * colm[i];
+      __syncwarp();
+    }
+  }
+  // Linv[i][j] = x_i (row-major [c][m] with ld = ldl), zero above the diagonal
+  for (int i = lane; i < ldl; i += 32) Linv[(size_t)i * ldl + j] = (j < nt && i < nt && i >= j) ? x[i] : 0.0;
+}
+
+// ------------------------------------------------------------------------ //
+// Local top-2 argmax with the reference tie rule (selector.hpp:132-134):   //
+// larger gain wins, exact ties go to the lower sensor index.              //
+// ------------------------------------------------------------------------ //
+struct ArgRec {
+  double g1;
+  double g2;
+  int s1;
+  int s2;
+  int n_eval;
+  int n_inf;
+};
+
+__device__ __forceinline__ bool better(double d, int s, double bd, int bs) {
+  return d > bd || (d == bd && (bs < 0 || s < bs));
+}
+
+__device__ __forceinline__ void top2_insert(double d, int s, double& g1, int& s1, double& g2, int& s2) {
+  if (s < 0) return;
+  if (s1 < 0 || better(d, s, g1, s1)) {
+    g2 = g1;
+    s2 = s1;
+    g1 = d;
+    s1 = s;
+  } else if (s2 < 0 || better(d, s, g2, s2)) {
+    g2 = d;
+    s2 = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) argmax_kernel(const double* gain, const int* status,
+                                                     const int* sensor, int n, ArgRec* out) {
+  __shared__ double sg1[256], sg2[256];
+  __shared__ int ss1[256], ss2[256], sinf[256];
+  const int tid = threadIdx.x;
+  double g1 = -INFINITY, g2 = -INFINITY;
+  int s1 = -1, s2 = -1, ninf = 0;
+  for (int i = tid; i < n; i += 256) {
+    if (status[i] >= 0) {
+      ++ninf;
+      continue;
+    }
+    top2_insert(gain[i], sensor[i], g1, s1, g2, s2);
+  }
+  sg1[tid] = g1;
+  sg2[tid] = g2;
+  ss1[tid] = s1;
+  ss2[tid] = s2;
+  sinf[tid] = ninf;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (tid < w) {
+      double a1 = sg1[tid], a2 = sg2[tid];
+      int b1 = ss1[tid], b2 = ss2[tid];
+      top2_insert(sg1[tid + w], ss1[tid + w], a1, b1, a2, b2);
+      top2_insert(sg2[tid + w], ss2[tid + w], a1, b1, a2, b2);
+      sg1[tid] = a1;
+      sg2[tid] = a2;
+      ss1[tid] = b1;
+      ss2[tid] = b2;
+      sinf[tid] += sinf[tid + w];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    out->g1 = sg1[0];
+    out->g2 = sg2[0];
+    out->s1 = ss1[0];
+    out->s2 = ss2[0];
+    out->n_eval = n;
+    out->n_inf = sinf[0];
+  }
+}
+
+// ------------------------------------------------------------------------ //
+// Factor-export history: hist[slot][step] = W rows of the local candidate   //
+// (nt x nt row-major) -- one block of L_S (linalg.hpp:159-178 layout).     //
+// ------------------------------------------------------------------------ //
+__global__ void hist_copy_kernel(const double* W, int ldw, const int* col_slot, const int* col_g,
+                                 int n_blocks, int nt, double* hist, long long slot_stride,
+                                 long long step_off) {
+  const int h = blockIdx.y;
+  if (h >= n_blocks) return;
+  const long long n2 = (long long)nt * nt;
+  double* dst = hist + (long long)col_slot[h] * slot_stride + step_off;
+  const double* srcw = W + (size_t)col_g[h] * nt * ldw;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n2;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / nt), c = (int)(e - (long long)r * nt);
+    dst[e] = srcw[(size_t)r * ldw + c];
+  }
+}
+
+// L_k (column-major) -> lower-triangular row-major block into hist.
+__global__ void hist_diag_kernel(const double* Lk, int nt, double* dst) {
+  const long long n2 = (long long)nt * nt;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n2;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / nt), c = (int)(e - (long long)r * nt);
+    dst[e] = c <= r ? Lk[(size_t)c * nt + r] : 0.0;
+  }
+}
+
+// ------------------------------------------------------------------------ //
+// Panel store ingest.                                                       //
+// ------------------------------------------------------------------------ //
+// Block row j of K (blocks (j, i), i = 0..nd-1, each row-major nt x nt, the  //
+// KBF / DataSpaceHessian order, kstore.hpp:22-35) -> panel of candidate j,  //
+// using K(i,j)[r][c] = K(j,i)[c][r] (exact for symmetric K).               //
+__global__ void scatter_block_row_kernel(const double* row, int nt, const int* pos_sensor,
+                                         int n_cand, double* panel, long long ldc) {
+  // panel[(c)*ldc + p*nt + r] = row[sensor(p)*nt*nt + c*nt + r]
+  const long long total = (long long)n_cand * nt * nt;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e % nt);
+    const long long rest = e / nt;
+    const int p = (int)(rest % n_cand);
+    const int c = (int)(rest / n_cand);
+    panel[(size_t)c * ldc + (size_t)p * nt + r] =
+        row[(size_t)pos_sensor[p] * nt * nt + (size_t)c * nt + r];
+  }
+}
+
+// Block column j (blocks (i, j), i = 0..nd-1, each row-major) -> panel
+// (exact reference semantics: read_test_column reads blocks (S[t], s),
+// kaccess.hpp:27-35).
+__global__ void scatter_block_col_kernel(const double* colblk, int nt, const int* pos_sensor,
+                                         int n_cand, double* panel, long long ldc) {
+  const long long total = (long long)n_cand * nt * nt;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e % nt);
+    const long long rest = e / nt;
+    const int p = (int)(rest % n_cand);
+    const int c = (int)(rest / n_cand);
+    panel[(size_t)c * ldc + (size_t)p * nt + r] =
+        colblk[(size_t)pos_sensor[p] * nt * nt + (size_t)r * nt + c];
+  }
+}
+
+// Inverse of scatter_block_row: panel -> block row j (for export/tests).
+__global__ void gather_block_row_kernel(const double* panel, long long ldc, int nt,
+                                        const int* pos_sensor, int n_cand, double* row) {
+  const long long total = (long long)n_cand * nt * nt;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e % nt);
+    const long long rest = e / nt;
+    const int p = (int)(rest % n_cand);
+    const int c = (int)(rest / n_cand);
+    row[(size_t)pos_sensor[p] * nt * nt + (size_t)c * nt + r] =
+        panel[(size_t)c * ldc + (size_t)p * nt + r];
+  }
+}
+
+// ------------------------------------------------------------------------ //
+// Bit-exact synthetic panel generator (SyntheticKAccess::read_block,        //
+// kaccess.hpp:98-116): K(i,j)[r][c] = sum_t V[i*nt+r][t]*V[j*nt+c][t] with   //
+// sequential t order and no FMA contraction, then + sigma^2 on the diagonal.//
+// Thread computes a 4x4 micro-tile; V tiles staged through shared memory.   //
+// ------------------------------------------------------------------------ //
+namespace gen {
+constexpr int BM = 64, BN = 64, KT = 16, THREADS = 256;
+}
+
+struct GenArgs {
+  const double* V;       // (nd*nt) x rank row-major, sensor-major rows
+  int rank;
+  double noise2;
+  int nt;
+  const int* row_sensor;  // candidate position p -> sensor id
+  int n_rows;             // n_cand * nt
+  const int* col_sensor;  // local slot q -> sensor id
+  int n_cols;             // n_loc * nt
+  double* C;
+  long long ldc;
+};
+
+__global__ void __launch_bounds__(gen::THREADS) synth_panel_kernel(GenArgs a) {
+  using namespace gen;
+  __shared__ double sA[KT][BM + 1];
+  __shared__ double sB[KT][BN + 1];
+  __shared__ int arow[BM], brow[BN];
+  const int r0 = blockIdx.x * BM, c0 = blockIdx.y * BN;
+  const int tid = threadIdx.x;
+  const int nt = a.nt;
+  for (int i = tid; i < BM; i += THREADS) {
+    const int r = r0 + i;
+    arow[i] = r < a.n_rows ? a.row_sensor[r / nt] * nt + r % nt : -1;
+  }
+  for (int i = tid; i < BN; i += THREADS) {
+    const int c = c0 + i;
+    brow[i] = c < a.n_cols ? a.col_sensor[c / nt] * nt + c % nt : -1;
+  }
+  __syncthreads();
+  const int tr = (tid / 16) * 4, tc = (tid % 16) * 4;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  for (int t0 = 0; t0 < a.rank; t0 += KT) {
+    const int kw = min(KT, a.rank - t0);
+    for (int idx = tid; idx < KT * BM; idx += THREADS) {
+      const int i = idx / KT, k = idx % KT;
+      sA[k][i] = (arow[i] >= 0 && k < kw) ? a.V[(size_t)arow[i] * a.rank + t0 + k] : 0.0;
+      sB[k][i] = (brow[i] >= 0 && k < kw) ? a.V[(size_t)brow[i] * a.rank + t0 + k] : 0.0;
+    }
+    __syncthreads();
+    for (int k = 0; k < kw; ++k) {
+      double x[4], y[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) x[i] = sA[k][tr + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) y[j] = sB[k][tc + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(x[i], y[j]));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = r0 + tr + i;
+    if (r >= a.n_rows) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = c0 + tc + j;
+      if (c >= a.n_cols) continue;
+      double v = acc[i][j];
+      if (arow[tr + i] == brow[tc + j]) v = __dadd_rn(v, a.noise2);
+      const int q = c / nt, cc = c % nt;
+      a.C[(size_t)(q * nt + cc) * a.ldc + r] = v;
+    }
+  }
+}
+
+}  // namespace dsel

@@ -1,0 +1,338 @@
+"""Host-side mirror of the reference selection interface over the C ABI.
+
+Reference interface (C++, /root/reference/proj/include/doptsel):
+  greedy_select<Real,A>(k, candidates, budget, opts)        selector.hpp:181-248
+  run_parallel_greedy<Real,A>(k, candidates, budget, opts)  parallel.hpp:281-483
+  -> (SelectionState{chosen, factor, objective}, SelectionTrace{rows, warning})
+
+Here the same call goes to libdsel.so (one engine per GPU). Error behaviour
+follows errors.hpp: InvalidConfig / IndexOutOfRange raised before any work,
+InfeasibleRound when round 1 has no feasible candidate, a partial selection
+with a warning when a later round has none, WorkerFailure for device or
+collective failures. The C++ drop-in for the reference tree is
+include/doptsel_gpu.hpp; this module is what tests and bench.py drive.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._abi import DSEL_OK, STATUS_NAMES, DselConfig, DselStats, DselStepInfo, lib
+
+
+# ---- errors (errors.hpp:10-86) -------------------------------------------- #
+class DselError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class InvalidConfig(DselError):
+    pass
+
+
+class IndexOutOfRange(DselError):
+    pass
+
+
+class InfeasibleRound(DselError):
+    round = 1
+
+
+class WorkerFailure(DselError):
+    pass
+
+
+_EXC = {1: InvalidConfig, 2: IndexOutOfRange, 3: InfeasibleRound, 4: WorkerFailure,
+        5: WorkerFailure, 6: WorkerFailure, 7: DselError, 8: DselError}
+
+
+def _check(rc: int, handle=None) -> None:
+    if rc != DSEL_OK:
+        msg = lib.dsel_last_error(handle).decode(errors="replace")
+        raise _EXC.get(rc, DselError)(rc, msg)
+
+
+def _ptr(a: np.ndarray):
+    return C.c_void_p(a.ctypes.data)
+
+
+def _host_ptr(a):
+    """numpy array or (pinned) torch CPU tensor -> void*."""
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"] or a.dtype != np.float64:
+            raise InvalidConfig(1, "host K must be C-contiguous float64")
+        return C.c_void_p(a.ctypes.data)
+    return C.c_void_p(a.data_ptr())
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    _check(lib.dsel_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def synthetic_v(n_sensors: int, n_steps: int, rank: int, seed: int, threads: int = 0) -> np.ndarray:
+    """V of SyntheticKAccess (kaccess.hpp:89-92), bit-identical, shape (nd*nt, rank)."""
+    out = np.empty(n_sensors * n_steps * rank, dtype=np.float64)
+    _check(lib.dsel_synthetic_v(n_sensors, n_steps, rank, seed, _ptr(out), threads))
+    return out.reshape(n_sensors * n_steps, rank)
+
+
+class Engine:
+    """One selection engine on one GPU (one rank of a world_size group)."""
+
+    def __init__(self, n_sensors: int, n_steps: int, budget: int, candidates=None, device: int = 0,
+                 world_size: int = 1, rank: int = 0, nccl_id: bytes | None = None,
+                 keep_pristine: bool = False, export_factor: bool = False,
+                 near_tie_tau: float = 1e-9, storage: int = 0):
+        cfg = DselConfig()
+        cfg.n_sensors, cfg.n_steps, cfg.budget = n_sensors, n_steps, budget
+        self._cands = None
+        if candidates is not None:
+            self._cands = np.ascontiguousarray(np.asarray(candidates, dtype=np.int32))
+            cfg.n_candidates = len(self._cands)
+            cfg.candidates = self._cands.ctypes.data_as(C.POINTER(C.c_int))
+        cfg.device, cfg.world_size, cfg.rank = device, world_size, rank
+        self._id = None
+        if nccl_id is not None:
+            self._id = (C.c_ubyte * 128).from_buffer_copy(nccl_id)
+            cfg.nccl_id = C.cast(self._id, C.c_void_p)
+        cfg.storage = storage
+        cfg.keep_pristine = int(keep_pristine)
+        cfg.export_factor = int(export_factor)
+        cfg.near_tie_tau = near_tie_tau
+        h = C.c_void_p()
+        _check(lib.dsel_create(C.byref(cfg), C.byref(h)), None)
+        self.h = h
+        self.n_sensors, self.n_steps, self.budget = n_sensors, n_steps, budget
+        self.world_size, self.rank = world_size, rank
+
+    # -- lifecycle --
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            lib.dsel_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def sync(self) -> None:
+        _check(lib.dsel_sync(self.h), self.h)
+
+    @property
+    def device_bytes(self) -> int:
+        return int(lib.dsel_device_bytes(self.h))
+
+    # -- panel store ingest --
+    def load_k(self, k) -> None:
+        """Whole K, block-row-major (DataSpaceHessian / KBF payload order)."""
+        _check(lib.dsel_load_k(self.h, _host_ptr(k)), self.h)
+
+    def load_block_row(self, j: int, row) -> None:
+        _check(lib.dsel_load_block_row(self.h, j, _host_ptr(row)), self.h)
+
+    def load_block_col(self, j: int, col) -> None:
+        _check(lib.dsel_load_block_col(self.h, j, _host_ptr(col)), self.h)
+
+    def gen_synthetic(self, v: np.ndarray, rank: int, sigma: float) -> None:
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        _check(lib.dsel_gen_synthetic(self.h, _ptr(v), rank, sigma), self.h)
+
+    def read_block_row(self, j: int) -> np.ndarray:
+        out = np.empty(self.n_sensors * self.n_steps * self.n_steps)
+        _check(lib.dsel_read_block_row(self.h, j, _ptr(out)), self.h)
+        return out
+
+    # -- selection --
+    def step(self, forced: int | None = None) -> dict:
+        info = DselStepInfo()
+        if forced is None:
+            _check(lib.dsel_step(self.h, C.byref(info)), self.h)
+        else:
+            _check(lib.dsel_step_forced(self.h, int(forced), C.byref(info)), self.h)
+        return info.as_dict()
+
+    def run(self) -> int:
+        n = C.c_int(0)
+        _check(lib.dsel_run(self.h, C.byref(n)), self.h)
+        return n.value
+
+    def peek_gains(self) -> np.ndarray:
+        g = np.full(self.n_sensors, np.nan)
+        _check(lib.dsel_peek_gains(self.h, _ptr(g)), self.h)
+        return g
+
+    def trace(self) -> list:
+        rows = (DselStepInfo * max(self.budget, 1))()
+        n = lib.dsel_get_trace(self.h, rows, max(self.budget, 1))
+        if n < 0:
+            _check(4, self.h)
+        return [rows[i].as_dict() for i in range(n)]
+
+    def stats(self) -> dict:
+        st = DselStats()
+        _check(lib.dsel_get_stats(self.h, C.byref(st)), self.h)
+        return st.as_dict()
+
+    def reset(self) -> None:
+        _check(lib.dsel_reset(self.h), self.h)
+
+    def export_factor(self, k: int) -> np.ndarray:
+        dim = k * self.n_steps
+        out = np.zeros((max(dim, 1), max(dim, 1)))
+        if k:
+            _check(lib.dsel_export_factor(self.h, _ptr(out), dim), self.h)
+        return out[:dim, :dim]
+
+
+# ---- reference-shaped results (selector.hpp:31-54, parallel.hpp:23-52) ---- #
+@dataclass
+class TraceRow:
+    k: int
+    chosen_index: int
+    objective: float
+    gain: float
+    n_evaluated: int
+    n_infeasible: int
+    wall_ms: float
+    mean_candidate_ms: float
+    runner_up: int = -1
+    runner_up_gain: float = float("-inf")
+    near_tie: bool = False
+
+
+@dataclass
+class SelectionState:
+    chosen: list
+    factor: np.ndarray | None
+    objective: float
+
+
+@dataclass
+class SelectionTrace:
+    rows: list = field(default_factory=list)
+    warning: str = ""
+
+
+@dataclass
+class RoundResult:
+    d_max: float
+    s_star: int
+    bytes_exchanged: int
+    ms: dict
+
+
+@dataclass
+class ParallelRunReport:
+    trace: SelectionTrace
+    rounds: list
+
+
+@dataclass
+class GpuOptions:
+    """GpuOptions of SURVEY.md §8(b): ParallelOptions (parallel.hpp:37-47) with
+    n_workers -> one engine per GPU. `seed` is accepted and, as in the
+    reference, does not change results (the shuffle is result-invariant)."""
+    device: int = 0
+    world_size: int = 1
+    rank: int = 0
+    nccl_id: bytes | None = None
+    mode: str = "raw"              # raw | normalized (SelectionOptions, selector.hpp:26-29)
+    noise_logdets: list | None = None
+    near_tie_tau: float = 1e-9
+    export_factor: bool = True
+    seed: int = 0
+
+
+def gpu_greedy_select(k, candidates, budget: int, opts: GpuOptions | None = None):
+    """Drop-in for run_parallel_greedy<double> (parallel.hpp:281-483).
+
+    k: either a raw block-row-major array with attributes given as a tuple
+    (k_raw, n_sensors, n_steps), or an object with n_sensors(), n_steps() and
+    read_block(i, j, out) (the KAccess concept, kaccess.hpp:18-23).
+    Returns (SelectionState, ParallelRunReport).
+    """
+    opts = opts or GpuOptions()
+    if isinstance(k, tuple):
+        k_raw, nd, nt = k
+        reader = None
+    else:
+        k_raw, nd, nt, reader = None, int(k.n_sensors()), int(k.n_steps()), k
+    if budget < 0:
+        raise InvalidConfig(1, "budget must be nonnegative")
+    cands = list(range(nd)) if candidates is None else [int(c) for c in candidates]
+    seen = set()
+    for c in cands:
+        if c < 0 or c >= nd:
+            raise IndexOutOfRange(2, "candidate index out of range")
+        if c in seen:
+            raise InvalidConfig(1, "duplicate candidate index")
+        seen.add(c)
+    if opts.mode == "normalized" and (opts.noise_logdets is None or len(opts.noise_logdets) != nd):
+        raise InvalidConfig(1, "normalized mode requires one noise log-determinant per sensor")
+    trace = SelectionTrace()
+    if budget > len(cands):
+        trace.warning = "budget exceeds candidate count; selecting all candidates"
+    eff = min(budget, len(cands))
+    if eff == 0 or not cands:
+        return SelectionState([], np.zeros((0, 0)), 0.0), ParallelRunReport(trace, [])
+    eng = Engine(nd, nt, eff, candidates=cands, device=opts.device, world_size=opts.world_size,
+                 rank=opts.rank, nccl_id=opts.nccl_id, export_factor=opts.export_factor,
+                 near_tie_tau=opts.near_tie_tau)
+    try:
+        if reader is None:
+            eng.load_k(np.ascontiguousarray(k_raw, dtype=np.float64))
+        else:
+            # true block columns (i, j): exact reference semantics (kaccess.hpp:27-35)
+            col = np.empty((nd, nt, nt))
+            for p, j in enumerate(sorted(cands)):
+                if p % opts.world_size != opts.rank:
+                    continue  # panel owned by another rank
+                for i in range(nd):
+                    reader.read_block(i, j, col[i])
+                eng.load_block_col(j, col)
+        for _ in range(eff):
+            info = eng.step()
+            if info["chosen_index"] < 0:
+                trace.warning = "no feasible candidates remain; returning partial selection"
+                break
+        rows = eng.trace()
+        chosen = [r["chosen_index"] for r in rows if r["chosen_index"] >= 0]
+        factor = eng.export_factor(len(chosen)) if opts.export_factor else None
+    finally:
+        eng.close()
+    out_rows, rounds = [], []
+    noise_acc = 0.0
+    for r in rows:
+        if r["chosen_index"] < 0:
+            continue
+        s = r["chosen_index"]
+        gain, obj = r["gain"], r["objective"]
+        if opts.mode == "normalized":
+            noise_acc += opts.noise_logdets[s]
+            gain = gain - opts.noise_logdets[s]
+            obj = obj - noise_acc
+        out_rows.append(TraceRow(k=r["k"], chosen_index=s, objective=obj, gain=gain,
+                                 n_evaluated=r["n_evaluated"], n_infeasible=r["n_infeasible"],
+                                 wall_ms=r["ms_round"],
+                                 mean_candidate_ms=r["ms_round"] / max(r["n_evaluated"], 1),
+                                 runner_up=r["runner_up"], runner_up_gain=r["runner_up_gain"],
+                                 near_tie=bool(r["near_tie"])))
+        rounds.append(RoundResult(d_max=r["gain"], s_star=s, bytes_exchanged=r["bytes_exchanged"],
+                                  ms={key: r[key] for key in ("ms_gain", "ms_exchange", "ms_panel",
+                                                              "ms_update", "ms_round")}))
+    trace.rows = out_rows
+    objective = rows[len(out_rows) - 1]["objective"] if out_rows else 0.0
+    return SelectionState(chosen, factor, objective), ParallelRunReport(trace, rounds)
