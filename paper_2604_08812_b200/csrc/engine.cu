@@ -77,6 +77,8 @@ struct dsel_engine {
   int nloc = 0;        // local slots
   int ldw = 0;         // W / Linv pitch
   int eff_budget = 0;
+  int n_sms = 148;
+  int mpad = 0;  // rows of the tiled W buffers
   bool keep = false, export_factor = false;
   double tau = 1e-9;
   std::vector<int> pos_sensor, sensor_pos, slot_sensor;
@@ -85,7 +87,7 @@ struct dsel_engine {
   cudaStream_t s = nullptr;
   ncclComm_t comm = nullptr;
   double *C = nullptr, *K0 = nullptr, *W = nullptr, *Pbuf = nullptr, *Lk = nullptr,
-         *Linv = nullptr, *Lscr = nullptr, *gains = nullptr, *hist = nullptr, *kgain = nullptr,
+         *Linv = nullptr, *Lscr = nullptr, *Wn = nullptr, *Wt = nullptr, *Wnt = nullptr, *gains = nullptr, *hist = nullptr, *kgain = nullptr,
          *stage = nullptr, *xbuf = nullptr;
   int *status = nullptr, *kstatus = nullptr;
   int *d_pos_sensor = nullptr, *d_slot_sensor = nullptr;
@@ -295,6 +297,7 @@ void set_smem_limits(int dev) {
   allow_smem(panel_w_kernel<2>, optin);
   allow_smem(panel_w_kernel<1>, optin);
   allow_smem(trinv_kernel, optin);
+  allow_smem(schur_update_ws_kernel, optin);
 }
 
 void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
@@ -403,6 +406,10 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       pa.Linv = e->Linv;
       pa.ldl = e->ldw;
       pa.W = e->W;
+      pa.Wn = e->Wn;
+      pa.Wt = e->Wt;
+      pa.Wnt = e->Wnt;
+      pa.mpad = e->mpad;
       pa.ldw = e->ldw;
       pa.row_pos = e->row_pos();
       pa.nt = nt;
@@ -435,29 +442,51 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   }
   CU(cudaEventRecord(ev[3], e->s));
   if (!last && R > 0 && Rl > 0) {
-    UpdateArgs ua;
-    ua.C = e->C;
-    ua.ldc = e->n;
-    ua.W = e->W;
-    ua.ldw = e->ldw;
-    ua.row_pos = e->row_pos();
-    ua.col_slot = e->col_slot();
-    ua.col_g = e->col_g();
-    ua.nt = nt;
-    ua.n_rows = R * nt;
-    ua.n_cols = Rl * nt;
-    ua.n_row_tiles = (ua.n_rows + upd::BR - 1) / upd::BR;
-    ua.n_col_tiles = (ua.n_cols + upd::BC - 1) / upd::BC;
-    ua.group = 16;
-    const long long tiles = (long long)ua.n_row_tiles * ua.n_col_tiles;
-    if (nt % 2 == 0)
-      schur_update_kernel<2><<<(unsigned)tiles, upd::THREADS, upd::SMEM, e->s>>>(ua);
-    else
-      schur_update_kernel<1><<<(unsigned)tiles, upd::THREADS, upd::SMEM, e->s>>>(ua);
+    const int n_rows = R * nt, n_cols = Rl * nt;
+    if (nt % 2 == 0) {
+      UpdateWSArgs ua;
+      ua.C = e->C;
+      ua.ldc = e->n;
+      ua.Wt = e->Wt;
+      ua.Wnt = e->Wnt;
+      ua.mpad = e->mpad;
+      ua.n_k = e->ldw / ws::KC;
+      ua.row_pos = e->row_pos();
+      ua.col_slot = e->col_slot();
+      ua.col_g = e->col_g();
+      ua.nt = nt;
+      ua.n_rows = n_rows;
+      ua.n_cols = n_cols;
+      ua.n_row_tiles = (n_rows + ws::BR - 1) / ws::BR;
+      ua.n_col_tiles = (n_cols + ws::BC - 1) / ws::BC;
+      ua.group = 16;
+      const long long tiles = (long long)ua.n_row_tiles * ua.n_col_tiles;
+      const int grid = (int)std::min<long long>(e->n_sms, tiles);
+      schur_update_ws_kernel<<<grid, ws::THREADS, ws::SMEM, e->s>>>(ua);
+    } else {
+      UpdateArgs ua;
+      ua.C = e->C;
+      ua.ldc = e->n;
+      ua.W = e->W;
+      ua.Wn = e->Wn;
+      ua.ldw = e->ldw;
+      ua.row_pos = e->row_pos();
+      ua.col_slot = e->col_slot();
+      ua.col_g = e->col_g();
+      ua.nt = nt;
+      ua.n_rows = n_rows;
+      ua.n_cols = n_cols;
+      ua.n_row_tiles = (n_rows + upd::BR - 1) / upd::BR;
+      ua.n_col_tiles = (n_cols + upd::BC - 1) / upd::BC;
+      ua.group = 16;
+      const long long tiles = (long long)ua.n_row_tiles * ua.n_col_tiles;
+      const int grid = (int)std::min<long long>(e->n_sms, (tiles + 1) / 2);
+      schur_update_kernel<1><<<grid, upd::THREADS, upd::SMEM, e->s>>>(ua);
+    }
     CU(cudaGetLastError());
     e->launches += 1;
     e->update_flops += 2.0 * nt * (double)(R * nt) * (double)(Rl * nt);
-    flops = 2.0 * nt * (double)ua.n_rows * (double)ua.n_cols;
+    flops = 2.0 * nt * (double)n_rows * (double)n_cols;
   }
   CU(cudaEventRecord(ev[4], e->s));
 
@@ -500,7 +529,7 @@ void destroy_impl(dsel_engine* e) {
   if (e->s) cudaStreamSynchronize(e->s);
   if (e->cs) cudaStreamSynchronize(e->cs);
   for (auto ev : e->ev) cudaEventDestroy(ev);
-  double* dptr[] = {e->C, e->K0, e->W, e->Pbuf, e->Lk, e->Linv, e->Lscr, e->gains, e->hist,
+  double* dptr[] = {e->C, e->K0, e->W, e->Wn, e->Wt, e->Wnt, e->Pbuf, e->Lk, e->Linv, e->Lscr, e->gains, e->hist,
                     e->kgain, e->stage, e->xbuf};
   for (double* d : dptr)
     if (d) cudaFree(d);
@@ -576,6 +605,7 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
 
     CU(cudaSetDevice(e->dev));
     set_smem_limits(e->dev);
+    CU(cudaDeviceGetAttribute(&e->n_sms, cudaDevAttrMultiProcessorCount, e->dev));
     CU(cudaStreamCreateWithFlags(&e->s, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&e->cs, cudaStreamNonBlocking));
     for (int b = 0; b < 2; ++b) {
@@ -587,6 +617,13 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     e->C = dmalloc<double>(shard, tot);
     if (e->keep) e->K0 = dmalloc<double>(shard, tot);
     e->W = dmalloc<double>((size_t)e->n * e->ldw, tot);
+    e->mpad = round_up((int)e->n, ws::BR);
+    if (e->nt % 2 == 0) {
+      e->Wt = dmalloc<double>((size_t)e->mpad * e->ldw, tot);
+      e->Wnt = dmalloc<double>((size_t)e->mpad * e->ldw, tot);
+    } else {
+      e->Wn = dmalloc<double>((size_t)e->n * e->ldw, tot);
+    }
     if (e->G > 1) e->Pbuf = dmalloc<double>((size_t)e->n * e->nt, tot);
     e->Lk = dmalloc<double>((size_t)e->nt * e->nt, tot);
     e->Linv = dmalloc<double>((size_t)e->ldw * e->ldw, tot);
@@ -607,6 +644,11 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     CU(cudaMallocHost(&e->h_recs, sizeof(ArgRec) * e->G));
     CU(cudaMallocHost(&e->h_tab, sizeof(int) * ((size_t)e->nc + 2 * e->nloc + 1)));
     CU(cudaMemsetAsync(e->W, 0, sizeof(double) * (size_t)e->n * e->ldw, e->s));
+    if (e->Wn) CU(cudaMemsetAsync(e->Wn, 0, sizeof(double) * (size_t)e->n * e->ldw, e->s));
+    if (e->Wt) {
+      CU(cudaMemsetAsync(e->Wt, 0, sizeof(double) * (size_t)e->mpad * e->ldw, e->s));
+      CU(cudaMemsetAsync(e->Wnt, 0, sizeof(double) * (size_t)e->mpad * e->ldw, e->s));
+    }
     CU(cudaMemsetAsync(e->C, 0, sizeof(double) * shard, e->s));
     CU(cudaMemcpyAsync(e->d_pos_sensor, e->pos_sensor.data(), sizeof(int) * e->nc,
                        cudaMemcpyHostToDevice, e->s));

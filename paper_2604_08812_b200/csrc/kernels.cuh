@@ -51,22 +51,33 @@ __device__ __forceinline__ void cp_async_wait() {
 // Rank-nt Schur update: C[rows, local cols] -= W[rows] * W[cols]^T          //
 // (north-star (2); replaces the per-candidate forward substitution +       //
 // schur_complement of linalg.hpp:39-114 by one right-looking update).     //
+//                                                                          //
+// Persistent, one CTA per SM, two consumer warpgroups in PING-PONG: while  //
+// one warpgroup runs its DMMA mainloop alone on the FP64 tensor pipe, the  //
+// other stores its finished tile, streams the next C tile into its         //
+// accumulators and prefetches its operand stages. Turn order is enforced   //
+// with named barriers, so C traffic (16 B/element, AI = Nt/8 flop/B) hides //
+// behind the other warpgroup's math. The c-side operand comes from Wn = -W //
+// so the accumulators start at +C and the DMMA chain yields C - W W^T.     //
 // ------------------------------------------------------------------------ //
 namespace upd {
-constexpr int BR = 128;       // compact rows per CTA tile (r-side)
-constexpr int BC = 64;        // local compact columns per CTA tile (c-side)
+constexpr int BR = 128;       // compact rows per warpgroup tile (r-side)
+constexpr int BC = 64;        // local compact columns per warpgroup tile (c-side)
 constexpr int KC = 16;        // k-chunk per pipeline stage
 constexpr int LDK = KC + 4;   // smem row pitch (doubles): conflict-free fragment reads
 constexpr int STAGES = 3;
-constexpr int THREADS = 256;
-constexpr size_t SMEM = (size_t)STAGES * (BR + BC) * LDK * sizeof(double) +
-                        BC * sizeof(long long) + (BR + BC) * sizeof(int);
+constexpr int WG = 128;       // threads per warpgroup
+constexpr int THREADS = 2 * WG;
+constexpr size_t WG_SMEM = (size_t)STAGES * (BR + BC) * LDK * sizeof(double) +
+                           BC * sizeof(long long) + (BR + BC) * sizeof(int);
+constexpr size_t SMEM = 2 * WG_SMEM;
 }  // namespace upd
 
 struct UpdateArgs {
   double* C;            // local shard, column-major
   long long ldc;        // = n
-  const double* W;      // compact rows, row-major
+  const double* W;      // compact rows, row-major (r-side operand)
+  const double* Wn;     // -W (c-side operand)
   int ldw;              // multiple of 16
   const int* row_pos;   // compact global block g -> candidate position p
   const int* col_slot;  // local compact block h -> local slot q
@@ -77,19 +88,16 @@ struct UpdateArgs {
   int n_row_tiles, n_col_tiles, group;
 };
 
-template <int VEC>
-__global__ void __launch_bounds__(upd::THREADS, 2) schur_update_kernel(UpdateArgs a) {
-  using namespace upd;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* sR = reinterpret_cast<double*>(smem_raw);          // [STAGES][BR][LDK]
-  double* sC = sR + STAGES * BR * LDK;                        // [STAGES][BC][LDK]
-  long long* colbase = reinterpret_cast<long long*>(sC + STAGES * BC * LDK);  // [BC]
-  int* rowphys = reinterpret_cast<int*>(colbase + BC);        // [BR]
-  int* cwrow = rowphys + BR;                                  // [BC]
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
 
-  // grouped rasterization: GROUP column tiles sweep all row tiles together
-  // so their W rows stay L2-resident while the row-side W streams.
-  const int tile = blockIdx.x;
+// grouped rasterization: GROUP column tiles sweep all row tiles together so
+// their W rows stay L2-resident while the row-side W streams.
+__device__ __forceinline__ void tile_coords(const UpdateArgs& a, int tile, int& r0, int& c0) {
   const int gsz = a.group * a.n_row_tiles;
   const int grp = tile / gsz;
   const int within = tile - grp * gsz;
@@ -97,39 +105,42 @@ __global__ void __launch_bounds__(upd::THREADS, 2) schur_update_kernel(UpdateArg
   const int gw = min(a.group, a.n_col_tiles - ct0);
   const int rt = within / gw;
   const int ct = ct0 + within % gw;
-  const int r0 = rt * BR, c0 = ct * BC;
-  const int tid = threadIdx.x;
+  r0 = rt * upd::BR;
+  c0 = ct * upd::BC;
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(upd::THREADS, 1) schur_update_kernel(UpdateArgs a) {
+  using namespace upd;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int wg = threadIdx.x / WG;       // warpgroup 0 / 1
+  const int tid = threadIdx.x % WG;      // thread within the warpgroup
+  unsigned char* base = smem_raw + (size_t)wg * WG_SMEM;
+  double* sR = reinterpret_cast<double*>(base);                              // [STAGES][BR][LDK]
+  double* sC = sR + STAGES * BR * LDK;                                       // [STAGES][BC][LDK]
+  long long* colbase = reinterpret_cast<long long*>(sC + STAGES * BC * LDK);  // [BC]
+  int* rowphys = reinterpret_cast<int*>(colbase + BC);                       // [BR]
+  int* cwrow = rowphys + BR;                                                 // [BC]
+  const int bar_wg = 1 + wg;        // intra-warpgroup barrier
+  const int bar_me = 3 + wg;        // my turn on the tensor pipe
+  const int bar_other = 3 + (1 - wg);
   const int nt = a.nt;
-
-  for (int i = tid; i < BR; i += THREADS) {
-    const int r = r0 + i;
-    if (r < a.n_rows) {
-      const int blk = r / nt;
-      rowphys[i] = a.row_pos[blk] * nt + (r - blk * nt);
-    } else {
-      rowphys[i] = -1;
-    }
-  }
-  for (int i = tid; i < BC; i += THREADS) {
-    const int c = c0 + i;
-    if (c < a.n_cols) {
-      const int blk = c / nt;
-      const int off = c - blk * nt;
-      colbase[i] = (long long)(a.col_slot[blk] * nt + off) * a.ldc;
-      cwrow[i] = a.col_g[blk] * nt + off;
-    } else {
-      colbase[i] = -1;
-      cwrow[i] = -1;
-    }
-  }
-  __syncthreads();
-
   const int n_k = a.ldw / KC;
+  const int n_tiles = a.n_row_tiles * a.n_col_tiles;
+  const int n_slots = (n_tiles + 2 * gridDim.x - 1) / (2 * gridDim.x);
+
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = (warp & 1) * 64;   // r-side offset of this warp (64 rows)
+  const int wc = (warp >> 1) * 32;  // c-side offset of this warp (32 cols)
+
+  int r0 = 0, c0 = 0;
   auto load_stage = [&](int stage, int kc) {
     double* dR = sR + stage * BR * LDK;
     double* dC = sC + stage * BC * LDK;
     constexpr int CPR = KC / 2;  // 16-byte chunks per row
-    for (int idx = tid; idx < (BR + BC) * CPR; idx += THREADS) {
+#pragma unroll 4
+    for (int idx = tid; idx < (BR + BC) * CPR; idx += WG) {
       const int row = idx / CPR;
       const int ch = idx - row * CPR;
       if (row < BR) {
@@ -139,79 +150,428 @@ __global__ void __launch_bounds__(upd::THREADS, 2) schur_update_kernel(UpdateArg
         cp_async16(dR + row * LDK + ch * 2, src, ok);
       } else {
         const int cr = row - BR;
-        const int wr = cwrow[cr];
-        const bool ok = wr >= 0;
-        const double* src = a.W + (size_t)(ok ? wr : 0) * a.ldw + kc + ch * 2;
+        const int w = cwrow[cr];
+        const bool ok = w >= 0;
+        const double* src = a.Wn + (size_t)(ok ? w : 0) * a.ldw + kc + ch * 2;
         cp_async16(dC + cr * LDK + ch * 2, src, ok);
       }
     }
   };
 
+  if (wg == 1) named_arrive(3, THREADS);  // warpgroup 0 takes the first turn
+
+  double acc[4][8][2];
+  for (int slot = 0; slot < n_slots; ++slot) {
+    const int tile = (slot * gridDim.x + blockIdx.x) * 2 + wg;
+    const bool valid = tile < n_tiles;
+    if (valid) {
+      tile_coords(a, tile, r0, c0);
+      named_sync(bar_wg, WG);  // previous tile's readers of the maps are done
+      for (int i = tid; i < BR; i += WG) {
+        const int r = r0 + i;
+        if (r < a.n_rows) {
+          const int blk = r / nt;
+          rowphys[i] = a.row_pos[blk] * nt + (r - blk * nt);
+        } else {
+          rowphys[i] = -1;
+        }
+      }
+      for (int i = tid; i < BC; i += WG) {
+        const int c = c0 + i;
+        if (c < a.n_cols) {
+          const int blk = c / nt;
+          const int off = c - blk * nt;
+          colbase[i] = (long long)(a.col_slot[blk] * nt + off) * a.ldc;
+          cwrow[i] = a.col_g[blk] * nt + off;
+        } else {
+          colbase[i] = -1;
+          cwrow[i] = -1;
+        }
+      }
+      named_sync(bar_wg, WG);
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < n_k) load_stage(s, s * KC);
-    cp_async_commit();
+      for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < n_k) load_stage(s, s * KC);
+        cp_async_commit();
+      }
+      // accumulators <- C tile (streaming loads, issued back to back)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const long long cb = colbase[wc + i * 8 + g];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int rl = wr + j * 8 + 2 * t;
+          const int p0 = rowphys[rl];
+          acc[i][j][0] = acc[i][j][1] = 0.0;
+          if (cb >= 0 && p0 >= 0) {
+            const double* col = a.C + cb;
+            if (VEC == 2) {
+              const double2 v = __ldcs(reinterpret_cast<const double2*>(col + p0));
+              acc[i][j][0] = v.x;
+              acc[i][j][1] = v.y;
+            } else {
+              acc[i][j][0] = __ldcs(col + p0);
+              const int p1 = rowphys[rl + 1];
+              if (p1 >= 0) acc[i][j][1] = __ldcs(col + p1);
+            }
+          }
+        }
+      }
+    }
+    named_sync(bar_me, THREADS);  // wait for my turn on the tensor pipe
+    if (valid) {
+      for (int kb = 0; kb < n_k; ++kb) {
+        cp_async_wait<STAGES - 2>();
+        named_sync(bar_wg, WG);
+        {
+          const int nk = kb + STAGES - 1;
+          if (nk < n_k) load_stage(nk % STAGES, nk * KC);
+          cp_async_commit();
+        }
+        const double* tR = sR + (kb % STAGES) * BR * LDK;
+        const double* tC = sC + (kb % STAGES) * BC * LDK;
+#pragma unroll
+        for (int k4 = 0; k4 < KC / 4; ++k4) {
+          double fa[4], fb[8];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) fa[i] = tC[(wc + i * 8 + g) * LDK + k4 * 4 + t];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) fb[j] = tR[(wr + j * 8 + g) * LDK + k4 * 4 + t];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) dmma884(acc[i][j], fa[i], fb[j]);
+        }
+      }
+      cp_async_wait<0>();
+    }
+    if (wg == 0 || slot + 1 < n_slots) named_arrive(bar_other, THREADS);  // hand the pipe over
+    if (valid) {
+      // epilogue: C[r, c] = acc  (acc[i][j] holds rows r, r+1 of column c)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const long long cb = colbase[wc + i * 8 + g];
+        if (cb < 0) continue;
+        double* col = a.C + cb;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int rl = wr + j * 8 + 2 * t;
+          const int p0 = rowphys[rl];
+          if (p0 < 0) continue;
+          if (VEC == 2) {
+            __stcs(reinterpret_cast<double2*>(col + p0), make_double2(acc[i][j][0], acc[i][j][1]));
+          } else {
+            __stcs(col + p0, acc[i][j][0]);
+            const int p1 = rowphys[rl + 1];
+            if (p1 >= 0) __stcs(col + p1, acc[i][j][1]);
+          }
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------ //
+// Warp-specialized persistent Schur update (even nt; the production path). //
+//                                                                          //
+//   1 producer warp : cp.async.bulk (TMA bulk copies) of the W operand     //
+//                     k-chunks into a 4-stage ring, and of the NEXT tile's //
+//                     C block into shared memory, all on mbarriers;        //
+//   8 consumer warps: accumulators <- C tile (shared), DMMA.8x8x4 mainloop //
+//                     on W (r-side) x Wn = -W (c-side), streaming stores.  //
+// W is stored "tiled": k-chunk-major, 16 doubles per row per chunk, with   //
+// the 4-double groups rotated by (row % 4) so fragment loads are bank-     //
+// conflict free while every operand tile is one contiguous bulk copy.      //
+// The C tile load of tile i+1 and the stores of tile i overlap the DMMA    //
+// mainloop, so the C traffic (AI = nt/8 flop/B) hides behind the math.     //
+// ------------------------------------------------------------------------ //
+namespace ws {
+constexpr int BR = 128, BC = 64, KC = 16, STAGES = 4;
+constexpr int CONSUMERS = 256, THREADS = CONSUMERS + 32;
+constexpr int CP = BR + 8;  // C tile column pitch (doubles): conflict-free LDS.128
+constexpr size_t OFF_R = 0;
+constexpr size_t OFF_C = OFF_R + (size_t)STAGES * BR * KC * 8;
+constexpr size_t OFF_CT = OFF_C + (size_t)STAGES * BC * KC * 8;
+constexpr size_t OFF_MAPS = OFF_CT + (size_t)BC * CP * 8;                // 2 x {colbase[BC], rowphys[BR]}
+constexpr size_t MAPS_BYTES = (size_t)BC * 8 + BR * 4;
+constexpr size_t OFF_RUNS = OFF_MAPS + 2 * MAPS_BYTES;                   // producer scratch
+constexpr size_t OFF_BAR = OFF_RUNS + (size_t)(BC + BR + 8) * 8;
+constexpr size_t SMEM = OFF_BAR + 16 * 8;
+}  // namespace ws
+
+__host__ __device__ __forceinline__ size_t wt_index(int row, int k, int mpad) {
+  const int kc = k >> 4, kk = k & 15;
+  return ((size_t)kc * mpad + row) * 16 + ((((kk >> 2) + row) & 3) << 2) + (kk & 3);
+}
+
+struct UpdateWSArgs {
+  double* C;
+  long long ldc;
+  const double* Wt;   // +W tiled (r-side)
+  const double* Wnt;  // -W tiled (c-side)
+  int mpad;           // rows of the tiled buffers (multiple of BR)
+  int n_k;            // k-chunks (ldw / 16)
+  const int* row_pos;
+  const int* col_slot;
+  const int* col_g;
+  int nt;
+  int n_rows, n_cols;
+  int n_row_tiles, n_col_tiles, group;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateWSArgs a) {
+  using namespace ws;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sR = reinterpret_cast<double*>(smem_raw + OFF_R);
+  double* sCc = reinterpret_cast<double*>(smem_raw + OFF_C);
+  double* sCt = reinterpret_cast<double*>(smem_raw + OFF_CT);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + OFF_BAR);
+  uint64_t* full = bars;                  // [STAGES]  operands landed
+  uint64_t* empty = bars + STAGES;        // [STAGES]  consumers released the stage
+  uint64_t* tfull = bars + 2 * STAGES;    // [2]       maps + C tile landed (per map buffer)
+  uint64_t* mempty = bars + 2 * STAGES + 2;  // [2]    consumers finished the tile's epilogue
+  uint64_t* cempty = bars + 2 * STAGES + 4;  // [1]    consumers copied the C tile to registers
+  auto colbase_of = [&](int b) {
+    return reinterpret_cast<long long*>(smem_raw + OFF_MAPS + b * MAPS_BYTES);
+  };
+  auto rowphys_of = [&](int b) {
+    return reinterpret_cast<int*>(smem_raw + OFF_MAPS + b * MAPS_BYTES + BC * 8);
+  };
+  int* cw = reinterpret_cast<int*>(smem_raw + OFF_RUNS);        // [BC] W row of each c column
+  int* runs = cw + BC;                                          // row runs: start,len pairs
+  const int nt = a.nt;
+  const int n_tiles = a.n_row_tiles * a.n_col_tiles;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CONSUMERS / 32);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&mempty[b], CONSUMERS / 32);
+    }
+    mbar_init(cempty, CONSUMERS / 32);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == CONSUMERS / 32) {
+    // =============================== producer ===============================
+    int stage = 0;
+    unsigned ephase = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+      int r0, c0;
+      {
+        const int gsz = a.group * a.n_row_tiles;
+        const int grp = tile / gsz;
+        const int within = tile - grp * gsz;
+        const int ct0 = grp * a.group;
+        const int gw = min(a.group, a.n_col_tiles - ct0);
+        r0 = (within / gw) * BR;
+        c0 = (ct0 + within % gw) * BC;
+      }
+      const int b = it & 1;
+      if (it >= 2) mbar_wait(&mempty[b], ((it >> 1) - 1) & 1);
+      long long* colbase = colbase_of(b);
+      int* rowphys = rowphys_of(b);
+      for (int i = lane; i < BR; i += 32) {
+        const int r = r0 + i;
+        if (r < a.n_rows) {
+          const int blk = r / nt;
+          rowphys[i] = a.row_pos[blk] * nt + (r - blk * nt);
+        } else {
+          rowphys[i] = -1;
+        }
+      }
+      for (int i = lane; i < BC; i += 32) {
+        const int c = c0 + i;
+        if (c < a.n_cols) {
+          const int blk = c / nt;
+          const int off = c - blk * nt;
+          colbase[i] = (long long)(a.col_slot[blk] * nt + off) * a.ldc;
+          cw[i] = a.col_g[blk] * nt + off;
+        } else {
+          colbase[i] = -1;
+          cw[i] = -1;
+        }
+      }
+      __syncwarp();
+      // row runs of the tile (contiguous physical rows) -- same for every column
+      if (lane == 0) {
+        int nr = 0, i = 0;
+        while (i < BR && rowphys[i] >= 0) {
+          int j = i + 1;
+          while (j < BR && rowphys[j] == rowphys[j - 1] + 1) ++j;
+          runs[2 * nr] = i;
+          runs[2 * nr + 1] = j - i;
+          ++nr;
+          i = j;
+        }
+        runs[2 * BR] = nr;  // count slot (runs array sized BR pairs + 1)
+      }
+      __syncwarp();
+      const int nr = runs[2 * BR];
+      // C tile of this tile -> sCt (wait until consumers copied the previous one)
+      if (it >= 1) mbar_wait(cempty, (it - 1) & 1);
+      if (lane == 0) {
+        unsigned bytes = 0;
+        int ncols = 0;
+        for (int c = 0; c < BC; ++c) ncols += colbase[c] >= 0;
+        for (int q = 0; q < nr; ++q) bytes += (unsigned)runs[2 * q + 1] * 8u;
+        mbar_expect_tx(&tfull[b], bytes * (unsigned)ncols);
+      }
+      __syncwarp();
+      for (int c = lane; c < BC; c += 32) {
+        const long long cb = colbase[c];
+        if (cb < 0) continue;
+        for (int q = 0; q < nr; ++q) {
+          const int i0 = runs[2 * q], len = runs[2 * q + 1];
+          bulk_g2s(sCt + c * CP + i0, a.C + cb + rowphys[i0], (unsigned)len * 8u, &tfull[b]);
+        }
+      }
+      // operand k-chunks
+      for (int kb = 0; kb < a.n_k; ++kb) {
+        if (lane == 0) mbar_wait(&empty[stage], ephase ^ 1);
+        __syncwarp();
+        double* dR = sR + stage * BR * KC;
+        double* dC = sCc + stage * BC * KC;
+        // c-side runs of W rows
+        if (lane == 0) {
+          unsigned bytes = BR * KC * 8;
+          int c = 0;
+          while (c < BC) {
+            const int w0 = cw[c] >= 0 ? cw[c] : 0;
+            int j = c + 1;
+            while (j < BC && (cw[j] >= 0 ? cw[j] : 0) == (cw[j - 1] >= 0 ? cw[j - 1] : 0) + 1) ++j;
+            bytes += (unsigned)(j - c) * KC * 8;
+            c = j;
+            (void)w0;
+          }
+          mbar_expect_tx(&full[stage], bytes);
+          bulk_g2s(dR, a.Wt + ((size_t)kb * a.mpad + r0) * KC, BR * KC * 8, &full[stage]);
+          c = 0;
+          while (c < BC) {
+            const int w0 = cw[c] >= 0 ? cw[c] : 0;
+            int j = c + 1;
+            while (j < BC && (cw[j] >= 0 ? cw[j] : 0) == (cw[j - 1] >= 0 ? cw[j - 1] : 0) + 1) ++j;
+            bulk_g2s(dC + c * KC, a.Wnt + ((size_t)kb * a.mpad + w0) * KC, (unsigned)(j - c) * KC * 8,
+                     &full[stage]);
+            c = j;
+          }
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          ephase ^= 1;
+        }
+      }
+    }
+    return;
   }
 
-  const int warp = tid >> 5, lane = tid & 31;
+  // ================================ consumers ================================
   const int g = lane >> 2, t = lane & 3;
   const int wr = (warp & 3) * 32;   // r-side offset of this warp
   const int wc = (warp >> 2) * 32;  // c-side offset of this warp
-  double acc[4][4][2];
+  int stage = 0;
+  unsigned fphase = 0;
+  int it = 0;
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+    const int b = it & 1;
+    mbar_wait(&tfull[b], (it >> 1) & 1);
+    double acc[4][4][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-  for (int kb = 0; kb < n_k; ++kb) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    {
-      const int nk = kb + STAGES - 1;
-      if (nk < n_k) load_stage(nk % STAGES, nk * KC);
-      cp_async_commit();
-    }
-    const double* tR = sR + (kb % STAGES) * BR * LDK;
-    const double* tC = sC + (kb % STAGES) * BC * LDK;
+      for (int j = 0; j < 4; ++j) {
+        const double2 v =
+            *reinterpret_cast<const double2*>(sCt + (wc + i * 8 + g) * CP + wr + j * 8 + 2 * t);
+        acc[i][j][0] = v.x;
+        acc[i][j][1] = v.y;
+      }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(cempty);
+    for (int kb = 0; kb < a.n_k; ++kb) {
+      mbar_wait(&full[stage], fphase);
+      const double* tR = sR + stage * BR * KC;
+      const double* tC = sCc + stage * BC * KC;
 #pragma unroll
-    for (int k4 = 0; k4 < KC / 4; ++k4) {
-      double fa[4], fb[4];
+      for (int k4 = 0; k4 < KC / 4; ++k4) {
+        double fa[4], fb[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) fa[i] = tC[(wc + i * 8 + g) * LDK + k4 * 4 + t];
+        for (int i = 0; i < 4; ++i) {
+          const int row = wc + i * 8 + g;
+          fa[i] = tC[row * KC + (((k4 + row) & 3) << 2) + t];
+        }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) fb[j] = tR[(wr + j * 8 + g) * LDK + k4 * 4 + t];
+        for (int j = 0; j < 4; ++j) {
+          const int row = wr + j * 8 + g;
+          fb[j] = tR[row * KC + (((k4 + row) & 3) << 2) + t];
+        }
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma884(acc[i][j], fa[i], fb[j]);
-    }
-  }
-  cp_async_wait<0>();
-
-  // epilogue: acc[i][j] = (W W^T)[c][r], [r], [r+1]; C[r, c] -= acc
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int cl = wc + i * 8 + g;
-    const long long cb = colbase[cl];
-    if (cb < 0) continue;
-    double* col = a.C + cb;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int rl = wr + j * 8 + 2 * t;
-      const int p0 = rowphys[rl];
-      if (p0 < 0) continue;
-      if (VEC == 2) {
-        double2* ptr = reinterpret_cast<double2*>(col + p0);
-        double2 v = *ptr;
-        v.x -= acc[i][j][0];
-        v.y -= acc[i][j][1];
-        *ptr = v;
-      } else {
-        col[p0] -= acc[i][j][0];
-        const int p1 = rowphys[rl + 1];
-        if (p1 >= 0) col[p1] -= acc[i][j][1];
+          for (int j = 0; j < 4; ++j) dmma884(acc[i][j], fa[i], fb[j]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == STAGES) {
+        stage = 0;
+        fphase ^= 1;
       }
     }
+    const long long* colbase = colbase_of(b);
+    const int* rowphys = rowphys_of(b);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const long long cb = colbase[wc + i * 8 + g];
+      if (cb < 0) continue;
+      double* col = a.C + cb;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int p0 = rowphys[wr + j * 8 + 2 * t];
+        if (p0 < 0) continue;
+        __stcs(reinterpret_cast<double2*>(col + p0), make_double2(acc[i][j][0], acc[i][j][1]));
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&mempty[b]);
   }
 }
 
@@ -236,6 +596,10 @@ struct PanelArgs {
   const double* Linv;   // row-major [c][m], ld = ldl, zero above the diagonal and in pads
   int ldl;
   double* W;            // out, row-major, ld = ldw
+  double* Wn;           // out, -W (same layout); may be null
+  double* Wt;           // out, +W tiled (wt_index); may be null
+  double* Wnt;          // out, -W tiled; may be null
+  int mpad;             // rows of the tiled buffers
   int ldw;
   const int* row_pos;   // compact block -> position
   int nt;
@@ -349,6 +713,13 @@ __global__ void __launch_bounds__(pw::THREADS, 2) panel_w_kernel(PanelArgs a) {
         v.x = acc[i][j][0];
         v.y = c + 1 < nt ? acc[i][j][1] : 0.0;
         *reinterpret_cast<double2*>(a.W + (size_t)r * a.ldw + c) = v;
+        if (a.Wn)
+          *reinterpret_cast<double2*>(a.Wn + (size_t)r * a.ldw + c) = make_double2(-v.x, -v.y);
+        if (a.Wt) {
+          const size_t o = wt_index(r, c, a.mpad);
+          *reinterpret_cast<double2*>(a.Wt + o) = v;
+          *reinterpret_cast<double2*>(a.Wnt + o) = make_double2(-v.x, -v.y);
+        }
       }
     }
   }
