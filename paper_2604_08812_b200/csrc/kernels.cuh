@@ -295,7 +295,7 @@ constexpr size_t OFF_CT = OFF_C + (size_t)STAGES * BC * KC * 8;
 constexpr size_t OFF_MAPS = OFF_CT + (size_t)BC * CP * 8;                // 2 x {colbase[BC], rowphys[BR]}
 constexpr size_t MAPS_BYTES = (size_t)BC * 8 + BR * 4;
 constexpr size_t OFF_RUNS = OFF_MAPS + 2 * MAPS_BYTES;                   // producer scratch
-constexpr size_t OFF_BAR = OFF_RUNS + (size_t)(BC + BR + 8) * 8;
+constexpr size_t OFF_BAR = OFF_RUNS + (size_t)(2 * BC + BR + 8) * 8;
 constexpr size_t SMEM = OFF_BAR + 16 * 8;
 }  // namespace ws
 
@@ -392,6 +392,8 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
 
   if (warp == CONSUMERS / 32) {
     // =============================== producer ===============================
+    int* rrun = runs;            // [BR+1] row-run starts (then the end)
+    int* crun = runs + BR + 1;   // [BC+1] c-side run starts (then the end)
     int stage = 0;
     unsigned ephase = 0;
     int it = 0;
@@ -406,96 +408,106 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
         r0 = (within / gw) * BR;
         c0 = (ct0 + within % gw) * BC;
       }
+      const int nrv = min(BR, a.n_rows - r0);  // valid rows of the tile
+      const int ncv = min(BC, a.n_cols - c0);  // valid columns
       const int b = it & 1;
       if (it >= 2) mbar_wait(&mempty[b], ((it >> 1) - 1) & 1);
       long long* colbase = colbase_of(b);
       int* rowphys = rowphys_of(b);
-      for (int i = lane; i < BR; i += 32) {
+      int rp[BR / 32];
+#pragma unroll
+      for (int m = 0; m < BR / 32; ++m) {
+        const int i = lane + 32 * m;
         const int r = r0 + i;
-        if (r < a.n_rows) {
+        if (i < nrv) {
           const int blk = r / nt;
-          rowphys[i] = a.row_pos[blk] * nt + (r - blk * nt);
+          rp[m] = a.row_pos[blk] * nt + (r - blk * nt);
         } else {
-          rowphys[i] = -1;
+          rp[m] = -1;
         }
+        rowphys[i] = rp[m];
       }
-      for (int i = lane; i < BC; i += 32) {
+      int cwl[BC / 32];
+#pragma unroll
+      for (int m = 0; m < BC / 32; ++m) {
+        const int i = lane + 32 * m;
         const int c = c0 + i;
-        if (c < a.n_cols) {
+        if (i < ncv) {
           const int blk = c / nt;
           const int off = c - blk * nt;
           colbase[i] = (long long)(a.col_slot[blk] * nt + off) * a.ldc;
-          cw[i] = a.col_g[blk] * nt + off;
+          cwl[m] = a.col_g[blk] * nt + off;
         } else {
           colbase[i] = -1;
-          cw[i] = -1;
+          cwl[m] = 0;  // columns past the edge read W row 0 (never stored)
         }
+        cw[i] = cwl[m];
       }
       __syncwarp();
-      // row runs of the tile (contiguous physical rows) -- same for every column
+      // run starts via ballots: a run breaks where the source row is not the
+      // previous one + 1 (candidate-block boundaries in the compact order)
+      unsigned rmask[BR / 32], cmask[BC / 32];
+#pragma unroll
+      for (int m = 0; m < BR / 32; ++m) {
+        const int i = lane + 32 * m;
+        const bool s = i < nrv && (i == 0 || rowphys[i - 1] + 1 != rp[m]);
+        rmask[m] = __ballot_sync(0xffffffffu, s);
+      }
+#pragma unroll
+      for (int m = 0; m < BC / 32; ++m) {
+        const int i = lane + 32 * m;
+        const bool s = i == 0 || cw[i - 1] + 1 != cwl[m];
+        cmask[m] = __ballot_sync(0xffffffffu, s);
+      }
+      int nrr = 0, ncr = 0;
       if (lane == 0) {
-        int nr = 0, i = 0;
-        while (i < BR && rowphys[i] >= 0) {
-          int j = i + 1;
-          while (j < BR && rowphys[j] == rowphys[j - 1] + 1) ++j;
-          runs[2 * nr] = i;
-          runs[2 * nr + 1] = j - i;
-          ++nr;
-          i = j;
+#pragma unroll
+        for (int m = 0; m < BR / 32; ++m) {
+          unsigned x = rmask[m];
+          while (x) {
+            const int bpos = __ffs(x) - 1;
+            x &= x - 1;
+            rrun[nrr++] = 32 * m + bpos;
+          }
         }
-        runs[2 * BR] = nr;  // count slot (runs array sized BR pairs + 1)
+        rrun[nrr] = nrv;
+#pragma unroll
+        for (int m = 0; m < BC / 32; ++m) {
+          unsigned x = cmask[m];
+          while (x) {
+            const int bpos = __ffs(x) - 1;
+            x &= x - 1;
+            crun[ncr++] = 32 * m + bpos;
+          }
+        }
+        crun[ncr] = BC;
       }
+      nrr = __shfl_sync(0xffffffffu, nrr, 0);
+      ncr = __shfl_sync(0xffffffffu, ncr, 0);
       __syncwarp();
-      const int nr = runs[2 * BR];
-      // C tile of this tile -> sCt (wait until consumers copied the previous one)
+      // C tile -> sCt once consumers copied the previous tile to registers
       if (it >= 1) mbar_wait(cempty, (it - 1) & 1);
-      if (lane == 0) {
-        unsigned bytes = 0;
-        int ncols = 0;
-        for (int c = 0; c < BC; ++c) ncols += colbase[c] >= 0;
-        for (int q = 0; q < nr; ++q) bytes += (unsigned)runs[2 * q + 1] * 8u;
-        mbar_expect_tx(&tfull[b], bytes * (unsigned)ncols);
-      }
+      if (lane == 0) mbar_expect_tx(&tfull[b], (unsigned)(nrv * ncv) * 8u);
       __syncwarp();
-      for (int c = lane; c < BC; c += 32) {
-        const long long cb = colbase[c];
-        if (cb < 0) continue;
-        for (int q = 0; q < nr; ++q) {
-          const int i0 = runs[2 * q], len = runs[2 * q + 1];
-          bulk_g2s(sCt + c * CP + i0, a.C + cb + rowphys[i0], (unsigned)len * 8u, &tfull[b]);
-        }
+      for (int p = lane; p < ncv * nrr; p += 32) {
+        const int c = p / nrr, q = p - c * nrr;
+        const int i0 = rrun[q], len = rrun[q + 1] - i0;
+        bulk_g2s(sCt + c * CP + i0, a.C + colbase[c] + rowphys[i0], (unsigned)len * 8u, &tfull[b]);
       }
-      // operand k-chunks
+      // operand k-chunks: r-side one contiguous tile, c-side one copy per run
       for (int kb = 0; kb < a.n_k; ++kb) {
-        if (lane == 0) mbar_wait(&empty[stage], ephase ^ 1);
-        __syncwarp();
-        double* dR = sR + stage * BR * KC;
-        double* dC = sCc + stage * BC * KC;
-        // c-side runs of W rows
         if (lane == 0) {
-          unsigned bytes = BR * KC * 8;
-          int c = 0;
-          while (c < BC) {
-            const int w0 = cw[c] >= 0 ? cw[c] : 0;
-            int j = c + 1;
-            while (j < BC && (cw[j] >= 0 ? cw[j] : 0) == (cw[j - 1] >= 0 ? cw[j - 1] : 0) + 1) ++j;
-            bytes += (unsigned)(j - c) * KC * 8;
-            c = j;
-            (void)w0;
-          }
-          mbar_expect_tx(&full[stage], bytes);
-          bulk_g2s(dR, a.Wt + ((size_t)kb * a.mpad + r0) * KC, BR * KC * 8, &full[stage]);
-          c = 0;
-          while (c < BC) {
-            const int w0 = cw[c] >= 0 ? cw[c] : 0;
-            int j = c + 1;
-            while (j < BC && (cw[j] >= 0 ? cw[j] : 0) == (cw[j - 1] >= 0 ? cw[j - 1] : 0) + 1) ++j;
-            bulk_g2s(dC + c * KC, a.Wnt + ((size_t)kb * a.mpad + w0) * KC, (unsigned)(j - c) * KC * 8,
-                     &full[stage]);
-            c = j;
-          }
+          mbar_wait(&empty[stage], ephase ^ 1);
+          mbar_expect_tx(&full[stage], (unsigned)(BR + BC) * KC * 8u);
+          bulk_g2s(sR + stage * BR * KC, a.Wt + ((size_t)kb * a.mpad + r0) * KC, BR * KC * 8,
+                   &full[stage]);
         }
         __syncwarp();
+        for (int q = lane; q < ncr; q += 32) {
+          const int i0 = crun[q], len = crun[q + 1] - i0;
+          bulk_g2s(sCc + stage * BC * KC + i0 * KC, a.Wnt + ((size_t)kb * a.mpad + cw[i0]) * KC,
+                   (unsigned)len * KC * 8u, &full[stage]);
+        }
         if (++stage == STAGES) {
           stage = 0;
           ephase ^= 1;
