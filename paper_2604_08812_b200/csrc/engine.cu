@@ -160,10 +160,6 @@ __global__ void gain_tables_kernel(const int* col_slot, int n, int G, int rank, 
   sensor[b] = pos_sensor[p];
 }
 
-__global__ void fixed_tables_kernel(int col, int row, int* src_col, int* src_row) {
-  src_col[0] = col;
-  src_row[0] = row;
-}
 
 // forced winner: record with that sensor's gain (if local & feasible)
 __global__ void pick_kernel(const double* gain, const int* status, const int* sensor, int n,
@@ -213,15 +209,21 @@ struct GainTabs {
 };
 
 // panel width of the gain kernel: two NB x mp panels must fit in 227 KB
-int chol_nb(int nt) { return nt <= 440 ? 32 : (nt <= 900 ? 16 : 8); }
+int chol_nb(int nt) { return nt <= 440 ? 32 : 8; }
+
+// smem pitch of the gain kernel panels: >= nt rounded to 8, == 4 or 12 mod 16
+// so the DMMA fragment loads are bank-conflict free
+int chol_mp(int nt) {
+  int mp = round_up(nt, 8);
+  if (mp % 16 == 0 || mp % 16 == 8) mp += 4;
+  return mp;
+}
 
 void launch_chol(const CholArgs& a, int n_batch, cudaStream_t s) {
   const int nb = chol_nb(a.nt);
   const size_t smem = (size_t)2 * nb * a.mp * sizeof(double);
   if (nb == 32)
     chol_logdet_kernel<32><<<n_batch, 256, smem, s>>>(a);
-  else if (nb == 16)
-    chol_logdet_kernel<16><<<n_batch, 256, smem, s>>>(a);
   else
     chol_logdet_kernel<8><<<n_batch, 256, smem, s>>>(a);
 }
@@ -248,34 +250,12 @@ void run_gain(dsel_engine* e, const int* slots, int n_batch) {
   a.status = e->status;
   a.nt = e->nt;
   a.n = n_batch;
-  a.mp = round_up(e->nt, 2);
+  a.mp = chol_mp(e->nt);
   launch_chol(a, n_batch, e->s);
   CU(cudaGetLastError());
   e->launches += 2;
 }
 
-void chol_winner(dsel_engine* e, const double* panel, long long ldp, int pos) {
-  // batch of one: block rows pos*nt of the panel, panel columns 0..nt
-  GainTabs t = gain_tabs(e);
-  int* fc = t.src_col + e->nloc;  // spare slot at the end of each table
-  int* fr = t.src_row + e->nloc;
-  fixed_tables_kernel<<<1, 1, 0, e->s>>>(0, pos * e->nt, fc, fr);
-  CholArgs a;
-  a.src = panel;
-  a.lds = ldp;
-  a.src_col = fc;
-  a.src_row = fr;
-  a.L = e->Lk;
-  a.l_stride = (long long)e->nt * e->nt;
-  a.gain = e->kgain;
-  a.status = e->kstatus;
-  a.nt = e->nt;
-  a.n = 1;
-  a.mp = round_up(e->nt, 2);
-  launch_chol(a, 1, e->s);
-  CU(cudaGetLastError());
-  e->launches += 2;
-}
 
 template <class K>
 void allow_smem(K kernel, int optin) {
@@ -290,7 +270,6 @@ void set_smem_limits(int dev) {
   int optin = 0;
   CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   allow_smem(chol_logdet_kernel<32>, optin);
-  allow_smem(chol_logdet_kernel<16>, optin);
   allow_smem(chol_logdet_kernel<8>, optin);
   allow_smem(schur_update_kernel<2>, optin);
   allow_smem(schur_update_kernel<1>, optin);
@@ -378,15 +357,32 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   const int owner = p % e->G;
   const int q = p / e->G;
 
-  // ---- panel: broadcast C[:,k] from its owner; chol(C_kk); W ----
+  // ---- panel: broadcast C[:,k] and L_k = chol(C_kk) from the owner ----
+  // The owner's gain kernel already factored C_kk (scratch slot bidx); every
+  // rank uses those exact bits (broadcast), so no rank refactors.
   double* P = nullptr;
-  if (!last || e->export_factor) {
+  const double* Lk = e->Lk;
+  if (owner == e->rank) {
+    int bidx = -1;
+    const int* cs = e->h_tab + e->nc;
+    for (int h = 0; h < e->n_cols_tab; ++h)
+      if (cs[h] == q) bidx = h;
+    if (bidx < 0) throw Fail{DSEL_E_STATE, "winner not in the local gain batch"};
+    const double* lsrc = e->Lscr + (size_t)bidx * nt * nt;
+    if (e->G > 1 && !last)
+      CU(cudaMemcpyAsync(e->Lk, lsrc, sizeof(double) * nt * nt, cudaMemcpyDeviceToDevice, e->s));
+    else
+      Lk = lsrc;
+  }
+  if (!last) {
     P = (owner == e->rank) ? e->C + (size_t)q * nt * e->n : e->Pbuf;
-    if (e->G > 1 && !last) {
+    if (e->G > 1) {
+      NC(ncclGroupStart());
       NC(ncclBroadcast(P, P, (size_t)e->n * nt, ncclDouble, owner, e->comm, e->s));
-      bytes += (uint64_t)e->n * nt * sizeof(double) * (uint64_t)(e->G - 1);
+      NC(ncclBroadcast(e->Lk, e->Lk, (size_t)nt * nt, ncclDouble, owner, e->comm, e->s));
+      NC(ncclGroupEnd());
+      bytes += (uint64_t)(e->n + nt) * nt * sizeof(double) * (uint64_t)(e->G - 1);
     }
-    if (!last || owner == e->rank) chol_winner(e, P, e->n, p);
   }
   e->alive[p] = 0;
   e->n_alive -= 1;
@@ -396,7 +392,7 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   if (!last) {
     const int tb = 256 / 32;
     trinv_kernel<<<(e->ldw + tb - 1) / tb, 256, (size_t)tb * e->ldw * sizeof(double), e->s>>>(
-        e->Lk, nt, e->Linv, e->ldw);
+        Lk, nt, e->Linv, e->ldw);
     CU(cudaGetLastError());
     e->launches += 1;
     if (R > 0) {
@@ -435,7 +431,7 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
     }
     if (owner == e->rank) {
       hist_diag_kernel<<<(unsigned)std::min<long long>((n2 + 255) / 256, 1024), 256, 0, e->s>>>(
-          e->Lk, nt, e->hist + (long long)q * slot_stride + (long long)round * n2);
+          Lk, nt, e->hist + (long long)q * slot_stride + (long long)round * n2);
       CU(cudaGetLastError());
       e->launches += 1;
     }

@@ -112,7 +112,7 @@ __device__ __forceinline__ void tile_coords(const UpdateArgs& a, int tile, int& 
 template <int VEC>
 __global__ void __launch_bounds__(upd::THREADS, 1) schur_update_kernel(UpdateArgs a) {
   using namespace upd;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int wg = threadIdx.x / WG;       // warpgroup 0 / 1
   const int tid = threadIdx.x % WG;      // thread within the warpgroup
   unsigned char* base = smem_raw + (size_t)wg * WG_SMEM;
@@ -621,7 +621,7 @@ struct PanelArgs {
 template <int VEC>
 __global__ void __launch_bounds__(pw::THREADS, 2) panel_w_kernel(PanelArgs a) {
   using namespace pw;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sA = reinterpret_cast<double*>(smem_raw);  // [STAGES][KC][LDA]
   double* sB = sA + STAGES * KC * LDA;                // [STAGES][BN][LDB]
   int* rowphys = reinterpret_cast<int*>(sB + STAGES * BN * LDB);
@@ -760,7 +760,8 @@ struct CholArgs {
 
 template <int NB>
 __global__ void __launch_bounds__(256) chol_logdet_kernel(CholArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  static_assert(NB % 8 == 0, "panel width");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int b = blockIdx.x;
   if (b >= a.n) return;
   const int nt = a.nt, mp = a.mp;
@@ -769,8 +770,10 @@ __global__ void __launch_bounds__(256) chol_logdet_kernel(CholArgs a) {
   __shared__ double s_logsum;
   __shared__ int s_fail;
   const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
   const double* src = a.src + (size_t)a.src_col[b] * a.lds + a.src_row[b];
-  double* L = a.L + (size_t)b * a.l_stride;
+  double* L = a.L + (size_t)b * a.l_stride;  // column-major nt x nt
   if (tid == 0) {
     s_logsum = 0.0;
     s_fail = -1;
@@ -778,64 +781,59 @@ __global__ void __launch_bounds__(256) chol_logdet_kernel(CholArgs a) {
   for (int J0 = 0; J0 < nt; J0 += NB) {
     const int nb = min(NB, nt - J0);
     const int m = nt - J0;
-    // load panel rows J0..nt, cols J0..J0+nb
     for (int j = 0; j < nb; ++j)
-      for (int i = tid; i < m; i += blockDim.x) S[j * mp + i] = src[(size_t)(J0 + j) * a.lds + J0 + i];
-    // left-looking update with previous factor columns
+      for (int i = tid; i < m; i += 256) S[j * mp + i] = src[(size_t)(J0 + j) * a.lds + J0 + i];
+    // left-looking: S -= L[J0:, kk:kk+NB] * L[J0:J0+nb, kk:kk+NB]^T on DMMA
     for (int kk = 0; kk < J0; kk += NB) {
-      const int kw = min(NB, J0 - kk);
       __syncthreads();
-      for (int c = 0; c < kw; ++c)
-        for (int i = tid; i < m; i += blockDim.x) Lc[c * mp + i] = L[(size_t)(kk + c) * nt + J0 + i];
+      for (int c = 0; c < NB; ++c)
+        for (int i = tid; i < m; i += 256) Lc[c * mp + i] = L[(size_t)(kk + c) * nt + J0 + i];
       __syncthreads();
-      for (int i = tid; i < m; i += blockDim.x) {
-        double acc[NB];
+      const int mt_n = (m + 7) >> 3;
+      constexpr int NT8 = NB / 8;
+      for (int tt = warp; tt < mt_n * NT8; tt += 8) {
+        const int mt = tt / NT8, n8 = tt - mt * NT8;
+        double acc[2] = {0.0, 0.0};
 #pragma unroll
-        for (int j = 0; j < NB; ++j) acc[j] = 0.0;
-        for (int c = 0; c < kw; ++c) {
-          const double x = Lc[c * mp + i];
-#pragma unroll
-          for (int j = 0; j < NB; ++j) acc[j] += x * Lc[c * mp + j];
+        for (int k4 = 0; k4 < NB / 4; ++k4) {
+          const double av = Lc[(k4 * 4 + t) * mp + mt * 8 + g];
+          const double bv = Lc[(k4 * 4 + t) * mp + n8 * 8 + g];
+          dmma884(acc, av, bv);
         }
-#pragma unroll
-        for (int j = 0; j < NB; ++j)
-          if (j < nb) S[j * mp + i] -= acc[j];
+        const int i = mt * 8 + g, j0 = n8 * 8 + 2 * t;
+        if (i < m) {
+          if (j0 < nb) S[j0 * mp + i] -= acc[0];
+          if (j0 + 1 < nb) S[(j0 + 1) * mp + i] -= acc[1];
+        }
       }
     }
-    __syncthreads();
-    // factor the panel: unblocked right-looking over its nb columns
+    // factor the panel: unblocked right-looking, 2-D parallel trailing update
     for (int j = 0; j < nb; ++j) {
+      __syncthreads();
       const double piv = S[j * mp + j];
-      const bool bad = !(piv > 0.0) || !isfinite(piv);
-      if (bad) {
+      if (!(piv > 0.0) || !isfinite(piv)) {
         if (tid == 0) s_fail = J0 + j;
         break;
       }
       const double d = sqrt(piv);
-      double lij[4];
-      int cnt = 0;
-      for (int i = j + 1 + tid; i < m; i += blockDim.x) lij[cnt++ & 3] = S[j * mp + i] / d;
-      __syncthreads();
-      cnt = 0;
-      for (int i = j + 1 + tid; i < m; i += blockDim.x) S[j * mp + i] = lij[cnt++ & 3];
+      for (int i = j + 1 + tid; i < m; i += 256) S[j * mp + i] /= d;
       if (tid == 0) {
         S[j * mp + j] = d;
         s_logsum += log(d);
       }
       __syncthreads();
-      for (int i = j + 1 + tid; i < m; i += blockDim.x) {
-        const double li = S[j * mp + i];
-        const int cmax = min(nb - 1, i);
-        for (int c = j + 1; c <= cmax; ++c) S[c * mp + i] -= li * S[j * mp + c];
+      const int cl = tid >> 6, il = tid & 63;
+      for (int c = j + 1 + cl; c < nb; c += 4) {
+        const double ljc = S[j * mp + c];
+        for (int i = c + il; i < m; i += 64) S[c * mp + i] -= S[j * mp + i] * ljc;
       }
-      __syncthreads();
     }
     __syncthreads();
     if (s_fail >= 0) break;
     for (int j = 0; j < nb; ++j)
-      for (int i = tid; i < m; i += blockDim.x) L[(size_t)(J0 + j) * nt + J0 + i] = S[j * mp + i];
-    __syncthreads();
+      for (int i = tid; i < m; i += 256) L[(size_t)(J0 + j) * nt + J0 + i] = S[j * mp + i];
   }
+  __syncthreads();
   if (tid == 0) {
     a.status[b] = s_fail;
     a.gain[b] = s_fail >= 0 ? -INFINITY : 2.0 * s_logsum;
@@ -847,7 +845,7 @@ __global__ void __launch_bounds__(256) chol_logdet_kernel(CholArgs a) {
 // with zeros above the diagonal and in the pad (ld = ldl). Warp per column. //
 // ------------------------------------------------------------------------ //
 __global__ void __launch_bounds__(256) trinv_kernel(const double* L, int nt, double* Linv, int ldl) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int j = blockIdx.x * (blockDim.x >> 5) + wib;  // column of Linv
