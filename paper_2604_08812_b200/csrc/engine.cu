@@ -209,7 +209,7 @@ struct GainTabs {
 };
 
 // panel width of the gain kernel: two NB x mp panels must fit in 227 KB
-int chol_nb(int nt) { return nt <= 440 ? 32 : 8; }
+int chol_nb(int nt) { return nt <= 436 ? 32 : 8; }
 
 // smem pitch of the gain kernel panels: >= nt rounded to 8, == 4 or 12 mod 16
 // so the DMMA fragment loads are bank-conflict free
@@ -221,7 +221,7 @@ int chol_mp(int nt) {
 
 void launch_chol(const CholArgs& a, int n_batch, cudaStream_t s) {
   const int nb = chol_nb(a.nt);
-  const size_t smem = (size_t)2 * nb * a.mp * sizeof(double);
+  const size_t smem = ((size_t)2 * nb * a.mp + a.nt) * sizeof(double);
   if (nb == 32)
     chol_logdet_kernel<32><<<n_batch, 256, smem, s>>>(a);
   else

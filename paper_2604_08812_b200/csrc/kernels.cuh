@@ -40,6 +40,14 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pre
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
 }
 
+// shared-memory load the compiler may not hoist (keeps loop-invariant
+// broadcast operands in smem instead of hundreds of registers)
+__device__ __forceinline__ double lds_volatile(const double* p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 
 template <int N>
@@ -760,34 +768,41 @@ struct CholArgs {
 
 template <int NB>
 __global__ void __launch_bounds__(256) chol_logdet_kernel(CholArgs a) {
-  static_assert(NB % 8 == 0, "panel width");
+  static_assert(NB % 8 == 0 && NB <= 32, "panel width");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int b = blockIdx.x;
   if (b >= a.n) return;
   const int nt = a.nt, mp = a.mp;
   double* S = reinterpret_cast<double*>(smem_raw);  // [NB][mp] panel, column-major
   double* Lc = S + NB * mp;                         // [NB][mp] staged factor columns
-  __shared__ double s_logsum;
+  double* diagv = Lc + NB * mp;                     // [nt] pivots sqrt
   __shared__ int s_fail;
+  __shared__ double s_red[8];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const double* src = a.src + (size_t)a.src_col[b] * a.lds + a.src_row[b];
   double* L = a.L + (size_t)b * a.l_stride;  // column-major nt x nt
-  if (tid == 0) {
-    s_logsum = 0.0;
-    s_fail = -1;
-  }
+  if (tid == 0) s_fail = -1;
   for (int J0 = 0; J0 < nt; J0 += NB) {
     const int nb = min(NB, nt - J0);
     const int m = nt - J0;
-    for (int j = 0; j < nb; ++j)
-      for (int i = tid; i < m; i += 256) S[j * mp + i] = src[(size_t)(J0 + j) * a.lds + J0 + i];
+    // async gathers (all loads in flight at once; one latency per stage)
+    __syncthreads();  // previous panel's readers of S are done
+    for (int e = tid; e < nb * m; e += 256) {
+      const int j = e / m, i = e - j * m;
+      cp_async8(S + j * mp + i, src + (size_t)(J0 + j) * a.lds + J0 + i, true);
+    }
+    cp_async_commit();
     // left-looking: S -= L[J0:, kk:kk+NB] * L[J0:J0+nb, kk:kk+NB]^T on DMMA
     for (int kk = 0; kk < J0; kk += NB) {
       __syncthreads();
-      for (int c = 0; c < NB; ++c)
-        for (int i = tid; i < m; i += 256) Lc[c * mp + i] = L[(size_t)(kk + c) * nt + J0 + i];
+      for (int e = tid; e < NB * m; e += 256) {
+        const int c = e / m, i = e - c * m;
+        cp_async8(Lc + c * mp + i, L + (size_t)(kk + c) * nt + J0 + i, true);
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
       __syncthreads();
       const int mt_n = (m + 7) >> 3;
       constexpr int NT8 = NB / 8;
@@ -807,36 +822,75 @@ __global__ void __launch_bounds__(256) chol_logdet_kernel(CholArgs a) {
         }
       }
     }
-    // factor the panel: unblocked right-looking, 2-D parallel trailing update
-    for (int j = 0; j < nb; ++j) {
-      __syncthreads();
-      const double piv = S[j * mp + j];
-      if (!(piv > 0.0) || !isfinite(piv)) {
-        if (tid == 0) s_fail = J0 + j;
-        break;
+    cp_async_wait<0>();
+    __syncthreads();
+    // (1) diagonal nb x nb block: one warp, right-looking in shared memory,
+    //     lane l owns row l (warp-synchronous, no block barriers)
+    if (warp == 0) {
+      int fail = -1;
+      for (int j = 0; j < nb; ++j) {
+        const double piv = S[j * mp + j];
+        const bool bad = !(piv > 0.0) || !isfinite(piv);
+        if (bad) {
+          fail = j;
+          break;
+        }
+        const double d = sqrt(piv);
+        const double rd = 1.0 / d;
+        __syncwarp();
+        double lj = 0.0;
+        if (lane > j && lane < nb) {
+          lj = S[j * mp + lane] * rd;
+          S[j * mp + lane] = lj;
+        }
+        if (lane == j) {
+          S[j * mp + j] = d;
+          diagv[J0 + j] = d;
+        }
+        __syncwarp();
+        if (lane > j && lane < nb)
+          for (int c = j + 1; c <= lane; ++c) S[c * mp + lane] -= lj * S[j * mp + c];
+        __syncwarp();
       }
-      const double d = sqrt(piv);
-      for (int i = j + 1 + tid; i < m; i += 256) S[j * mp + i] /= d;
-      if (tid == 0) {
-        S[j * mp + j] = d;
-        s_logsum += log(d);
-      }
-      __syncthreads();
-      const int cl = tid >> 6, il = tid & 63;
-      for (int c = j + 1 + cl; c < nb; c += 4) {
-        const double ljc = S[j * mp + c];
-        for (int i = c + il; i < m; i += 64) S[c * mp + i] -= S[j * mp + i] * ljc;
-      }
+      if (lane == 0 && fail >= 0) s_fail = J0 + fail;
     }
     __syncthreads();
     if (s_fail >= 0) break;
-    for (int j = 0; j < nb; ++j)
-      for (int i = tid; i < m; i += 256) L[(size_t)(J0 + j) * nt + J0 + i] = S[j * mp + i];
+    // (2) panel rows below the diagonal block: forward substitution
+    //     x L_dd^T = s per row (one thread per row, in place in shared memory)
+    for (int i = nb + tid; i < m; i += 256) {
+      for (int j = 0; j < nb; ++j) {
+        const double xj = S[j * mp + i] / S[j * mp + j];
+        S[j * mp + i] = xj;
+        for (int c = j + 1; c < nb; ++c) S[c * mp + i] -= xj * S[j * mp + c];
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < nb * m; e += 256) {
+      const int j = e / m, i = e - j * m;
+      L[(size_t)(J0 + j) * nt + J0 + i] = S[j * mp + i];
+    }
   }
   __syncthreads();
+  if (s_fail >= 0) {
+    if (tid == 0) {
+      a.status[b] = s_fail;
+      a.gain[b] = -INFINITY;
+    }
+    return;
+  }
+  // log det = 2 sum log(d_j): fixed-order (deterministic) reduction
+  double part = 0.0;
+  for (int j = tid; j < nt; j += 256) part += log(diagv[j]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
+  if (lane == 0) s_red[warp] = part;
+  __syncthreads();
   if (tid == 0) {
-    a.status[b] = s_fail;
-    a.gain[b] = s_fail >= 0 ? -INFINITY : 2.0 * s_logsum;
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += s_red[w];
+    a.status[b] = -1;
+    a.gain[b] = 2.0 * s;
   }
 }
 
