@@ -275,7 +275,6 @@ void set_smem_limits(int dev) {
   allow_smem(schur_update_kernel<1>, optin);
   allow_smem(panel_w_kernel<2>, optin);
   allow_smem(panel_w_kernel<1>, optin);
-  allow_smem(trinv_kernel, optin);
   allow_smem(schur_update_ws_kernel, optin);
 }
 
@@ -391,8 +390,18 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   double flops = 0.0;
   if (!last) {
     const int tb = 256 / 32;
-    trinv_kernel<<<(e->ldw + tb - 1) / tb, 256, (size_t)tb * e->ldw * sizeof(double), e->s>>>(
-        Lk, nt, e->Linv, e->ldw);
+    {
+      const unsigned g = (unsigned)((e->ldw + tb - 1) / tb);
+      const size_t sm = (size_t)nt * sizeof(double);
+      if (e->ldw <= 128)
+        trinv_kernel<4><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+      else if (e->ldw <= 256)
+        trinv_kernel<8><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+      else if (e->ldw <= 512)
+        trinv_kernel<16><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+      else
+        trinv_kernel<32><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+    }
     CU(cudaGetLastError());
     e->launches += 1;
     if (R > 0) {

@@ -766,6 +766,56 @@ struct CholArgs {
   int mp;                   // smem pitch (>= nt)
 };
 
+// Register-resident, compile-time-unrolled pieces of the panel factorization
+// (template recursion guarantees constant indices, so r[]/s[] stay in registers).
+template <int J, int C, int NB>
+__device__ __forceinline__ void diag_upd(double (&r)[NB], int lane) {
+  if constexpr (C < NB) {
+    const double lcj = __shfl_sync(0xffffffffu, r[J], C);
+    if (lane >= C) r[C] -= r[J] * lcj;
+    diag_upd<J, C + 1, NB>(r, lane);
+  }
+}
+// lane l owns row l of the (identity-padded) NB x NB diagonal block
+template <int J, int NB>
+__device__ __forceinline__ void diag_step(double (&r)[NB], int lane, int nb, double* dv, double* rdv,
+                                          int& fail) {
+  if constexpr (J < NB) {
+    const double piv = __shfl_sync(0xffffffffu, r[J], J);
+    const bool bad = !(piv > 0.0) || !isfinite(piv);
+    if (bad && fail < 0 && J < nb) fail = J;
+    const double p2 = bad ? 1.0 : piv;
+    const double rd = rsqrt(p2);
+    const double d = p2 * rd;
+    if (lane == J) r[J] = d;
+    if (lane > J) r[J] *= rd;
+    if (lane == 0 && J < nb) {
+      dv[J] = d;
+      rdv[J] = rd;
+    }
+    diag_upd<J, J + 1, NB>(r, lane);
+    diag_step<J + 1, NB>(r, lane, nb, dv, rdv, fail);
+  }
+}
+template <int J, int C, int NB>
+__device__ __forceinline__ void trsm_upd(double (&s)[NB], double x, const double* Ld, int mp) {
+  if constexpr (C < NB) {
+    s[C] -= x * Ld[J * mp + C];
+    trsm_upd<J, C + 1, NB>(s, x, Ld, mp);
+  }
+}
+// one row: x L_dd^T = s, right-looking (chain length 2 per column)
+template <int J, int NB>
+__device__ __forceinline__ void trsm_step(double (&s)[NB], const double* Ld, int mp,
+                                          const double* rdv) {
+  if constexpr (J < NB) {
+    const double x = s[J] * rdv[J];
+    s[J] = x;
+    trsm_upd<J, J + 1, NB>(s, x, Ld, mp);
+    trsm_step<J + 1, NB>(s, Ld, mp, rdv);
+  }
+}
+
 template <int NB>
 __global__ void __launch_bounds__(256) chol_logdet_kernel(CholArgs a) {
   static_assert(NB % 8 == 0 && NB <= 32, "panel width");
@@ -776,6 +826,7 @@ __global__ void __launch_bounds__(256) chol_logdet_kernel(CholArgs a) {
   double* S = reinterpret_cast<double*>(smem_raw);  // [NB][mp] panel, column-major
   double* Lc = S + NB * mp;                         // [NB][mp] staged factor columns
   double* diagv = Lc + NB * mp;                     // [nt] pivots sqrt
+  __shared__ double rdiag[NB];                      // 1/d of the current panel
   __shared__ int s_fail;
   __shared__ double s_red[8];
   const int tid = threadIdx.x;
@@ -784,6 +835,13 @@ __global__ void __launch_bounds__(256) chol_logdet_kernel(CholArgs a) {
   const double* src = a.src + (size_t)a.src_col[b] * a.lds + a.src_row[b];
   double* L = a.L + (size_t)b * a.l_stride;  // column-major nt x nt
   if (tid == 0) s_fail = -1;
+#ifdef DSEL_PROBE
+  int st_i = 0;
+#define STAMP() do { if (b == 0 && tid == 0 && st_i < 64) g_stamps[st_i++] = clock64(); } while (0)
+#else
+#define STAMP() do {} while (0)
+#endif
+  STAMP();
   for (int J0 = 0; J0 < nt; J0 += NB) {
     const int nb = min(NB, nt - J0);
     const int m = nt - J0;
@@ -824,53 +882,46 @@ __global__ void __launch_bounds__(256) chol_logdet_kernel(CholArgs a) {
     }
     cp_async_wait<0>();
     __syncthreads();
-    // (1) diagonal nb x nb block: one warp, right-looking in shared memory,
-    //     lane l owns row l (warp-synchronous, no block barriers)
+    STAMP();
+    // (1) diagonal NB x NB block (identity-padded past nb): one warp, lane l
+    //     owns row l in registers, pivots by shuffles
     if (warp == 0) {
+      double r[NB];
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        r[c] = (lane < nb && c < nb) ? (c <= lane ? S[c * mp + lane] : 0.0)
+                                     : (c == lane ? 1.0 : 0.0);
       int fail = -1;
-      for (int j = 0; j < nb; ++j) {
-        const double piv = S[j * mp + j];
-        const bool bad = !(piv > 0.0) || !isfinite(piv);
-        if (bad) {
-          fail = j;
-          break;
-        }
-        const double d = sqrt(piv);
-        const double rd = 1.0 / d;
-        __syncwarp();
-        double lj = 0.0;
-        if (lane > j && lane < nb) {
-          lj = S[j * mp + lane] * rd;
-          S[j * mp + lane] = lj;
-        }
-        if (lane == j) {
-          S[j * mp + j] = d;
-          diagv[J0 + j] = d;
-        }
-        __syncwarp();
-        if (lane > j && lane < nb)
-          for (int c = j + 1; c <= lane; ++c) S[c * mp + lane] -= lj * S[j * mp + c];
-        __syncwarp();
+      diag_step<0, NB>(r, lane, nb, diagv + J0, rdiag, fail);
+      if (lane < nb) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+          if (c <= lane) S[c * mp + lane] = r[c];
       }
       if (lane == 0 && fail >= 0) s_fail = J0 + fail;
     }
     __syncthreads();
+    STAMP();
     if (s_fail >= 0) break;
-    // (2) panel rows below the diagonal block: forward substitution
-    //     x L_dd^T = s per row (one thread per row, in place in shared memory)
-    for (int i = nb + tid; i < m; i += 256) {
-      for (int j = 0; j < nb; ++j) {
-        const double xj = S[j * mp + i] / S[j * mp + j];
-        S[j * mp + i] = xj;
-        for (int c = j + 1; c < nb; ++c) S[c * mp + i] -= xj * S[j * mp + c];
-      }
+    // (2) panel rows below the diagonal block (full panels: nb == NB):
+    //     x L_dd^T = s, one row per thread, row in registers
+#pragma unroll 1
+    for (int i = NB + tid; i < m; i += 256) {
+      double s[NB];
+#pragma unroll
+      for (int c = 0; c < NB; ++c) s[c] = S[c * mp + i];
+      trsm_step<0, NB>(s, S, mp, rdiag);
+#pragma unroll
+      for (int c = 0; c < NB; ++c) S[c * mp + i] = s[c];
     }
     __syncthreads();
+    STAMP();
     for (int e = tid; e < nb * m; e += 256) {
       const int j = e / m, i = e - j * m;
       L[(size_t)(J0 + j) * nt + J0 + i] = S[j * mp + i];
     }
   }
+  STAMP();
   __syncthreads();
   if (s_fail >= 0) {
     if (tid == 0) {
@@ -898,28 +949,47 @@ __global__ void __launch_bounds__(256) chol_logdet_kernel(CholArgs a) {
 // Triangular inverse of the chosen factor: Linv = L_k^{-1}, row-major [c][m] //
 // with zeros above the diagonal and in the pad (ld = ldl). Warp per column. //
 // ------------------------------------------------------------------------ //
+// Warp per column j of Linv: x = e_j, column-oriented forward substitution
+// x_m *= 1/L_mm; x_i -= x_m L_im (i > m). Lane l holds x_{l+32s} in
+// registers (S slots, compile-time), pivots broadcast by shuffles; the L
+// column loads are independent of the chain so they pipeline.
+template <int S>
 __global__ void __launch_bounds__(256) trinv_kernel(const double* L, int nt, double* Linv, int ldl) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int wib = threadIdx.x >> 5;
+  double* rdiag = reinterpret_cast<double*>(smem_raw);  // [nt]
+  for (int m = threadIdx.x; m < nt; m += blockDim.x) rdiag[m] = 1.0 / L[(size_t)m * nt + m];
+  __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int j = blockIdx.x * (blockDim.x >> 5) + wib;  // column of Linv
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (j >= ldl) return;
-  double* x = reinterpret_cast<double*>(smem_raw) + (size_t)wib * ldl;
-  for (int i = lane; i < ldl; i += 32) x[i] = (i == j) ? 1.0 : 0.0;
-  __syncwarp();
+  double x[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) x[s] = (lane + 32 * s == j) ? 1.0 : 0.0;
   if (j < nt) {
-    // column-oriented forward substitution: x_m /= L[m][m]; x_i -= x_m L[i][m]
-    for (int m = j; m < nt; ++m) {
-      const double xm = x[m] / L[(size_t)m * nt + m];
-      __syncwarp();
-      if (lane == 0) x[m] = xm;
-      const double* colm = L + (size_t)m * nt;
-      for (int i = m + 1 + lane; i < nt; i += 32) x[i] -= xm * colm[i];
-      __syncwarp();
+#pragma unroll
+    for (int sb = 0; sb < S; ++sb) {
+      if (32 * sb + 31 < j) continue;
+      for (int ml = 0; ml < 32; ++ml) {
+        const int m = 32 * sb + ml;
+        if (m >= nt) break;
+        if (m < j) continue;
+        const double xm = __shfl_sync(0xffffffffu, x[sb], ml) * rdiag[m];
+        if (lane == ml) x[sb] = xm;
+        const double* colm = L + (size_t)m * nt;
+#pragma unroll
+        for (int s = sb; s < S; ++s) {
+          const int i = lane + 32 * s;
+          if (i > m && i < nt) x[s] -= xm * colm[i];
+        }
+      }
     }
   }
-  // Linv[i][j] = x_i (row-major [c][m] with ld = ldl), zero above the diagonal
-  for (int i = lane; i < ldl; i += 32) Linv[(size_t)i * ldl + j] = (j < nt && i < nt && i >= j) ? x[i] : 0.0;
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int i = lane + 32 * s;
+    if (i < ldl) Linv[(size_t)i * ldl + j] = (j < nt && i < nt && i >= j) ? x[s] : 0.0;
+  }
+  // pad rows beyond 32*S (ldl > 32*S never happens: ldl <= 32*S by dispatch)
 }
 
 // ------------------------------------------------------------------------ //

@@ -1,0 +1,40 @@
+// Probe: phase timing of the gain kernel (chol_logdet_kernel) on a batch of
+// SPD blocks, via clock64 stamps (thread 0 of block 0).
+#define DSEL_PROBE 1
+#include <cstdio>
+#include <vector>
+#include <cmath>
+__device__ long long g_stamps[64];
+#include "../paper_2604_08812_b200/csrc/kernels.cuh"
+using namespace dsel;
+int main(int argc, char** argv) {
+  int nt = argc > 1 ? atoi(argv[1]) : 128, batch = argc > 2 ? atoi(argv[2]) : 200;
+  int mp = ((nt + 7) / 8) * 8; if (mp % 16 == 0 || mp % 16 == 8) mp += 4;
+  size_t n2 = (size_t)nt * nt;
+  std::vector<double> h(n2 * batch);
+  for (int b = 0; b < batch; ++b) for (int i = 0; i < nt; ++i) for (int j = 0; j < nt; ++j)
+    h[b * n2 + (size_t)j * nt + i] = (i == j ? nt : 0.0) + 1.0 / (1 + abs(i - j));
+  double *src, *L, *gain; int *st, *sc, *sr;
+  cudaMalloc(&src, h.size() * 8); cudaMalloc(&L, h.size() * 8); cudaMalloc(&gain, batch * 8);
+  cudaMalloc(&st, batch * 4); cudaMalloc(&sc, batch * 4); cudaMalloc(&sr, batch * 4);
+  cudaMemcpy(src, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+  std::vector<int> cols(batch), rows(batch, 0);
+  for (int b = 0; b < batch; ++b) cols[b] = b * nt;  // block b = columns b*nt.., rows 0..nt (ld = nt)
+  cudaMemcpy(sc, cols.data(), batch * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(sr, rows.data(), batch * 4, cudaMemcpyHostToDevice);
+  CholArgs a; a.src = src; a.lds = nt; a.src_col = sc; a.src_row = sr; a.L = L; a.l_stride = n2;
+  a.gain = gain; a.status = st; a.nt = nt; a.n = batch; a.mp = mp;
+  size_t smem = ((size_t)2 * 32 * mp + nt) * 8;
+  cudaFuncSetAttribute(chol_logdet_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  for (int r = 0; r < 3; ++r) chol_logdet_kernel<32><<<batch, 256, smem>>>(a);
+  cudaEventRecord(e0);
+  chol_logdet_kernel<32><<<batch, 256, smem>>>(a);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  long long stamps[64]; cudaMemcpyFromSymbol(stamps, g_stamps, sizeof(stamps));
+  double g; cudaMemcpy(&g, gain, 8, cudaMemcpyDeviceToHost);
+  printf("nt %d batch %d: %.1f us  gain[0]=%.6f err=%s\n", nt, batch, ms * 1e3, g, cudaGetErrorString(cudaGetLastError()));
+  for (int i = 1; i < 64 && stamps[i]; ++i) printf("  stamp %2d: +%lld cycles\n", i, stamps[i] - stamps[i - 1]);
+  return 0;
+}
