@@ -44,7 +44,8 @@ typedef enum {
   DSEL_E_NCCL = 5,       /* collective failure -> WorkerFailure */
   DSEL_E_OOM = 6,        /* device/pinned allocation failed in dsel_create */
   DSEL_E_IO = 7,         /* IoError / CorruptFile */
-  DSEL_E_STATE = 8       /* call out of order (e.g. step after the budget) */
+  DSEL_E_STATE = 8,      /* call out of order (e.g. step after the budget) */
+  DSEL_E_CORRUPT = 9     /* CorruptFile: KBF header/size invalid (kstore.hpp:92-125) */
 } dsel_status;
 
 typedef enum { DSEL_STORAGE_AUTO = 0, DSEL_STORAGE_HBM = 1, DSEL_STORAGE_STREAM = 2 } dsel_storage;
@@ -112,6 +113,13 @@ dsel_status dsel_load_block_col(dsel_engine* e, int j, const double* host_col);
 /* Whole K in DataSpaceHessian / KBF payload order (n_sensors^2 blocks,
  * block-row-major, hessian.hpp:17-84): loads every owned panel. */
 dsel_status dsel_load_k(dsel_engine* e, const double* host_k);
+/* KBF store (`doptsel select <kbf>`, KStoreReader, kstore.hpp:22-186): validates
+ * the header and size like KStoreReader (E_CORRUPT / E_IO) and loads this
+ * rank's panels with parallel pread into pinned buffers, overlapped with the
+ * H2D. exact_columns=1 reads true block columns (blocks (i,j), what the
+ * reference reads); 0 reads contiguous block rows and relies on symmetry
+ * (write_kbf guarantees |K - K^T| <= 1e-10). threads = pread threads (0 = auto). */
+dsel_status dsel_load_kbf(dsel_engine* e, const char* path, int exact_columns, int threads);
 /* Export block row j (same layout as dsel_load_block_row) of the CURRENT
  * conditional covariance (= K before the first step); owner rank only. */
 dsel_status dsel_read_block_row(dsel_engine* e, int j, double* host_row);

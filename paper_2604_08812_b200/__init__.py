@@ -4,11 +4,11 @@ Product = libdsel.so (sm_100a CUDA + NCCL) behind the C ABI include/dsel.h.
 This package is the thin host mirror of the reference selection interface.
 """
 from ._abi import LIB_PATH, lib  # noqa: F401  (raises ImportError if the library is missing)
-from .selector import (DselError, Engine, GpuOptions, IndexOutOfRange,  # noqa: F401
+from .selector import (CorruptFile, DselError, Engine, IoError, GpuOptions, IndexOutOfRange,  # noqa: F401
                        InfeasibleRound, InvalidConfig, ParallelRunReport, SelectionState,
                        SelectionTrace, TraceRow, WorkerFailure, gpu_greedy_select,
                        nccl_unique_id, synthetic_v)
 
 __all__ = ["Engine", "GpuOptions", "gpu_greedy_select", "synthetic_v", "nccl_unique_id",
-           "DselError", "InvalidConfig", "IndexOutOfRange", "InfeasibleRound", "WorkerFailure",
+           "DselError", "IoError", "CorruptFile", "InvalidConfig", "IndexOutOfRange", "InfeasibleRound", "WorkerFailure",
            "SelectionState", "SelectionTrace", "ParallelRunReport", "TraceRow", "LIB_PATH"]

@@ -54,7 +54,8 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
     os.makedirs(OUT, exist_ok=True)
     inc = os.path.join(ROOT, "include")
     nccl_inc, nccl_lib = nccl_dirs()
-    deps = sources() + [os.path.join(inc, "dsel.h"), __file__]
+    deps = sources() + [os.path.join(inc, "dsel.h"), __file__,
+                        os.path.join(PKG, "tools", "doptsel_main.cpp")]
     if not force and up_to_date(LIB, deps):
         return LIB
     objs = []
@@ -77,7 +78,16 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
           "-Xlinker", "-rpath=" + nccl_lib, "-Xcompiler", "-pthread"])
     for o in objs:
         os.remove(o)
+    build_cli()
     return LIB
+
+
+def build_cli() -> str:
+    """The drop-in `doptsel select` CLI (tools/doptsel_main.cpp) over libdsel.so."""
+    src = os.path.join(PKG, "tools", "doptsel_main.cpp")
+    _run(["g++", "-O2", "-std=gnu++20", "-Wall", "-I", os.path.join(ROOT, "include"), src,
+          "-o", CLI, "-L", OUT, "-ldsel", "-Wl,-rpath,$ORIGIN", "-pthread"])
+    return CLI
 
 
 if __name__ == "__main__":

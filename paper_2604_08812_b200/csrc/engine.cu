@@ -15,7 +15,13 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <cerrno>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -799,6 +805,114 @@ dsel_status dsel_load_k(dsel_engine* e, const double* host_k) {
     }
     CU(cudaStreamSynchronize(e->s));
   });
+}
+
+// KBF store ingest (kstore.hpp:22-35 layout; validation as KStoreReader,
+// kstore.hpp:92-125). Owned panels only; parallel pread of each block row
+// (contiguous) or of the Nd blocks of a block column (exact reference
+// semantics) into two pinned host buffers, alternated so the pread of panel
+// q+1 overlaps the H2D + scatter of panel q.
+namespace {
+void pread_exact(int fd, void* dst, size_t bytes, off_t off, const std::string& path) {
+  unsigned char* p = static_cast<unsigned char*>(dst);
+  size_t done = 0;
+  while (done < bytes) {
+    const ssize_t got = ::pread(fd, p + done, bytes - done, off + (off_t)done);
+    if (got < 0) {
+      if (errno == EINTR) continue;
+      throw Fail{DSEL_E_IO, path + ": pread failed: " + std::strerror(errno)};
+    }
+    if (got == 0) throw Fail{DSEL_E_CORRUPT, path + ": unexpected end of file"};
+    done += (size_t)got;
+  }
+}
+
+void load_kbf_impl(dsel_engine* e, const char* path, bool exact_columns, int threads) {
+  const std::string ps(path ? path : "");
+  const int fd = ::open(ps.c_str(), O_RDONLY);
+  if (fd < 0) throw Fail{DSEL_E_IO, "cannot open " + ps + ": " + std::strerror(errno)};
+  struct Closer {
+    int fd;
+    ~Closer() { ::close(fd); }
+  } closer{fd};
+  unsigned char h[32];
+  if (::pread(fd, h, 32, 0) != 32) throw Fail{DSEL_E_CORRUPT, ps + ": header truncated"};
+  auto u32 = [&](int o) {
+    return (uint32_t)h[o] | ((uint32_t)h[o + 1] << 8) | ((uint32_t)h[o + 2] << 16) |
+           ((uint32_t)h[o + 3] << 24);
+  };
+  if (std::memcmp(h, "KBF1", 4) != 0) throw Fail{DSEL_E_CORRUPT, ps + ": bad magic"};
+  const int nd = (int)u32(8), nt = (int)u32(12);
+  if (u32(4) != 1 || u32(16) != 1 || u32(20) != 1 || nd < 1 || nt < 1)
+    throw Fail{DSEL_E_CORRUPT, ps + ": unsupported header fields"};
+  struct stat st {};
+  if (::fstat(fd, &st) != 0) throw Fail{DSEL_E_IO, ps + ": fstat failed"};
+  const size_t bsz = (size_t)nt * nt * sizeof(double);
+  const size_t expect = 32 + (size_t)nd * nd * bsz;
+  if ((size_t)st.st_size != expect)
+    throw Fail{DSEL_E_CORRUPT, ps + ": size " + std::to_string(st.st_size) + " != expected " +
+                                   std::to_string(expect)};
+  if (nd != e->nd || nt != e->nt)
+    throw Fail{DSEL_E_INVALID, ps + ": store shape does not match the engine configuration"};
+  const size_t row_bytes = (size_t)nd * bsz;
+  double* hb[2] = {nullptr, nullptr};
+  cudaEvent_t freed[2] = {nullptr, nullptr};
+  try {
+    for (int b = 0; b < 2; ++b) {
+      CU(cudaMallocHost(&hb[b], row_bytes));
+      CU(cudaEventCreateWithFlags(&freed[b], cudaEventDisableTiming));
+    }
+    if (threads <= 0) threads = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    int flip = 0;
+    for (int q = 0; q < e->nloc; ++q) {
+      const int j = e->slot_sensor[q];
+      double* buf = hb[flip];
+      CU(cudaEventSynchronize(freed[flip]));  // its previous H2D has completed
+      // parallel pread of the Nd blocks of this panel
+      auto work = [&](int w) {
+        for (int i = w; i < nd; i += threads) {
+          const size_t blk = exact_columns ? ((size_t)i * nd + j) : ((size_t)j * nd + i);
+          pread_exact(fd, reinterpret_cast<unsigned char*>(buf) + (size_t)i * bsz, bsz,
+                      (off_t)(32 + blk * bsz), ps);
+        }
+      };
+      std::vector<std::thread> pool;
+      std::vector<std::string> errs(threads);
+      std::vector<int> codes(threads, 0);
+      for (int w = 0; w < threads; ++w)
+        pool.emplace_back([&, w] {
+          try {
+            work(w);
+          } catch (const Fail& f) {
+            codes[w] = f.st;
+            errs[w] = f.msg;
+          }
+        });
+      for (auto& t : pool) t.join();
+      for (int w = 0; w < threads; ++w)
+        if (codes[w]) throw Fail{(dsel_status)codes[w], errs[w]};
+      load_panel(e, j, buf, exact_columns);
+      CU(cudaEventRecord(freed[flip], e->cs));
+      flip ^= 1;
+    }
+    CU(cudaStreamSynchronize(e->s));
+    CU(cudaStreamSynchronize(e->cs));
+  } catch (...) {
+    for (int b = 0; b < 2; ++b) {
+      if (hb[b]) cudaFreeHost(hb[b]);
+      if (freed[b]) cudaEventDestroy(freed[b]);
+    }
+    throw;
+  }
+  for (int b = 0; b < 2; ++b) {
+    cudaFreeHost(hb[b]);
+    cudaEventDestroy(freed[b]);
+  }
+}
+}  // namespace
+
+dsel_status dsel_load_kbf(dsel_engine* e, const char* path, int exact_columns, int threads) {
+  return guard(e, [&] { load_kbf_impl(e, path, exact_columns != 0, threads); });
 }
 
 dsel_status dsel_read_block_row(dsel_engine* e, int j, double* host_row) {

@@ -45,8 +45,16 @@ class WorkerFailure(DselError):
     pass
 
 
+class IoError(DselError):
+    pass
+
+
+class CorruptFile(IoError):
+    pass
+
+
 _EXC = {1: InvalidConfig, 2: IndexOutOfRange, 3: InfeasibleRound, 4: WorkerFailure,
-        5: WorkerFailure, 6: WorkerFailure, 7: DselError, 8: DselError}
+        5: WorkerFailure, 6: WorkerFailure, 7: IoError, 8: DselError, 9: CorruptFile}
 
 
 def _check(rc: int, handle=None) -> None:
@@ -139,6 +147,10 @@ class Engine:
     def load_k(self, k) -> None:
         """Whole K, block-row-major (DataSpaceHessian / KBF payload order)."""
         _check(lib.dsel_load_k(self.h, _host_ptr(k)), self.h)
+
+    def load_kbf(self, path: str, exact_columns: bool = True, threads: int = 0) -> None:
+        """KBF store (kstore.hpp:22-186) -> this engine's panels."""
+        _check(lib.dsel_load_kbf(self.h, path.encode(), int(exact_columns), threads), self.h)
 
     def load_block_row(self, j: int, row) -> None:
         _check(lib.dsel_load_block_row(self.h, j, _host_ptr(row)), self.h)

@@ -1,0 +1,34 @@
+"""Run the C++ drop-in test (tests/cpp/test_doptsel_gpu.cpp): the reference's
+own KAccess types (SyntheticKAccess, KStoreReader, DataSpaceHessian) through
+include/doptsel_gpu.hpp vs the reference run_parallel_greedy, in one process."""
+import os
+import subprocess
+
+import pytest
+
+from conftest import ROOT, gpu_available
+
+BIN = os.path.join(ROOT, "tests", "cpp", "build", "test_doptsel_gpu")
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not gpu_available(), reason="needs a CUDA GPU")
+@pytest.mark.skipif(not os.path.exists(BIN), reason="built only where /root/reference exists")
+def test_cpp_dropin_against_reference():
+    r = subprocess.run([BIN, os.path.join(ROOT, "tests", "golden", "wave.kbf")],
+                       capture_output=True, text=True, timeout=900)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_dropin_header_compiles_against_reference(tmp_path):
+    """Compile-only check here (no GPU): the adapter header builds against the
+    reference headers."""
+    ref = "/root/reference/proj"
+    if not os.path.isdir(ref):
+        pytest.skip("reference headers absent")
+    src = tmp_path / "t.cpp"
+    src.write_text('#include "doptsel/parallel.hpp"\n#include "doptsel_gpu.hpp"\n'
+                   'int main(){ doptsel::GpuOptions o; (void)o; return 0; }\n')
+    subprocess.run(["g++", "-std=gnu++20", "-fsyntax-only", "-I", ref + "/include",
+                    "-I", os.path.join(ROOT, "include"), str(src)], check=True)
