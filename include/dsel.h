@@ -91,6 +91,15 @@ typedef struct {
   double update_flops;    /* algorithmic flops of this rank's update: 2*nt*rows*cols */
 } dsel_step_info;
 
+/* Per-rank argmax record exchanged each round (32 bytes, allgathered): the
+ * local best and runner-up under the reference order (larger gain wins, exact
+ * ties to the lower sensor index, selector.hpp:132-134); s = -1 when empty. */
+typedef struct {
+  double g1, g2;
+  int s1, s2;
+  int n_eval, n_inf;
+} dsel_argrec;
+
 /* ---- lifecycle ---------------------------------------------------------- */
 int dsel_abi_version(void);
 dsel_status dsel_nccl_unique_id(void* out128);
@@ -133,6 +142,11 @@ dsel_status dsel_synthetic_v(int n_sensors, int n_steps, int rank, uint64_t seed
 /* Device: generate this rank's panels of K = sigma^2 I + V V^T bit-exactly
  * (sequential non-FMA dot products). V_host as produced above. */
 dsel_status dsel_gen_synthetic(dsel_engine* e, const double* v_host, int rank, double sigma);
+
+/* The fold every rank applies to the allgathered records (reduce_argmax,
+ * parallel.hpp:61-74, extended to the global top-2). Pure host function;
+ * associative and order-independent. out->s1 = -1 when all are infeasible. */
+void dsel_fold_records(const dsel_argrec* recs, int n, dsel_argrec* out);
 
 /* ---- selection (north-star (2)-(4)) ------------------------------------- */
 /* One round: gains of all remaining candidates, cross-rank argmax, panel

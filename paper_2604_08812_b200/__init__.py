@@ -7,8 +7,8 @@ from ._abi import LIB_PATH, lib  # noqa: F401  (raises ImportError if the librar
 from .selector import (CorruptFile, DselError, Engine, IoError, GpuOptions, IndexOutOfRange,  # noqa: F401
                        InfeasibleRound, InvalidConfig, ParallelRunReport, SelectionState,
                        SelectionTrace, TraceRow, WorkerFailure, gpu_greedy_select,
-                       nccl_unique_id, synthetic_v)
+                       fold_records, nccl_unique_id, synthetic_v)
 
-__all__ = ["Engine", "GpuOptions", "gpu_greedy_select", "synthetic_v", "nccl_unique_id",
+__all__ = ["Engine", "GpuOptions", "gpu_greedy_select", "synthetic_v", "nccl_unique_id", "fold_records",
            "DselError", "IoError", "CorruptFile", "InvalidConfig", "IndexOutOfRange", "InfeasibleRound", "WorkerFailure",
            "SelectionState", "SelectionTrace", "ParallelRunReport", "TraceRow", "LIB_PATH"]

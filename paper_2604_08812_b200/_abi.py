@@ -17,7 +17,7 @@ STATUS_NAMES = {0: "DSEL_OK", 1: "DSEL_E_INVALID", 2: "DSEL_E_RANGE", 3: "DSEL_E
                 8: "DSEL_E_STATE", 9: "DSEL_E_CORRUPT"}
 
 # every entry point declared in include/dsel.h (tests check the exports)
-EXPORTS = ["dsel_abi_version", "dsel_nccl_unique_id", "dsel_create", "dsel_destroy",
+EXPORTS = ["dsel_abi_version", "dsel_fold_records", "dsel_nccl_unique_id", "dsel_create", "dsel_destroy",
            "dsel_last_error", "dsel_sync", "dsel_device_bytes", "dsel_load_block_row",
            "dsel_load_block_col", "dsel_load_k", "dsel_load_kbf", "dsel_read_block_row", "dsel_synthetic_v",
            "dsel_gen_synthetic", "dsel_step", "dsel_step_forced", "dsel_run", "dsel_peek_gains",
@@ -44,6 +44,11 @@ class DselStepInfo(C.Structure):
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class DselArgRec(C.Structure):
+    _fields_ = [("g1", C.c_double), ("g2", C.c_double), ("s1", C.c_int), ("s2", C.c_int),
+                ("n_eval", C.c_int), ("n_inf", C.c_int)]
 
 
 class DselStats(C.Structure):
@@ -89,8 +94,10 @@ def _load():
     L.dsel_reset.argtypes = [vp]
     L.dsel_export_factor.argtypes = [vp, vp, C.c_int64]
     L.dsel_get_stats.argtypes = [vp, C.POINTER(DselStats)]
+    L.dsel_fold_records.argtypes = [C.POINTER(DselArgRec), C.c_int, C.POINTER(DselArgRec)]
+    L.dsel_fold_records.restype = None
     for name in EXPORTS:
-        if name not in ("dsel_destroy", "dsel_last_error", "dsel_device_bytes",
+        if name not in ("dsel_destroy", "dsel_last_error", "dsel_device_bytes", "dsel_fold_records",
                         "dsel_get_trace", "dsel_abi_version"):
             getattr(L, name).restype = C.c_int
     return L

@@ -319,30 +319,10 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   e->d2h_bytes += sizeof(ArgRec) * (uint64_t)e->G;
   CU(cudaStreamSynchronize(e->s));
   // identical fold on every rank (reduce_argmax, parallel.hpp:61-74, top-2)
-  double g1 = -INFINITY, g2 = -INFINITY;
-  int s1 = -1, s2 = -1, n_eval = 0, n_inf = 0;
-  auto ins = [&](double d, int s) {
-    if (s < 0) return;
-    auto better = [](double d, int s, double bd, int bs) {
-      return d > bd || (d == bd && (bs < 0 || s < bs));
-    };
-    if (s1 < 0 || better(d, s, g1, s1)) {
-      g2 = g1;
-      s2 = s1;
-      g1 = d;
-      s1 = s;
-    } else if (s2 < 0 || better(d, s, g2, s2)) {
-      g2 = d;
-      s2 = s;
-    }
-  };
-  for (int r = 0; r < e->G; ++r) {
-    const ArgRec& rr = e->h_recs[r];
-    ins(rr.g1, rr.s1);
-    ins(rr.g2, rr.s2);
-    n_eval += rr.n_eval;
-    n_inf += rr.n_inf;
-  }
+  dsel_argrec fold{};
+  dsel_fold_records(e->h_recs, e->G, &fold);
+  const double g1 = fold.g1, g2 = fold.g2;
+  const int s1 = fold.s1, s2 = fold.s2, n_eval = fold.n_eval, n_inf = fold.n_inf;
   dsel_step_info row{};
   row.k = round + 1;
   row.n_evaluated = n_eval;
@@ -750,6 +730,34 @@ void load_panel(dsel_engine* e, int j, const double* host, bool as_column) {
 extern "C" {
 
 int dsel_abi_version(void) { return DSEL_ABI_VERSION; }
+
+void dsel_fold_records(const dsel_argrec* recs, int n, dsel_argrec* out) {
+  auto better = [](double d, int s, double bd, int bs) {
+    return d > bd || (d == bd && (bs < 0 || s < bs));
+  };
+  dsel_argrec r{};
+  r.g1 = r.g2 = -INFINITY;
+  r.s1 = r.s2 = -1;
+  auto ins = [&](double d, int s) {
+    if (s < 0 || s == r.s1) return;
+    if (r.s1 < 0 || better(d, s, r.g1, r.s1)) {
+      r.g2 = r.g1;
+      r.s2 = r.s1;
+      r.g1 = d;
+      r.s1 = s;
+    } else if (r.s2 < 0 || better(d, s, r.g2, r.s2)) {
+      r.g2 = d;
+      r.s2 = s;
+    }
+  };
+  for (int i = 0; i < n; ++i) {
+    ins(recs[i].g1, recs[i].s1);
+    ins(recs[i].g2, recs[i].s2);
+    r.n_eval += recs[i].n_eval;
+    r.n_inf += recs[i].n_inf;
+  }
+  *out = r;
+}
 
 dsel_status dsel_nccl_unique_id(void* out128) {
   if (!out128) return DSEL_E_INVALID;

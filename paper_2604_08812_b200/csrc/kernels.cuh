@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "dsel.h"
+
 namespace dsel {
 
 // ------------------------------------------------------------------------ //
@@ -996,14 +998,7 @@ __global__ void __launch_bounds__(256) trinv_kernel(const double* L, int nt, dou
 // Local top-2 argmax with the reference tie rule (selector.hpp:132-134):   //
 // larger gain wins, exact ties go to the lower sensor index.              //
 // ------------------------------------------------------------------------ //
-struct ArgRec {
-  double g1;
-  double g2;
-  int s1;
-  int s2;
-  int n_eval;
-  int n_inf;
-};
+using ArgRec = dsel_argrec;  // include/dsel.h
 
 __device__ __forceinline__ bool better(double d, int s, double bd, int bs) {
   return d > bd || (d == bd && (bs < 0 || s < bs));

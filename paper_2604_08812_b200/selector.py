@@ -19,7 +19,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._abi import DSEL_OK, STATUS_NAMES, DselConfig, DselStats, DselStepInfo, lib
+from ._abi import DSEL_OK, STATUS_NAMES, DselArgRec, DselConfig, DselStats, DselStepInfo, lib
 
 
 # ---- errors (errors.hpp:10-86) -------------------------------------------- #
@@ -80,6 +80,19 @@ def nccl_unique_id() -> bytes:
     buf = (C.c_ubyte * 128)()
     _check(lib.dsel_nccl_unique_id(buf))
     return bytes(buf)
+
+
+def fold_records(records):
+    """The per-round fold every rank applies to the allgathered argmax records
+    (dsel_fold_records; reduce_argmax semantics, parallel.hpp:61-74).
+    records: iterable of (g1, s1, g2, s2, n_eval, n_inf). Returns the same tuple."""
+    recs = list(records)
+    arr = (DselArgRec * max(len(recs), 1))()
+    for i, (g1, s1, g2, s2, ne, ni) in enumerate(recs):
+        arr[i] = DselArgRec(g1, g2, s1, s2, ne, ni)
+    out = DselArgRec()
+    lib.dsel_fold_records(arr, len(recs), C.byref(out))
+    return (out.g1, out.s1, out.g2, out.s2, out.n_eval, out.n_inf)
 
 
 def synthetic_v(n_sensors: int, n_steps: int, rank: int, seed: int, threads: int = 0) -> np.ndarray:

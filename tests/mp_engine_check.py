@@ -1,0 +1,57 @@
+"""Multi-GPU check (one process per GPU): run under
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P tests/mp_engine_check.py [c1|c2|wave]
+Every rank must reproduce the reference golden sequence and gains, and all
+ranks must agree bitwise (the fold and the broadcast factor are identical)."""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2604_08812_b200 as d  # noqa: E402
+
+which = sys.argv[1] if len(sys.argv) > 1 else "c1"
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+local = int(os.environ.get("LOCAL_RANK", rank))
+torch.cuda.set_device(local)
+dist.init_process_group("gloo")
+nid = [d.nccl_unique_id() if rank == 0 else None]
+dist.broadcast_object_list(nid, src=0)
+gold = json.load(open(os.path.join(ROOT, "tests", "golden", f"{which}.json")))
+if which == "wave":
+    from oracle import oracle as O  # checker only: parses the KBF fixture
+    eng = d.Engine(32, 16, 12, device=local, world_size=world, rank=rank, nccl_id=nid[0],
+                   export_factor=True)
+    eng.load_kbf(os.path.join(ROOT, "tests", "golden", "wave.kbf"))
+else:
+    nd, nt, rk, b = gold["n_sensors"], gold["n_steps"], gold["rank"], gold["budget"]
+    v = d.synthetic_v(nd, nt, rk, gold["seed"])
+    eng = d.Engine(nd, nt, b, device=local, world_size=world, rank=rank, nccl_id=nid[0],
+                   export_factor=True)
+    eng.gen_synthetic(v, rk, gold["sigma"])
+eng.run()
+rows = eng.trace()
+L = eng.export_factor(len(rows))
+eng.close()
+chosen = [r["chosen_index"] for r in rows]
+ok = chosen == gold["chosen"]
+for r, g in zip(rows, gold["gains"]):
+    ok = ok and abs(r["gain"] - g) <= 1e-9 * max(abs(g), 1.0)
+# bitwise agreement across ranks
+mine = torch.tensor([r["gain"] for r in rows], dtype=torch.float64)
+allg = [torch.zeros_like(mine) for _ in range(world)]
+dist.all_gather(allg, mine)
+same = all(torch.equal(allg[0], x) for x in allg)
+fsum = torch.tensor([float(np.abs(L).sum())], dtype=torch.float64)
+allf = [torch.zeros_like(fsum) for _ in range(world)]
+dist.all_gather(allf, fsum)
+same = same and all(torch.equal(allf[0], x) for x in allf)
+print(f"rank {rank}/{world} {which}: sequence {'OK' if ok else 'MISMATCH'} ranks-agree {same} "
+      f"bytes_exchanged(r1)={rows[0]['bytes_exchanged']}", flush=True)
+dist.destroy_process_group()
+sys.exit(0 if (ok and same) else 1)

@@ -1,0 +1,54 @@
+"""Multi-GPU engine (NCCL over NVLink): run tests/mp_engine_check.py under
+torchrun on every visible GPU (skipped with fewer than 2)."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT, gpu_available
+
+
+def ngpu():
+    try:
+        import torch
+
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not gpu_available() or ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("which", ["c1", "wave", "c2"])
+def test_multi_gpu_matches_reference(which):
+    n = min(ngpu(), 8)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(ROOT, "tests", "mp_engine_check.py"), which]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    print(r.stdout[-3000:])
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not gpu_available() or ngpu() < 2, reason="needs >= 2 GPUs")
+def test_cli_multi_gpu(tmp_path):
+    import json
+
+    cli = os.path.join(ROOT, "paper_2604_08812_b200", "lib", "doptsel")
+    w = json.load(open(os.path.join(ROOT, "tests", "golden", "wave.json")))
+    r = subprocess.run([cli, "select", os.path.join(ROOT, "tests", "golden", "wave.kbf"),
+                        "--budget", "12", "--gpus", "2", "--out", str(tmp_path)],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    assert json.load(open(tmp_path / "selection.json"))["chosen"] == w["chosen"]

@@ -1,0 +1,127 @@
+"""World-size-2 tests of the multi-rank protocol on CPU (gloo, 127.0.0.1).
+
+The engine's distributed round is: local gains of the rank's own candidates
+(cyclic ownership by position, p % world) -> local top-2 record -> allgather
+-> the product's identical fold (dsel_fold_records) on every rank -> owner
+broadcasts the chosen conditional panel -> every rank applies the rank-Nt
+update to its own block columns. Here each rank runs that protocol with a
+float64 numpy restatement of the arithmetic and gloo collectives; the chosen
+sequence must equal the single-process reference oracle (and the fold must be
+associative / order independent, reduce_argmax semantics).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _record(gains, sensors):
+    """Local top-2 with the reference order (selector.hpp:132-134)."""
+    order = sorted(range(len(gains)), key=lambda i: (-gains[i], sensors[i]))
+    g1 = gains[order[0]] if order else float("-inf")
+    s1 = sensors[order[0]] if order else -1
+    g2 = gains[order[1]] if len(order) > 1 else float("-inf")
+    s2 = sensors[order[1]] if len(order) > 1 else -1
+    return (g1, s1, g2, s2, len(gains), 0)
+
+
+def _rank_main(rank, world, port, nd, nt, budget, k_flat, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2604_08812_b200 import fold_records
+    from oracle import oracle as O
+
+    K = O.blocks_to_dense(np.asarray(k_flat), nd, nt)
+    n = nd * nt
+    mine = [p for p in range(nd) if p % world == rank]            # cyclic ownership
+    C = {p: K[:, p * nt:(p + 1) * nt].copy() for p in mine}         # local block columns
+    alive = [True] * nd
+    seq, gains_out = [], []
+    for _ in range(budget):
+        live_local = [p for p in mine if alive[p]]
+        g = [2.0 * np.log(np.diag(np.linalg.cholesky(C[p][p * nt:(p + 1) * nt]))).sum()
+             for p in live_local]
+        rec = torch.tensor(_record(g, live_local), dtype=torch.float64)
+        allr = [torch.zeros(6, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(allr, rec)
+        recs = [(float(r[0]), int(r[1]), float(r[2]), int(r[3]), int(r[4]), int(r[5])) for r in allr]
+        # fold order must not matter
+        assert fold_records(recs) == fold_records(recs[::-1])
+        g1, s1, *_ = fold_records(recs)
+        owner = s1 % world
+        panel = torch.from_numpy(C[s1].copy()) if owner == rank else torch.zeros(n, nt, dtype=torch.float64)
+        dist.broadcast(panel, src=owner)
+        P = panel.numpy()
+        Lk = np.linalg.cholesky(P[s1 * nt:(s1 + 1) * nt])
+        W = np.linalg.solve(Lk, P.T).T                              # W = C[:,k] L_k^{-T}
+        alive[s1] = False
+        for p in mine:
+            if alive[p]:
+                C[p] -= W @ W[p * nt:(p + 1) * nt].T
+        seq.append(s1)
+        gains_out.append(g1)
+    out_q.put((rank, seq, gains_out))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_protocol_matches_oracle():
+    from oracle import oracle as O
+
+    nd, nt, budget = 14, 4, 7
+    k = O.random_hessian(nd, nt, 0.9, 48, 1234)
+    want = O.greedy_select(k, nd, nt, budget)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, nd, nt, budget, k.tolist(), q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, seq, gains in res:
+        assert seq == want.chosen, (rank, seq, want.chosen)
+        for a, b in zip(gains, want.gains):
+            assert abs(a - b) <= 1e-9 * max(abs(b), 1.0)
+
+
+def test_fold_records_tie_rule_and_associativity():
+    from paper_2604_08812_b200 import fold_records
+
+    inf = float("-inf")
+    # reduce_argmax cases (test_parallel.cpp:42-49)
+    assert fold_records([(1.0, 5, inf, -1, 1, 0), (2.0, 3, inf, -1, 1, 0)])[:2] == (2.0, 3)
+    assert fold_records([(2.0, 7, inf, -1, 1, 0), (2.0, 3, inf, -1, 1, 0)])[:2] == (2.0, 3)
+    r = fold_records([(inf, -1, inf, -1, 3, 3), (inf, -1, inf, -1, 2, 2)])
+    assert r[1] == -1 and r[4] == 5 and r[5] == 5
+    rng = np.random.default_rng(5)
+    recs = []
+    for i in range(9):
+        a, b = rng.integers(0, 4, size=2) * 0.5
+        s = rng.permutation(40)[:2]
+        hi, lo = ((a, s[0]), (b, s[1])) if (a, -s[0]) >= (b, -s[1]) else ((b, s[1]), (a, s[0]))
+        recs.append((float(hi[0]), int(hi[1]), float(lo[0]), int(lo[1]), 2, 0))
+    full = fold_records(recs)
+    for _ in range(10):
+        perm = [recs[i] for i in rng.permutation(len(recs))]
+        assert fold_records(perm)[:4] == full[:4]
+        cut = int(rng.integers(1, len(perm)))
+        left, right = fold_records(perm[:cut]), fold_records(perm[cut:])
+        assert fold_records([left, right])[:4] == full[:4]
