@@ -296,12 +296,14 @@ __global__ void __launch_bounds__(upd::THREADS, 1) schur_update_kernel(UpdateArg
 // mainloop, so the C traffic (AI = nt/8 flop/B) hides behind the math.     //
 // ------------------------------------------------------------------------ //
 namespace ws {
-constexpr int BR = 128, BC = 64, KC = 16, STAGES = 4;
+constexpr int BR = 128, BC = 64, KC = 16;
+constexpr int SC = 2;      // k-chunks per pipeline stage (one mbarrier round per 32 k)
+constexpr int STAGES = 3;
 constexpr int CONSUMERS = 256, THREADS = CONSUMERS + 32;
 constexpr int CP = BR + 8;  // C tile column pitch (doubles): conflict-free LDS.128
 constexpr size_t OFF_R = 0;
-constexpr size_t OFF_C = OFF_R + (size_t)STAGES * BR * KC * 8;
-constexpr size_t OFF_CT = OFF_C + (size_t)STAGES * BC * KC * 8;
+constexpr size_t OFF_C = OFF_R + (size_t)STAGES * SC * BR * KC * 8;
+constexpr size_t OFF_CT = OFF_C + (size_t)STAGES * SC * BC * KC * 8;
 constexpr size_t OFF_MAPS = OFF_CT + (size_t)BC * CP * 8;                // 2 x {colbase[BC], rowphys[BR]}
 constexpr size_t MAPS_BYTES = (size_t)BC * 8 + BR * 4;
 constexpr size_t OFF_RUNS = OFF_MAPS + 2 * MAPS_BYTES;                   // producer scratch
@@ -504,19 +506,24 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
         const int i0 = rrun[q], len = rrun[q + 1] - i0;
         bulk_g2s(sCt + c * CP + i0, a.C + colbase[c] + rowphys[i0], (unsigned)len * 8u, &tfull[b]);
       }
-      // operand k-chunks: r-side one contiguous tile, c-side one copy per run
-      for (int kb = 0; kb < a.n_k; ++kb) {
+      // operand k-chunks, SC per stage: r-side one contiguous tile per chunk,
+      // c-side one copy per run per chunk
+      for (int kb0 = 0; kb0 < a.n_k; kb0 += SC) {
+        const int sc = min(SC, a.n_k - kb0);
         if (lane == 0) {
           mbar_wait(&empty[stage], ephase ^ 1);
-          mbar_expect_tx(&full[stage], (unsigned)(BR + BC) * KC * 8u);
-          bulk_g2s(sR + stage * BR * KC, a.Wt + ((size_t)kb * a.mpad + r0) * KC, BR * KC * 8,
-                   &full[stage]);
+          mbar_expect_tx(&full[stage], (unsigned)(sc * (BR + BC) * KC * 8));
+          for (int c = 0; c < sc; ++c)
+            bulk_g2s(sR + (stage * SC + c) * BR * KC, a.Wt + ((size_t)(kb0 + c) * a.mpad + r0) * KC,
+                     BR * KC * 8, &full[stage]);
         }
         __syncwarp();
-        for (int q = lane; q < ncr; q += 32) {
-          const int i0 = crun[q], len = crun[q + 1] - i0;
-          bulk_g2s(sCc + stage * BC * KC + i0 * KC, a.Wnt + ((size_t)kb * a.mpad + cw[i0]) * KC,
-                   (unsigned)len * KC * 8u, &full[stage]);
+        for (int q = lane; q < ncr * sc; q += 32) {
+          const int c = q / ncr, qq = q - c * ncr;
+          const int i0 = crun[qq], len = crun[qq + 1] - i0;
+          bulk_g2s(sCc + (stage * SC + c) * BC * KC + i0 * KC,
+                   a.Wnt + ((size_t)(kb0 + c) * a.mpad + cw[i0]) * KC, (unsigned)len * KC * 8u,
+                   &full[stage]);
         }
         if (++stage == STAGES) {
           stage = 0;
@@ -549,27 +556,32 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
       }
     __syncwarp();
     if (lane == 0) mbar_arrive(cempty);
-    for (int kb = 0; kb < a.n_k; ++kb) {
+    for (int kb0 = 0; kb0 < a.n_k; kb0 += SC) {
+      const int sc = min(SC, a.n_k - kb0);
       mbar_wait(&full[stage], fphase);
-      const double* tR = sR + stage * BR * KC;
-      const double* tC = sCc + stage * BC * KC;
 #pragma unroll
-      for (int k4 = 0; k4 < KC / 4; ++k4) {
-        double fa[4], fb[4];
+      for (int c = 0; c < SC; ++c) {
+        if (c < sc) {
+          const double* tR = sR + (stage * SC + c) * BR * KC;
+          const double* tC = sCc + (stage * SC + c) * BC * KC;
+          // rows wc+8i+g / wr+8j+g are == g (mod 4): the swizzle offset only
+          // depends on (k4 + g), so each fragment is base + compile-time offset
+          const double* bC = tC + (wc + g) * KC + t;
+          const double* bR = tR + (wr + g) * KC + t;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int row = wc + i * 8 + g;
-          fa[i] = tC[row * KC + (((k4 + row) & 3) << 2) + t];
+          for (int k4 = 0; k4 < KC / 4; ++k4) {
+            const int sw = ((k4 + g) & 3) << 2;
+            double fa[4], fb[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) fa[i] = bC[i * 8 * KC + sw];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) fb[j] = bR[j * 8 * KC + sw];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) dmma884(acc[i][j], fa[i], fb[j]);
+          }
         }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int row = wr + j * 8 + g;
-          fb[j] = tR[row * KC + (((k4 + row) & 3) << 2) + t];
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) dmma884(acc[i][j], fa[i], fb[j]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
