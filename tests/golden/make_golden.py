@@ -93,5 +93,7 @@ if __name__ == "__main__":
         wave()
     if "random" in which:
         random_cases()
+    if "c3mini" in which:  # Nt = 420 (the CSZ block size) at oracle-friendly scale
+        synthetic_case("c3mini", 12, 420, 4096, 1.0, 2024, 6, workers=os.cpu_count(), replay=True)
     if "c2" in which:
         synthetic_case("c2", 200, 128, 8192, 1.0, 2024, 50, workers=os.cpu_count())

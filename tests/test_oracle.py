@@ -177,3 +177,13 @@ def test_oracle_vs_reference_live():
         a = O.ref_parallel_greedy(k, 9, 3, 5, workers=3, seed=seed)
         b = O.greedy_select(k, 9, 3, 5)
         assert a.chosen == b.chosen and a.gains == b.gains
+
+
+def test_c3mini_golden_is_reference_output(golden_dir):
+    g = json.load(open(os.path.join(golden_dir, "c3mini.json")))
+    assert g["n_steps"] == 420 and len(g["chosen"]) == 6
+    # the replay of the reference's own sequence picks the reference winner each round
+    for rnd, s in enumerate(g["chosen"]):
+        row = g["replay_gains"][rnd]
+        best = max((x, -j) for j, x in enumerate(row) if x is not None)
+        assert -best[1] == s and best[0] == g["gains"][rnd]
