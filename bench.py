@@ -249,7 +249,8 @@ def our_arm(args, world, rank, local):
         cpu = cpu_reference(cpu_k, nd, nt, budget, chosen)
     eng.close()
 
-    traffic = ncu_traffic(os.path.join(ROOT, "profiles"))
+    tr = ncu_traffic(os.path.join(ROOT, "profiles"))
+    traffic = tr.get("traffic_bytes_per_launch") if tr else None
     peak = FP64_DMMA_PEAK_TFLOPS
     line = {
         "metric": "time-to-k-sensors (s)",
@@ -280,13 +281,17 @@ def our_arm(args, world, rank, local):
                          "end_to_end_tflops_all_gpus": round(e2e_tf, 3),
                          "frac_of_fp64_peak_per_gpu": round(upd_tf / peak, 4),
                          "flop_model": "full-square right-looking: sum_t 2*Nt*(R_t*Nt)*(R_loc,t*Nt)"},
-        "roofline": {"bound": "tensor", "kernel": "schur_update_kernel (DMMA.8x8x4)",
+        "roofline": {"bound": "tensor", "kernel": "schur_update_ws_kernel (DMMA.8x8x4, TMA bulk)",
                      "achieved": round(upd_tf, 3), "peak": peak, "unit": "TFLOP/s",
                      "frac": round(upd_tf / peak, 4),
                      "peak_source": "measured FP64 DMMA peak on this pool's B200 "
                                     "(profiles/r01_fp64_peak_probe.log; cuBLAS DGEMM "
                                     f"{FP64_CUBLAS_TFLOPS}); MEASURED_PEAKS.json has no FP64 entry",
-                     "traffic": traffic},
+                     "traffic": traffic,
+                     "traffic_note": (f"dram read+write of one update launch ({tr['launch']}) "
+                                      f"from ncu --set full; algorithmic C read+write "
+                                      f"{tr['algorithmic_bytes_per_launch']:.4g} B "
+                                      f"(x{tr['traffic_over_algorithmic']})") if tr else None},
         "e2e": e2e,
         "gpu_launches": int(sum(launches) / len(launches)) if launches else 0,
         "clocks": clocks,
@@ -325,7 +330,8 @@ def cpu_reference(k_host, nd, nt, budget, prefix, iterates=None):
     total = sum(a * alg1_round_cost(nd, nt, k) + b * (nd - k) for k in range(budget))
     return {"value": round(total, 3), "unit": "s", "cores": cores, "kind": "reference",
             "sample": f"reference run_parallel_greedy round (detail::timed_round, {cores} "
-                      f"workers) timed at iterates {iterates} = {[round(x, 1) for x in ms]} ms; "
+                      f"workers) timed at iterates {list(iterates)} = "
+                      f"{[round(float(x), 1) for x in ms]} ms; "
                       f"time-to-{budget} EXTRAPOLATED with the Alg.1 cost model "
                       f"(a={a:.3e} s/flop, b={b:.3e} s/cand)",
             "sampled_rounds_ms": list(map(float, ms)), "setup_ms": list(map(float, setup))}
