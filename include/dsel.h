@@ -66,6 +66,9 @@ typedef struct {
   int keep_pristine;      /* keep a device copy of K so dsel_reset can rerun */
   int export_factor;      /* keep per-step W rows so dsel_export_factor can rebuild L_S */
   double near_tie_tau;    /* near-tie flag threshold (default 1e-9 when 0) */
+  int full_square;        /* 0 (default): update only the block-lower triangle of the
+                             symmetric C (half the flops); 1: full square C[:,J] update.
+                             Odd n_steps always use the full square. */
 } dsel_config;
 
 /* One selection round; field names follow TraceRow (selector.hpp:40-49) and

@@ -29,7 +29,8 @@ class DselConfig(C.Structure):
                 ("n_candidates", C.c_int), ("candidates", C.POINTER(C.c_int)),
                 ("device", C.c_int), ("world_size", C.c_int), ("rank", C.c_int),
                 ("nccl_id", C.c_void_p), ("storage", C.c_int), ("keep_pristine", C.c_int),
-                ("export_factor", C.c_int), ("near_tie_tau", C.c_double)]
+                ("export_factor", C.c_int), ("near_tie_tau", C.c_double),
+                ("full_square", C.c_int)]
 
 
 class DselStepInfo(C.Structure):

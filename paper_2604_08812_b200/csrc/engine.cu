@@ -85,6 +85,10 @@ struct dsel_engine {
   int eff_budget = 0;
   int n_sms = 148;
   int mpad = 0;  // rows of the tiled W buffers
+  bool sym = true;  // block-lower-triangle (symmetric) update
+  int* d_sym = nullptr;  // [first_rt per column tile | group prefix]
+  int* h_sym = nullptr;  // pinned
+  int sym_tiles = 0;
   bool keep = false, export_factor = false;
   double tau = 1e-9;
   std::vector<int> pos_sensor, sensor_pos, slot_sensor;
@@ -284,6 +288,32 @@ void set_smem_limits(int dev) {
   allow_smem(schur_update_ws_kernel, optin);
 }
 
+constexpr int ws_group = 16;
+
+// Block-lower tile schedule of the update (symmetric storage): first needed row
+// tile per column tile and the tile-id prefix per 16-column-tile group.
+void sym_tables(dsel_engine* e) {
+  const int nt = e->nt, R = e->n_rows_tab, Rl = e->n_cols_tab;
+  const int* cg = e->h_tab + e->nc + e->nloc;
+  const int n_rows = R * nt, n_cols = Rl * nt;
+  const int nrt = (n_rows + ws::BR - 1) / ws::BR, nct = (n_cols + ws::BC - 1) / ws::BC;
+  const int ng = (nct + ws_group - 1) / ws_group;
+  int* fr = e->h_sym;
+  int* gp = e->h_sym + nct;
+  for (int ct = 0; ct < nct; ++ct) {
+    const int h = (ct * ws::BC) / nt;
+    fr[ct] = (cg[h] * nt) / ws::BR;
+  }
+  gp[0] = 0;
+  for (int g = 0; g < ng; ++g) {
+    const int ct0 = g * ws_group, gw = std::min(ws_group, nct - ct0);
+    gp[g + 1] = gp[g] + (nrt - fr[ct0]) * gw;
+  }
+  e->sym_tiles = gp[ng];
+  CU(cudaMemcpyAsync(e->d_sym, e->h_sym, sizeof(int) * (size_t)(nct + ng + 1),
+                     cudaMemcpyHostToDevice, e->s));
+}
+
 void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   if (e->finished || (int)e->chosen.size() >= e->eff_budget)
     throw Fail{DSEL_E_STATE, "selection already finished"};
@@ -359,7 +389,7 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
     else
       Lk = lsrc;
   }
-  if (!last) {
+  if (!last && !e->sym) {
     P = (owner == e->rank) ? e->C + (size_t)q * nt * e->n : e->Pbuf;
     if (e->G > 1) {
       NC(ncclGroupStart());
@@ -373,6 +403,28 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   e->n_alive -= 1;
   build_tables(e);
   const int R = e->n_rows_tab, Rl = e->n_cols_tab;
+  if (!last && e->sym) {
+    // symmetric storage: column k of C assembled from the block-lower panels
+    // (own blocks from panel k, the rest transposed from panels i < k), summed
+    // across ranks (each block has exactly one nonzero contributor)
+    P = e->Pbuf;
+    if (e->G > 1) CU(cudaMemsetAsync(e->Pbuf, 0, sizeof(double) * (size_t)e->n * nt, e->s));
+    if (R > 0) {
+      const long long total = (long long)R * nt * nt;
+      gather_panel_sym_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 32), 256, 0,
+                                e->s>>>(e->C, e->n, nt, e->row_pos(), R, p, e->G, e->rank, e->Pbuf);
+      CU(cudaGetLastError());
+      e->launches += 1;
+    }
+    if (e->G > 1) {
+      NC(ncclGroupStart());
+      NC(ncclAllReduce(e->Pbuf, e->Pbuf, (size_t)e->n * nt, ncclDouble, ncclSum, e->comm, e->s));
+      NC(ncclBroadcast(e->Lk, e->Lk, (size_t)nt * nt, ncclDouble, owner, e->comm, e->s));
+      NC(ncclGroupEnd());
+      bytes += (uint64_t)(2 * e->n + nt) * nt * sizeof(double) * (uint64_t)(e->G - 1) / e->G;
+    }
+    sym_tables(e);
+  }
   double flops = 0.0;
   if (!last) {
     const int tb = 256 / 32;
@@ -450,9 +502,13 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       ua.n_cols = n_cols;
       ua.n_row_tiles = (n_rows + ws::BR - 1) / ws::BR;
       ua.n_col_tiles = (n_cols + ws::BC - 1) / ws::BC;
-      ua.group = 16;
-      const long long tiles = (long long)ua.n_row_tiles * ua.n_col_tiles;
-      const int grid = (int)std::min<long long>(e->n_sms, tiles);
+      ua.group = ws_group;
+      ua.sym = e->sym;
+      ua.first_rt = e->d_sym;
+      ua.gprefix = e->d_sym + ua.n_col_tiles;
+      ua.n_groups = (ua.n_col_tiles + ws_group - 1) / ws_group;
+      ua.n_tiles = e->sym ? e->sym_tiles : ua.n_row_tiles * ua.n_col_tiles;
+      const int grid = (int)std::min<long long>(e->n_sms, ua.n_tiles);
       schur_update_ws_kernel<<<grid, ws::THREADS, ws::SMEM, e->s>>>(ua);
     } else {
       UpdateArgs ua;
@@ -476,8 +532,16 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
     }
     CU(cudaGetLastError());
     e->launches += 1;
-    e->update_flops += 2.0 * nt * (double)(R * nt) * (double)(Rl * nt);
-    flops = 2.0 * nt * (double)n_rows * (double)n_cols;
+    if (e->sym) {
+      // block-lower triangle incl. diagonal blocks: 2 nt^3 sum_h (R - g_h)
+      const int* cg = e->h_tab + e->nc + e->nloc;
+      double blocks = 0.0;
+      for (int h = 0; h < Rl; ++h) blocks += (double)(R - cg[h]);
+      flops = 2.0 * (double)nt * nt * nt * blocks;
+    } else {
+      flops = 2.0 * nt * (double)n_rows * (double)n_cols;
+    }
+    e->update_flops += flops;
   }
   CU(cudaEventRecord(ev[4], e->s));
 
@@ -524,13 +588,14 @@ void destroy_impl(dsel_engine* e) {
                     e->kgain, e->stage, e->xbuf};
   for (double* d : dptr)
     if (d) cudaFree(d);
-  int* iptr[] = {e->status, e->kstatus, e->d_pos_sensor, e->d_slot_sensor, e->d_tab};
+  int* iptr[] = {e->status, e->kstatus, e->d_pos_sensor, e->d_slot_sensor, e->d_tab, e->d_sym};
   for (int* d : iptr)
     if (d) cudaFree(d);
   if (e->d_rec) cudaFree(e->d_rec);
   if (e->d_recs) cudaFree(e->d_recs);
   if (e->h_recs) cudaFreeHost(e->h_recs);
   if (e->h_tab) cudaFreeHost(e->h_tab);
+  if (e->h_sym) cudaFreeHost(e->h_sym);
   if (e->h_stage) cudaFreeHost(e->h_stage);
   if (e->comm) ncclCommDestroy(e->comm);
   for (int b = 0; b < 2; ++b) {
@@ -615,7 +680,14 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     } else {
       e->Wn = dmalloc<double>((size_t)e->n * e->ldw, tot);
     }
-    if (e->G > 1) e->Pbuf = dmalloc<double>((size_t)e->n * e->nt, tot);
+    e->sym = cfg->full_square == 0 && e->nt % 2 == 0;
+    if (e->G > 1 || e->sym) e->Pbuf = dmalloc<double>((size_t)e->n * e->nt, tot);
+    {
+      const size_t nct = (size_t)(e->nloc * e->nt + ws::BC - 1) / ws::BC + 2;
+      const size_t nsym = nct + nct / ws_group + 4;
+      e->d_sym = dmalloc<int>(nsym, tot);
+      CU(cudaMallocHost(&e->h_sym, sizeof(int) * nsym));
+    }
     e->Lk = dmalloc<double>((size_t)e->nt * e->nt, tot);
     e->Linv = dmalloc<double>((size_t)e->ldw * e->ldw, tot);
     e->Lscr = dmalloc<double>((size_t)std::max(e->nloc, 1) * e->nt * e->nt, tot);
@@ -935,8 +1007,14 @@ dsel_status dsel_read_block_row(dsel_engine* e, int j, double* host_row) {
     CU(cudaMemsetAsync(e->stage, 0, elems * sizeof(double), e->s));
     const long long total = (long long)e->nc * e->nt * e->nt;
     const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
-    gather_block_row_kernel<<<blocks, 256, 0, e->s>>>(e->C + (size_t)q * e->nt * e->n, e->n,
-                                                      e->nt, e->d_pos_sensor, e->nc, e->stage);
+    if (e->sym && !e->trace.empty()) {
+      if (e->G != 1) throw Fail{DSEL_E_STATE, "read_block_row after rounds needs world_size 1 in symmetric storage"};
+      gather_block_row_sym_kernel<<<blocks, 256, 0, e->s>>>(e->C, e->n, e->nt, p, e->d_pos_sensor,
+                                                            e->nc, e->stage);
+    } else {
+      gather_block_row_kernel<<<blocks, 256, 0, e->s>>>(e->C + (size_t)q * e->nt * e->n, e->n,
+                                                        e->nt, e->d_pos_sensor, e->nc, e->stage);
+    }
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(e->h_stage, e->stage, elems * sizeof(double), cudaMemcpyDeviceToHost, e->s));
     CU(cudaStreamSynchronize(e->s));

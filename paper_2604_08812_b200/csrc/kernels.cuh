@@ -329,7 +329,39 @@ struct UpdateWSArgs {
   int nt;
   int n_rows, n_cols;
   int n_row_tiles, n_col_tiles, group;
+  // block-lower-triangle (symmetric) mode: only tiles intersecting blocks
+  // (i, j) with i >= j are updated; first_rt[ct] = first needed row tile of
+  // column tile ct, gprefix[g] = first tile id of column-tile group g.
+  int sym;
+  const int* first_rt;
+  const int* gprefix;
+  int n_groups;
+  int n_tiles;
 };
+
+// tile id -> (r0, c0); false when the tile lies above the block diagonal
+__device__ __forceinline__ bool ws_tile(const UpdateWSArgs& a, int id, int& r0, int& c0) {
+  if (!a.sym) {
+    const int gsz = a.group * a.n_row_tiles;
+    const int grp = id / gsz;
+    const int within = id - grp * gsz;
+    const int ct0 = grp * a.group;
+    const int gw = min(a.group, a.n_col_tiles - ct0);
+    r0 = (within / gw) * 128;
+    c0 = (ct0 + within % gw) * 64;
+    return true;
+  }
+  int g = 0;
+  while (g + 1 < a.n_groups && a.gprefix[g + 1] <= id) ++g;
+  const int local = id - a.gprefix[g];
+  const int ct0 = g * a.group;
+  const int gw = min(a.group, a.n_col_tiles - ct0);
+  const int rt = a.first_rt[ct0] + local / gw;
+  const int ct = ct0 + local % gw;
+  r0 = rt * 128;
+  c0 = ct * 64;
+  return rt >= a.first_rt[ct];
+}
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -385,7 +417,7 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
   int* cw = reinterpret_cast<int*>(smem_raw + OFF_RUNS);        // [BC] W row of each c column
   int* runs = cw + BC;                                          // row runs: start,len pairs
   const int nt = a.nt;
-  const int n_tiles = a.n_row_tiles * a.n_col_tiles;
+  const int n_tiles = a.n_tiles;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -409,17 +441,9 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
     int stage = 0;
     unsigned ephase = 0;
     int it = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       int r0, c0;
-      {
-        const int gsz = a.group * a.n_row_tiles;
-        const int grp = tile / gsz;
-        const int within = tile - grp * gsz;
-        const int ct0 = grp * a.group;
-        const int gw = min(a.group, a.n_col_tiles - ct0);
-        r0 = (within / gw) * BR;
-        c0 = (ct0 + within % gw) * BC;
-      }
+      if (!ws_tile(a, tile, r0, c0)) continue;
       const int nrv = min(BR, a.n_rows - r0);  // valid rows of the tile
       const int ncv = min(BC, a.n_cols - c0);  // valid columns
       const int b = it & 1;
@@ -530,6 +554,7 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
           ephase ^= 1;
         }
       }
+      ++it;
     }
     return;
   }
@@ -541,7 +566,11 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
   int stage = 0;
   unsigned fphase = 0;
   int it = 0;
-  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    {
+      int r0_, c0_;
+      if (!ws_tile(a, tile, r0_, c0_)) continue;
+    }
     const int b = it & 1;
     mbar_wait(&tfull[b], (it >> 1) & 1);
     double acc[4][4][2];
@@ -606,6 +635,7 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&mempty[b]);
+    ++it;
   }
 }
 
@@ -1152,6 +1182,53 @@ __global__ void gather_block_row_kernel(const double* panel, long long ldc, int 
     const int c = (int)(rest / n_cand);
     row[(size_t)pos_sensor[p] * nt * nt + (size_t)c * nt + r] =
         panel[(size_t)c * ldc + (size_t)p * nt + r];
+  }
+}
+
+// Symmetric (block-lower) storage: column k of C for the live blocks, into a
+// full-height panel P (column-major, physical rows). Block (i,k) is stored in
+// panel k when p_i >= p_k, else as block (k,i)^T in panel i. Each rank writes
+// the blocks whose source panel it owns (the others stay zero for the
+// all-reduce that assembles P across ranks).
+__global__ void gather_panel_sym_kernel(const double* C, long long ldc, int nt, const int* row_pos,
+                                        int n_blocks, int pk, int G, int rank, double* P) {
+  const long long n2 = (long long)nt * nt;
+  const long long total = n2 * n_blocks;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int blk = (int)(e / n2);
+    const long long w = e - (long long)blk * n2;
+    const int c = (int)(w / nt), r = (int)(w - (long long)c * nt);  // P[(pi*nt + r), c]
+    const int pi = row_pos[blk];
+    double v;
+    if (pi >= pk) {
+      if (pk % G != rank) continue;
+      v = C[(size_t)((pk / G) * nt + c) * ldc + (size_t)pi * nt + r];
+    } else {
+      if (pi % G != rank) continue;
+      v = C[(size_t)((pi / G) * nt + r) * ldc + (size_t)pk * nt + c];
+    }
+    P[(size_t)c * ldc + (size_t)pi * nt + r] = v;
+  }
+}
+
+// Block row j of the current C in symmetric storage (single rank): block
+// (j,i) = panel j's block (i,j)^T when p_i >= p_j, else panel i's block (j,i).
+__global__ void gather_block_row_sym_kernel(const double* C, long long ldc, int nt, int pj,
+                                            const int* pos_sensor, int n_cand, double* row) {
+  const long long total = (long long)n_cand * nt * nt;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e % nt);  // column index inside block (j,i)
+    const long long rest = e / nt;
+    const int p = (int)(rest % n_cand);
+    const int c = (int)(rest / n_cand);  // row index inside block (j,i)
+    double v;
+    if (p >= pj)
+      v = C[(size_t)(pj * nt + c) * ldc + (size_t)p * nt + r];
+    else
+      v = C[(size_t)(p * nt + r) * ldc + (size_t)pj * nt + c];
+    row[(size_t)pos_sensor[p] * nt * nt + (size_t)c * nt + r] = v;
   }
 }
 

@@ -108,7 +108,7 @@ class Engine:
     def __init__(self, n_sensors: int, n_steps: int, budget: int, candidates=None, device: int = 0,
                  world_size: int = 1, rank: int = 0, nccl_id: bytes | None = None,
                  keep_pristine: bool = False, export_factor: bool = False,
-                 near_tie_tau: float = 1e-9, storage: int = 0):
+                 near_tie_tau: float = 1e-9, storage: int = 0, full_square: bool = False):
         cfg = DselConfig()
         cfg.n_sensors, cfg.n_steps, cfg.budget = n_sensors, n_steps, budget
         self._cands = None
@@ -125,6 +125,7 @@ class Engine:
         cfg.keep_pristine = int(keep_pristine)
         cfg.export_factor = int(export_factor)
         cfg.near_tie_tau = near_tie_tau
+        cfg.full_square = int(full_square)
         h = C.c_void_p()
         _check(lib.dsel_create(C.byref(cfg), C.byref(h)), None)
         self.h = h
