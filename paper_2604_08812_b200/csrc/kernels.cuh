@@ -308,7 +308,9 @@ constexpr size_t OFF_MAPS = OFF_CT + (size_t)BC * CP * 8;                // 2 x 
 constexpr size_t MAPS_BYTES = (size_t)BC * 8 + BR * 4;
 constexpr size_t OFF_RUNS = OFF_MAPS + 2 * MAPS_BYTES;                   // producer scratch
 constexpr size_t OFF_BAR = OFF_RUNS + (size_t)(2 * BC + BR + 8) * 8;
-constexpr size_t SMEM = OFF_BAR + 16 * 8;
+constexpr int MAX_SYM_CT = 1024;  // column tiles whose schedule fits in shared memory
+constexpr size_t OFF_SYM = OFF_BAR + 16 * 8;
+constexpr size_t SMEM = OFF_SYM + (size_t)(MAX_SYM_CT + MAX_SYM_CT / 16 + 4) * 4;
 }  // namespace ws
 
 __host__ __device__ __forceinline__ size_t wt_index(int row, int k, int mpad) {
@@ -339,8 +341,10 @@ struct UpdateWSArgs {
   int n_tiles;
 };
 
-// tile id -> (r0, c0); false when the tile lies above the block diagonal
-__device__ __forceinline__ bool ws_tile(const UpdateWSArgs& a, int id, int& r0, int& c0) {
+// tile id -> (r0, c0); false when the tile lies above the block diagonal.
+// fr / gp: first_rt and gprefix staged in shared memory (binary search).
+__device__ __forceinline__ bool ws_tile(const UpdateWSArgs& a, const int* fr, const int* gp, int id,
+                                        int& r0, int& c0) {
   if (!a.sym) {
     const int gsz = a.group * a.n_row_tiles;
     const int grp = id / gsz;
@@ -351,16 +355,20 @@ __device__ __forceinline__ bool ws_tile(const UpdateWSArgs& a, int id, int& r0, 
     c0 = (ct0 + within % gw) * 64;
     return true;
   }
-  int g = 0;
-  while (g + 1 < a.n_groups && a.gprefix[g + 1] <= id) ++g;
-  const int local = id - a.gprefix[g];
-  const int ct0 = g * a.group;
+  int lo = 0, hi = a.n_groups - 1;  // largest g with gp[g] <= id
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (gp[mid] <= id) lo = mid;
+    else hi = mid - 1;
+  }
+  const int local = id - gp[lo];
+  const int ct0 = lo * a.group;
   const int gw = min(a.group, a.n_col_tiles - ct0);
-  const int rt = a.first_rt[ct0] + local / gw;
+  const int rt = fr[ct0] + local / gw;
   const int ct = ct0 + local % gw;
   r0 = rt * 128;
   c0 = ct * 64;
-  return rt >= a.first_rt[ct];
+  return rt >= fr[ct];
 }
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -420,6 +428,17 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
   const int n_tiles = a.n_tiles;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+  // tile schedule (symmetric mode) in shared memory
+  int* sfr = reinterpret_cast<int*>(smem_raw + OFF_SYM);
+  int* sgp = sfr + MAX_SYM_CT;
+  const int* fr = a.first_rt;
+  const int* gp = a.gprefix;
+  if (a.sym && a.n_col_tiles <= MAX_SYM_CT) {
+    for (int i = threadIdx.x; i < a.n_col_tiles; i += blockDim.x) sfr[i] = a.first_rt[i];
+    for (int i = threadIdx.x; i <= a.n_groups; i += blockDim.x) sgp[i] = a.gprefix[i];
+    fr = sfr;
+    gp = sgp;
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -443,7 +462,7 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
     int it = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       int r0, c0;
-      if (!ws_tile(a, tile, r0, c0)) continue;
+      if (!ws_tile(a, fr, gp, tile, r0, c0)) continue;
       const int nrv = min(BR, a.n_rows - r0);  // valid rows of the tile
       const int ncv = min(BC, a.n_cols - c0);  // valid columns
       const int b = it & 1;
@@ -569,7 +588,7 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     {
       int r0_, c0_;
-      if (!ws_tile(a, tile, r0_, c0_)) continue;
+      if (!ws_tile(a, fr, gp, tile, r0_, c0_)) continue;
     }
     const int b = it & 1;
     mbar_wait(&tfull[b], (it >> 1) & 1);
