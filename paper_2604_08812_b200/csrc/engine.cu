@@ -286,6 +286,9 @@ void set_smem_limits(int dev) {
   allow_smem(panel_w_kernel<2>, optin);
   allow_smem(panel_w_kernel<1>, optin);
   allow_smem(schur_update_ws_kernel, optin);
+  allow_smem(trinv_smem_kernel<4>, optin);
+  allow_smem(trinv_smem_kernel<8>, optin);
+  allow_smem(trinv_smem_kernel<14>, optin);
 }
 
 constexpr int ws_group = 16;
@@ -430,15 +433,21 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
     const int tb = 256 / 32;
     {
       const unsigned g = (unsigned)((e->ldw + tb - 1) / tb);
-      const size_t sm = (size_t)nt * sizeof(double);
-      if (e->ldw <= 128)
-        trinv_kernel<4><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
-      else if (e->ldw <= 256)
-        trinv_kernel<8><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
-      else if (e->ldw <= 512)
-        trinv_kernel<16><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
-      else
-        trinv_kernel<32><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+      if (nt <= TRINV_SMEM_MAX_NT) {
+        const size_t sm = ((size_t)2 * 32 * nt + nt) * sizeof(double);
+        if (e->ldw <= 128)
+          trinv_smem_kernel<4><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+        else if (e->ldw <= 256)
+          trinv_smem_kernel<8><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+        else
+          trinv_smem_kernel<14><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+      } else {
+        const size_t sm = (size_t)nt * sizeof(double);
+        if (e->ldw <= 512)
+          trinv_kernel<16><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+        else
+          trinv_kernel<32><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+      }
     }
     CU(cudaGetLastError());
     e->launches += 1;
@@ -448,8 +457,13 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       pa.ldp = e->n;
       pa.Linv = e->Linv;
       pa.ldl = e->ldw;
-      pa.W = e->W;
+      pa.W = e->Wt ? nullptr : e->W;
       pa.Wn = e->Wn;
+      pa.hist = e->export_factor ? e->hist : nullptr;
+      pa.slot_stride = (long long)e->eff_budget * nt * nt;
+      pa.step_off = (long long)round * nt * nt;
+      pa.G = e->G;
+      pa.rank = e->rank;
       pa.Wt = e->Wt;
       pa.Wnt = e->Wnt;
       pa.mpad = e->mpad;
@@ -469,13 +483,6 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   if (e->export_factor) {
     const long long n2 = (long long)nt * nt;
     const long long slot_stride = (long long)e->eff_budget * n2;
-    if (!last && Rl > 0) {
-      dim3 grid((unsigned)std::min<long long>((n2 + 255) / 256, 64), Rl);
-      hist_copy_kernel<<<grid, 256, 0, e->s>>>(e->W, e->ldw, e->col_slot(), e->col_g(), Rl, nt,
-                                               e->hist, slot_stride, (long long)round * n2);
-      CU(cudaGetLastError());
-      e->launches += 1;
-    }
     if (owner == e->rank) {
       hist_diag_kernel<<<(unsigned)std::min<long long>((n2 + 255) / 256, 1024), 256, 0, e->s>>>(
           Lk, nt, e->hist + (long long)q * slot_stride + (long long)round * n2);
@@ -672,7 +679,7 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     const size_t shard = (size_t)e->n * (size_t)e->nloc * e->nt;
     e->C = dmalloc<double>(shard, tot);
     if (e->keep) e->K0 = dmalloc<double>(shard, tot);
-    e->W = dmalloc<double>((size_t)e->n * e->ldw, tot);
+    if (e->nt % 2) e->W = dmalloc<double>((size_t)e->n * e->ldw, tot);  // odd-nt update path
     e->mpad = round_up((int)e->n, ws::BR);
     if (e->nt % 2 == 0) {
       e->Wt = dmalloc<double>((size_t)e->mpad * e->ldw, tot);
@@ -706,7 +713,7 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     e->d_recs = dmalloc<ArgRec>(e->G, tot);
     CU(cudaMallocHost(&e->h_recs, sizeof(ArgRec) * e->G));
     CU(cudaMallocHost(&e->h_tab, sizeof(int) * ((size_t)e->nc + 2 * e->nloc + 1)));
-    CU(cudaMemsetAsync(e->W, 0, sizeof(double) * (size_t)e->n * e->ldw, e->s));
+    if (e->W) CU(cudaMemsetAsync(e->W, 0, sizeof(double) * (size_t)e->n * e->ldw, e->s));
     if (e->Wn) CU(cudaMemsetAsync(e->Wn, 0, sizeof(double) * (size_t)e->n * e->ldw, e->s));
     if (e->Wt) {
       CU(cudaMemsetAsync(e->Wt, 0, sizeof(double) * (size_t)e->mpad * e->ldw, e->s));

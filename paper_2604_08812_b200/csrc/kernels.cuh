@@ -678,7 +678,7 @@ struct PanelArgs {
   long long ldp;
   const double* Linv;   // row-major [c][m], ld = ldl, zero above the diagonal and in pads
   int ldl;
-  double* W;            // out, row-major, ld = ldw
+  double* W;            // out, row-major, ld = ldw; may be null
   double* Wn;           // out, -W (same layout); may be null
   double* Wt;           // out, +W tiled (wt_index); may be null
   double* Wnt;          // out, -W tiled; may be null
@@ -687,6 +687,11 @@ struct PanelArgs {
   const int* row_pos;   // compact block -> position
   int nt;
   int n_rows;           // R * nt
+  // factor history (export_factor): W rows of this rank's candidates go to
+  // hist[slot][round] (nt x nt row-major), fused into the epilogue
+  double* hist;
+  long long slot_stride, step_off;
+  int G, rank;
 };
 
 template <int VEC>
@@ -795,7 +800,17 @@ __global__ void __launch_bounds__(pw::THREADS, 2) panel_w_kernel(PanelArgs a) {
         double2 v;
         v.x = acc[i][j][0];
         v.y = c + 1 < nt ? acc[i][j][1] : 0.0;
-        *reinterpret_cast<double2*>(a.W + (size_t)r * a.ldw + c) = v;
+        if (a.W) *reinterpret_cast<double2*>(a.W + (size_t)r * a.ldw + c) = v;
+        if (a.hist) {
+          const int blk = r / nt;
+          const int pos = a.row_pos[blk];
+          if (pos % a.G == a.rank) {
+            double* h = a.hist + (long long)(pos / a.G) * a.slot_stride + a.step_off +
+                        (size_t)(r - blk * nt) * nt + c;
+            h[0] = v.x;
+            if (c + 1 < nt) h[1] = v.y;
+          }
+        }
         if (a.Wn)
           *reinterpret_cast<double2*>(a.Wn + (size_t)r * a.ldw + c) = make_double2(-v.x, -v.y);
         if (a.Wt) {
@@ -1025,10 +1040,21 @@ __global__ void __launch_bounds__(256) trinv_kernel(const double* L, int nt, dou
   const int lane = threadIdx.x & 31;
   const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (j >= ldl) return;
-  double x[S];
+  double x[S], cur[S], nxt[S];
 #pragma unroll
   for (int s = 0; s < S; ++s) x[s] = (lane + 32 * s == j) ? 1.0 : 0.0;
+  // column m of L for this lane's rows, prefetched one step ahead so the
+  // L2 latency overlaps the pivot chain
+  auto load_col = [&](int m, double (&dst)[S]) {
+    const double* col = L + (size_t)m * nt;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int i = lane + 32 * s;
+      dst[s] = i < nt ? col[i] : 0.0;
+    }
+  };
   if (j < nt) {
+    load_col(j, cur);
 #pragma unroll
     for (int sb = 0; sb < S; ++sb) {
       if (32 * sb + 31 < j) continue;
@@ -1036,14 +1062,16 @@ __global__ void __launch_bounds__(256) trinv_kernel(const double* L, int nt, dou
         const int m = 32 * sb + ml;
         if (m >= nt) break;
         if (m < j) continue;
+        if (m + 1 < nt) load_col(m + 1, nxt);
         const double xm = __shfl_sync(0xffffffffu, x[sb], ml) * rdiag[m];
         if (lane == ml) x[sb] = xm;
-        const double* colm = L + (size_t)m * nt;
 #pragma unroll
         for (int s = sb; s < S; ++s) {
           const int i = lane + 32 * s;
-          if (i > m && i < nt) x[s] -= xm * colm[i];
+          if (i > m && i < nt) x[s] -= xm * cur[s];
         }
+#pragma unroll
+        for (int s = 0; s < S; ++s) cur[s] = nxt[s];
       }
     }
   }
@@ -1053,6 +1081,70 @@ __global__ void __launch_bounds__(256) trinv_kernel(const double* L, int nt, dou
     if (i < ldl) Linv[(size_t)i * ldl + j] = (j < nt && i < nt && i >= j) ? x[s] : 0.0;
   }
   // pad rows beyond 32*S (ldl > 32*S never happens: ldl <= 32*S by dispatch)
+}
+
+// Shared-memory variant (nt <= 432): the factor columns stream through a
+// double-buffered 32-column smem window (cp.async), so every step of the
+// pivot chain reads L from shared memory instead of L2.
+constexpr int TRINV_SMEM_MAX_NT = 432;
+template <int S>
+__global__ void __launch_bounds__(256) trinv_smem_kernel(const double* L, int nt, double* Linv,
+                                                         int ldl) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int mp = nt;                                             // row pitch of a window column
+  double* win = reinterpret_cast<double*>(smem_raw);             // [2][32][mp]
+  double* rdiag = win + 2 * 32 * mp;                             // [nt]
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int j0 = blockIdx.x * 8;                                 // this CTA's first column
+  const int j = j0 + (tid >> 5);
+  for (int m = tid; m < nt; m += 256) rdiag[m] = 1.0 / L[(size_t)m * nt + m];
+  auto load_win = [&](int sb, int buf) {
+    const int m0 = 32 * sb;
+    const int cw = min(32, nt - m0);
+    const int rows = nt - m0;
+    for (int e = tid; e < cw * rows; e += 256) {
+      const int c = e / rows, i = m0 + (e - c * rows);
+      cp_async8(win + ((size_t)buf * 32 + c) * mp + i, L + (size_t)(m0 + c) * nt + i, true);
+    }
+    cp_async_commit();
+  };
+  double x[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) x[s] = (lane + 32 * s == j) ? 1.0 : 0.0;
+  const int sb0 = j0 >> 5;  // first window any warp of this CTA needs
+  const int nwin = (nt + 31) >> 5;
+  if (sb0 < nwin) load_win(sb0, sb0 & 1);
+#pragma unroll
+  for (int sb = 0; sb < S; ++sb) {
+    if (sb < sb0 || sb >= nwin) continue;
+    if (sb + 1 < nwin) load_win(sb + 1, (sb + 1) & 1);
+    if (sb + 1 < nwin) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    __syncthreads();
+    const double* w = win + (size_t)(sb & 1) * 32 * mp;
+    if (j < nt) {
+      for (int ml = 0; ml < 32; ++ml) {
+        const int m = 32 * sb + ml;
+        if (m >= nt) break;
+        if (m < j) continue;
+        const double xm = __shfl_sync(0xffffffffu, x[sb], ml) * rdiag[m];
+        if (lane == ml) x[sb] = xm;
+        const double* col = w + (size_t)ml * mp;
+#pragma unroll
+        for (int s = sb; s < S; ++s) {
+          const int i = lane + 32 * s;
+          if (i > m && i < nt) x[s] -= xm * col[i];
+        }
+      }
+    }
+    __syncthreads();  // window buffer reused two windows later
+  }
+  if (j >= ldl) return;
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int i = lane + 32 * s;
+    if (i < ldl) Linv[(size_t)i * ldl + j] = (j < nt && i < nt && i >= j) ? x[s] : 0.0;
+  }
 }
 
 // ------------------------------------------------------------------------ //
@@ -1126,20 +1218,6 @@ __global__ void __launch_bounds__(256) argmax_kernel(const double* gain, const i
 // Factor-export history: hist[slot][step] = W rows of the local candidate   //
 // (nt x nt row-major) -- one block of L_S (linalg.hpp:159-178 layout).     //
 // ------------------------------------------------------------------------ //
-__global__ void hist_copy_kernel(const double* W, int ldw, const int* col_slot, const int* col_g,
-                                 int n_blocks, int nt, double* hist, long long slot_stride,
-                                 long long step_off) {
-  const int h = blockIdx.y;
-  if (h >= n_blocks) return;
-  const long long n2 = (long long)nt * nt;
-  double* dst = hist + (long long)col_slot[h] * slot_stride + step_off;
-  const double* srcw = W + (size_t)col_g[h] * nt * ldw;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n2;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(e / nt), c = (int)(e - (long long)r * nt);
-    dst[e] = srcw[(size_t)r * ldw + c];
-  }
-}
 
 // L_k (column-major) -> lower-triangular row-major block into hist.
 __global__ void hist_diag_kernel(const double* Lk, int nt, double* dst) {
