@@ -86,6 +86,7 @@ struct dsel_engine {
   int n_sms = 148;
   int mpad = 0;  // rows of the tiled W buffers
   bool sym = true;  // block-lower-triangle (symmetric) update
+  bool full_panels = true;  // both triangles of every panel hold K (gen_synthetic / full-square load)
   int* d_sym = nullptr;  // [first_rt per column tile | group prefix]
   int* h_sym = nullptr;  // pinned
   int sym_tiles = 0;
@@ -764,6 +765,12 @@ void load_panel(dsel_engine* e, int j, const double* host, bool as_column) {
   if (p < 0 || p % e->G != e->rank) return;
   const int q = p / e->G;
   const size_t elems = (size_t)e->nd * e->nt * e->nt;
+  // symmetric storage needs only the block-lower part of the panel: blocks of
+  // candidates at positions >= p, i.e. sensors >= j -- a contiguous suffix
+  const int s_off = e->sym ? j : 0;
+  const int p_first = e->sym ? p : 0;
+  const size_t off = (size_t)s_off * e->nt * e->nt;
+  const size_t copy = elems - off;
   CU(cudaSetDevice(e->dev));
   ensure_stage(e, elems);
   const int b = e->stage_flip;
@@ -775,25 +782,28 @@ void load_panel(dsel_engine* e, int j, const double* host, bool as_column) {
                       attr.type == cudaMemoryTypeHost;
   cudaGetLastError();
   if (pinned) {
-    CU(cudaMemcpyAsync(buf, host, elems * sizeof(double), cudaMemcpyHostToDevice, e->cs));
+    CU(cudaMemcpyAsync(buf, host + off, copy * sizeof(double), cudaMemcpyHostToDevice, e->cs));
   } else {
     // pageable source: bounce through the engine's pinned buffer
     CU(cudaStreamSynchronize(e->cs));
-    std::memcpy(e->h_stage, host, elems * sizeof(double));
-    CU(cudaMemcpyAsync(buf, e->h_stage, elems * sizeof(double), cudaMemcpyHostToDevice, e->cs));
+    std::memcpy(e->h_stage, host + off, copy * sizeof(double));
+    CU(cudaMemcpyAsync(buf, e->h_stage, copy * sizeof(double), cudaMemcpyHostToDevice, e->cs));
   }
-  e->h2d_bytes += elems * sizeof(double);
+  e->h2d_bytes += copy * sizeof(double);
+  if (e->sym) e->full_panels = false;
   CU(cudaEventRecord(e->ev_copy[b], e->cs));
   CU(cudaStreamWaitEvent(e->s, e->ev_copy[b], 0));
   double* panel = e->C + (size_t)q * e->nt * e->n;
-  const long long total = (long long)e->nc * e->nt * e->nt;
+  const long long total = (long long)(e->nc - p_first) * e->nt * e->nt;
   const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
-  if (as_column)
-    scatter_block_col_kernel<<<blocks, 256, 0, e->s>>>(buf, e->nt, e->d_pos_sensor, e->nc,
-                                                       panel, e->n);
-  else
-    scatter_block_row_kernel<<<blocks, 256, 0, e->s>>>(buf, e->nt, e->d_pos_sensor, e->nc,
-                                                       panel, e->n);
+  if (total > 0) {
+    if (as_column)
+      scatter_block_col_kernel<<<blocks, 256, 0, e->s>>>(buf, e->nt, e->d_pos_sensor, e->nc,
+                                                         panel, e->n, p_first, s_off);
+    else
+      scatter_block_row_kernel<<<blocks, 256, 0, e->s>>>(buf, e->nt, e->d_pos_sensor, e->nc,
+                                                         panel, e->n, p_first, s_off);
+  }
   CU(cudaGetLastError());
   CU(cudaEventRecord(e->ev_scat[b], e->s));
   if (e->keep)
@@ -956,8 +966,9 @@ void load_kbf_impl(dsel_engine* e, const char* path, bool exact_columns, int thr
       double* buf = hb[flip];
       CU(cudaEventSynchronize(freed[flip]));  // its previous H2D has completed
       // parallel pread of the Nd blocks of this panel
+      const int i_first = e->sym ? j : 0;  // block-lower part only (symmetric storage)
       auto work = [&](int w) {
-        for (int i = w; i < nd; i += threads) {
+        for (int i = i_first + w; i < nd; i += threads) {
           const size_t blk = exact_columns ? ((size_t)i * nd + j) : ((size_t)j * nd + i);
           pread_exact(fd, reinterpret_cast<unsigned char*>(buf) + (size_t)i * bsz, bsz,
                       (off_t)(32 + blk * bsz), ps);
@@ -1014,8 +1025,10 @@ dsel_status dsel_read_block_row(dsel_engine* e, int j, double* host_row) {
     CU(cudaMemsetAsync(e->stage, 0, elems * sizeof(double), e->s));
     const long long total = (long long)e->nc * e->nt * e->nt;
     const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
-    if (e->sym && !e->trace.empty()) {
-      if (e->G != 1) throw Fail{DSEL_E_STATE, "read_block_row after rounds needs world_size 1 in symmetric storage"};
+    if (e->sym && (e->G == 1 || !e->full_panels || !e->trace.empty())) {
+      if (e->G != 1)
+        throw Fail{DSEL_E_STATE, "read_block_row of a sharded symmetric store needs full panels "
+                                 "and no rounds (or world_size 1)"};
       gather_block_row_sym_kernel<<<blocks, 256, 0, e->s>>>(e->C, e->n, e->nt, p, e->d_pos_sensor,
                                                             e->nc, e->stage);
     } else {
@@ -1056,6 +1069,7 @@ dsel_status dsel_gen_synthetic(dsel_engine* e, const double* v_host, int rank, d
     }
     cudaFree(V);
     if (ce != cudaSuccess) throw Fail{DSEL_E_CUDA, std::string("synthetic K: ") + cudaGetErrorString(ce)};
+    e->full_panels = true;
     if (e->keep)
       CU(cudaMemcpyAsync(e->K0, e->C, sizeof(double) * e->n * e->nloc * e->nt,
                          cudaMemcpyDeviceToDevice, e->s));

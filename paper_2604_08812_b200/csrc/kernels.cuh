@@ -1236,17 +1236,19 @@ __global__ void hist_diag_kernel(const double* Lk, int nt, double* dst) {
 // KBF / DataSpaceHessian order, kstore.hpp:22-35) -> panel of candidate j,  //
 // using K(i,j)[r][c] = K(j,i)[c][r] (exact for symmetric K).               //
 __global__ void scatter_block_row_kernel(const double* row, int nt, const int* pos_sensor,
-                                         int n_cand, double* panel, long long ldc) {
-  // panel[(c)*ldc + p*nt + r] = row[sensor(p)*nt*nt + c*nt + r]
-  const long long total = (long long)n_cand * nt * nt;
+                                         int n_cand, double* panel, long long ldc, int p_first,
+                                         int s_off) {
+  // panel[(c)*ldc + p*nt + r] = row[(sensor(p) - s_off)*nt*nt + c*nt + r], p >= p_first
+  const int np = n_cand - p_first;
+  const long long total = (long long)np * nt * nt;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const int r = (int)(e % nt);
     const long long rest = e / nt;
-    const int p = (int)(rest % n_cand);
-    const int c = (int)(rest / n_cand);
+    const int p = p_first + (int)(rest % np);
+    const int c = (int)(rest / np);
     panel[(size_t)c * ldc + (size_t)p * nt + r] =
-        row[(size_t)pos_sensor[p] * nt * nt + (size_t)c * nt + r];
+        row[(size_t)(pos_sensor[p] - s_off) * nt * nt + (size_t)c * nt + r];
   }
 }
 
@@ -1254,16 +1256,18 @@ __global__ void scatter_block_row_kernel(const double* row, int nt, const int* p
 // (exact reference semantics: read_test_column reads blocks (S[t], s),
 // kaccess.hpp:27-35).
 __global__ void scatter_block_col_kernel(const double* colblk, int nt, const int* pos_sensor,
-                                         int n_cand, double* panel, long long ldc) {
-  const long long total = (long long)n_cand * nt * nt;
+                                         int n_cand, double* panel, long long ldc, int p_first,
+                                         int s_off) {
+  const int np = n_cand - p_first;
+  const long long total = (long long)np * nt * nt;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const int r = (int)(e % nt);
     const long long rest = e / nt;
-    const int p = (int)(rest % n_cand);
-    const int c = (int)(rest / n_cand);
+    const int p = p_first + (int)(rest % np);
+    const int c = (int)(rest / np);
     panel[(size_t)c * ldc + (size_t)p * nt + r] =
-        colblk[(size_t)pos_sensor[p] * nt * nt + (size_t)r * nt + c];
+        colblk[(size_t)(pos_sensor[p] - s_off) * nt * nt + (size_t)r * nt + c];
   }
 }
 
