@@ -230,13 +230,20 @@ int chol_mp(int nt) {
   return mp;
 }
 
-void launch_chol(const CholArgs& a, int n_batch, cudaStream_t s) {
+void launch_chol(const CholArgs& a, int n_batch, cudaStream_t s, int n_sms) {
   const int nb = chol_nb(a.nt);
   const size_t smem = ((size_t)2 * nb * a.mp + a.nt) * sizeof(double);
-  if (nb == 32)
-    chol_logdet_kernel<32><<<n_batch, 256, smem, s>>>(a);
-  else
-    chol_logdet_kernel<8><<<n_batch, 256, smem, s>>>(a);
+  // more candidates than SMs: squeeze two CTAs per SM (capped registers) so the
+  // batch runs in one wave; otherwise one uncapped CTA per candidate
+  const bool two = n_batch > n_sms;
+  if (nb == 32) {
+    if (two)
+      chol_logdet_kernel<32, 2><<<n_batch, 256, smem, s>>>(a);
+    else
+      chol_logdet_kernel<32, 1><<<n_batch, 256, smem, s>>>(a);
+  } else {
+    chol_logdet_kernel<8, 1><<<n_batch, 256, smem, s>>>(a);
+  }
 }
 
 GainTabs gain_tabs(dsel_engine* e) {
@@ -262,7 +269,7 @@ void run_gain(dsel_engine* e, const int* slots, int n_batch) {
   a.nt = e->nt;
   a.n = n_batch;
   a.mp = chol_mp(e->nt);
-  launch_chol(a, n_batch, e->s);
+  launch_chol(a, n_batch, e->s, e->n_sms);
   CU(cudaGetLastError());
   e->launches += 2;
 }
@@ -280,8 +287,9 @@ void set_smem_limits(int dev) {
   // per device context; cheap, called from dsel_create on the engine's device
   int optin = 0;
   CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  allow_smem(chol_logdet_kernel<32>, optin);
-  allow_smem(chol_logdet_kernel<8>, optin);
+  allow_smem(chol_logdet_kernel<32, 1>, optin);
+  allow_smem(chol_logdet_kernel<32, 2>, optin);
+  allow_smem(chol_logdet_kernel<8, 1>, optin);
   allow_smem(schur_update_kernel<2>, optin);
   allow_smem(schur_update_kernel<1>, optin);
   allow_smem(panel_w_kernel<2>, optin);
