@@ -69,6 +69,11 @@ typedef struct {
   int full_square;        /* 0 (default): update only the block-lower triangle of the
                              symmetric C (half the flops); 1: full square C[:,J] update.
                              Odd n_steps always use the full square. */
+  int algorithm;          /* 0 (default): right-looking Schur update of the resident
+                             conditional covariance (the north-star kernel);
+                             1: left-looking W-resident variant:
+                             K stays pristine, W_all = K[:,S] L_S^{-T} is kept, one
+                             column c = K[:,k] - W_all W_all[k]^T per round. */
 } dsel_config;
 
 /* One selection round; field names follow TraceRow (selector.hpp:40-49) and

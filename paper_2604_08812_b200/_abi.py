@@ -30,7 +30,7 @@ class DselConfig(C.Structure):
                 ("device", C.c_int), ("world_size", C.c_int), ("rank", C.c_int),
                 ("nccl_id", C.c_void_p), ("storage", C.c_int), ("keep_pristine", C.c_int),
                 ("export_factor", C.c_int), ("near_tie_tau", C.c_double),
-                ("full_square", C.c_int)]
+                ("full_square", C.c_int), ("algorithm", C.c_int)]
 
 
 class DselStepInfo(C.Structure):

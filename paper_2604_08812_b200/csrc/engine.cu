@@ -85,6 +85,11 @@ struct dsel_engine {
   int eff_budget = 0;
   int n_sms = 148;
   int mpad = 0;  // rows of the tiled W buffers
+  bool ll = false;  // left-looking W-resident algorithm
+  double *Wown = nullptr, *Wkn = nullptr, *D = nullptr, *cbuf = nullptr, *ldiag = nullptr;
+  int* d_iota = nullptr;
+  int own_mpad = 0, k_mpad = 0;
+  long long ldo = 0;
   bool sym = true;  // block-lower-triangle (symmetric) update
   bool full_panels = true;  // both triangles of every panel hold K (gen_synthetic / full-square load)
   int* d_sym = nullptr;  // [first_rt per column tile | group prefix]
@@ -161,14 +166,48 @@ void build_tables(dsel_engine* e) {
 namespace {
 __global__ void gain_tables_kernel(const int* col_slot, int n, int G, int rank, int nt,
                                    const int* pos_sensor, int* src_col, int* src_row,
-                                   int* sensor) {
+                                   int* sensor, int diag_store) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= n) return;
   const int q = col_slot[b];
   const int p = q * G + rank;
   src_col[b] = q * nt;
-  src_row[b] = p * nt;
+  src_row[b] = diag_store ? 0 : p * nt;  // left-looking: separate D blocks, ld = nt
   sensor[b] = pos_sensor[p];
+}
+
+// left-looking: D[q] = diagonal block of this rank's K panel q
+__global__ void ll_init_d_kernel(const double* C, long long ldc, int nt, int nloc, int G, int rank,
+                                 double* D) {
+  const long long n2 = (long long)nt * nt;
+  const long long total = n2 * nloc;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(e / n2);
+    const long long w = e - (long long)q * n2;
+    const int c = (int)(w / nt), r = (int)(w - (long long)c * nt);
+    const int p = q * G + rank;
+    D[e] = C[(size_t)(q * nt + c) * ldc + (size_t)p * nt + r];
+  }
+}
+
+// left-looking factor export: block row i = [W_own row block (steps 0..i-1), L_k_i]
+__global__ void ll_pack_factor_row_kernel(const double* Wown, int own_mpad, int row0, int nt, int ldw,
+                                          int i_blocks, const double* ldiag_i, double* out) {
+  const long long n2 = (long long)nt * nt;
+  const long long total = n2 * i_blocks;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(e / n2);
+    const long long w = e - (long long)j * n2;
+    const int a = (int)(w / nt), b = (int)(w - (long long)a * nt);
+    double v;
+    if (j + 1 < i_blocks)
+      v = Wown[wt_index(row0 + a, j * ldw + b, own_mpad)];
+    else
+      v = b <= a ? ldiag_i[(size_t)b * nt + a] : 0.0;  // L_k column-major
+    out[(size_t)a * i_blocks * nt + (size_t)j * nt + b] = v;
+  }
 }
 
 
@@ -255,11 +294,12 @@ void run_gain(dsel_engine* e, const int* slots, int n_batch) {
   if (n_batch <= 0) return;
   GainTabs t = gain_tabs(e);
   gain_tables_kernel<<<(n_batch + 127) / 128, 128, 0, e->s>>>(
-      slots, n_batch, e->G, e->rank, e->nt, e->d_pos_sensor, t.src_col, t.src_row, t.sensor);
+      slots, n_batch, e->G, e->rank, e->nt, e->d_pos_sensor, t.src_col, t.src_row, t.sensor,
+      e->ll ? 1 : 0);
   CU(cudaGetLastError());
   CholArgs a;
-  a.src = e->C;
-  a.lds = e->n;
+  a.src = e->ll ? e->D : e->C;
+  a.lds = e->ll ? (long long)e->nt : e->n;
   a.src_col = t.src_col;
   a.src_row = t.src_row;
   a.L = e->Lscr;
@@ -295,6 +335,7 @@ void set_smem_limits(int dev) {
   allow_smem(panel_w_kernel<2>, optin);
   allow_smem(panel_w_kernel<1>, optin);
   allow_smem(schur_update_ws_kernel, optin);
+  allow_smem(ll_gemm_kernel, optin);
   allow_smem(trinv_smem_kernel<4>, optin);
   allow_smem(trinv_smem_kernel<8>, optin);
   allow_smem(trinv_smem_kernel<14>, optin);
@@ -326,6 +367,144 @@ void sym_tables(dsel_engine* e) {
                      cudaMemcpyHostToDevice, e->s));
 }
 
+void finish_row(dsel_engine* e, dsel_step_info& row, int s1, int s2, double g1, double g2,
+                uint64_t bytes, double flops, dsel_step_info* info) {
+  e->chosen.push_back(s1);
+  e->objective += g1;
+  row.chosen_index = s1;
+  row.gain = g1;
+  row.objective = e->objective;
+  row.runner_up = s2;
+  row.runner_up_gain = g2;
+  row.near_tie = (s2 >= 0 && (g1 - g2) / std::max(std::fabs(g1), 1.0) < e->tau) ? 1 : 0;
+  row.bytes_exchanged = bytes;
+  row.update_flops = flops;
+  e->nccl_bytes += bytes;
+  e->trace.push_back(row);
+  if (info) *info = row;
+}
+
+void launch_trinv(dsel_engine* e, const double* Lk) {
+  const int nt = e->nt, tb = 256 / 32;
+  const unsigned g = (unsigned)((e->ldw + tb - 1) / tb);
+  if (nt <= TRINV_SMEM_MAX_NT) {
+    const size_t sm = ((size_t)2 * 32 * nt + nt) * sizeof(double);
+    if (e->ldw <= 128)
+      trinv_smem_kernel<4><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+    else if (e->ldw <= 256)
+      trinv_smem_kernel<8><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+    else
+      trinv_smem_kernel<14><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+  } else {
+    const size_t sm = (size_t)nt * sizeof(double);
+    if (e->ldw <= 512)
+      trinv_kernel<16><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+    else
+      trinv_kernel<32><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+  }
+  CU(cudaGetLastError());
+  e->launches += 1;
+}
+
+// Left-looking round tail: W_k + L_k from the owner, then this rank's rows of
+// the new conditional column, W_t, and the D (gain input) downdate.
+void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, const double* Lk,
+             cudaEvent_t* ev, uint64_t bytes, dsel_step_info& row, double g1, double g2, int s1,
+             int s2, dsel_step_info* info) {
+  const int nt = e->nt;
+  const long long n2 = (long long)nt * nt;
+  const int kcols = round * e->ldw;  // W_all columns so far
+  if (owner == e->rank) {
+    CU(cudaMemcpyAsync(e->ldiag + (size_t)round * n2, Lk, sizeof(double) * n2,
+                       cudaMemcpyDeviceToDevice, e->s));
+    if (!last && e->G > 1 && Lk != e->Lk)
+      CU(cudaMemcpyAsync(e->Lk, Lk, sizeof(double) * n2, cudaMemcpyDeviceToDevice, e->s));
+    if (!last && kcols > 0) {
+      const long long total = (long long)nt * kcols;
+      ll_extract_wk_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 16), 256, 0,
+                             e->s>>>(e->Wown, e->own_mpad, q * nt, nt, kcols, e->Wkn, e->k_mpad);
+      CU(cudaGetLastError());
+      e->launches += 1;
+    }
+  }
+  if (!last && e->G > 1) {
+    NC(ncclGroupStart());
+    if (kcols > 0)
+      NC(ncclBroadcast(e->Wkn, e->Wkn, (size_t)kcols * e->k_mpad, ncclDouble, owner, e->comm, e->s));
+    NC(ncclBroadcast(e->Lk, e->Lk, (size_t)n2, ncclDouble, owner, e->comm, e->s));
+    NC(ncclGroupEnd());
+    bytes += (uint64_t)((size_t)kcols * e->k_mpad + n2) * sizeof(double) * (uint64_t)(e->G - 1);
+    Lk = e->Lk;
+  }
+  e->alive[p] = 0;
+  e->n_alive -= 1;
+  build_tables(e);
+  const int Rl = e->n_cols_tab;
+  double flops = 0.0;
+  if (!last) launch_trinv(e, Lk);
+  CU(cudaEventRecord(ev[3], e->s));
+  if (!last && Rl > 0) {
+    const int n_rows = Rl * nt;
+    LLGemmArgs ga;
+    ga.Wown = e->Wown;
+    ga.own_mpad = e->own_mpad;
+    ga.Wkn = e->Wkn;
+    ga.k_mpad = e->k_mpad;
+    ga.n_k = kcols / 16;
+    ga.Kp = e->C;
+    ga.ldk = e->n;
+    ga.pk = p;
+    ga.row_slot = e->col_slot();
+    ga.nt = nt;
+    ga.n_rows = n_rows;
+    ga.cout = e->cbuf;
+    ga.ldo = e->ldo;
+    dim3 gg((n_rows + llg::BM - 1) / llg::BM, (nt + llg::BN - 1) / llg::BN);
+    ll_gemm_kernel<<<gg, llg::THREADS, llg::SMEM, e->s>>>(ga);
+    CU(cudaGetLastError());
+    PanelArgs pa{};
+    pa.P = e->cbuf;
+    pa.ldp = e->ldo;
+    pa.Linv = e->Linv;
+    pa.ldl = e->ldw;
+    pa.ldw = e->ldw;
+    pa.row_pos = e->d_iota;
+    pa.nt = nt;
+    pa.n_rows = n_rows;
+    pa.Wown = e->Wown;
+    pa.out_slot = e->col_slot();
+    pa.own_mpad = e->own_mpad;
+    pa.koff = kcols;
+    pa.G = e->G;
+    pa.rank = e->rank;
+    dim3 grid((n_rows + pw::BR - 1) / pw::BR, (nt + pw::BN - 1) / pw::BN);
+    if (nt % 2 == 0)
+      panel_w_kernel<2><<<grid, pw::THREADS, pw::SMEM, e->s>>>(pa);
+    else
+      panel_w_kernel<1><<<grid, pw::THREADS, pw::SMEM, e->s>>>(pa);
+    CU(cudaGetLastError());
+    LLDArgs da;
+    da.D = e->D;
+    da.Wown = e->Wown;
+    da.own_mpad = e->own_mpad;
+    da.koff = kcols;
+    da.ldw = e->ldw;
+    da.row_slot = e->col_slot();
+    da.nt = nt;
+    da.n_tiles_1d = (nt + 63) / 64;
+    dim3 dg(da.n_tiles_1d * da.n_tiles_1d, Rl);
+    ll_dupdate_kernel<<<dg, 256, 0, e->s>>>(da);
+    CU(cudaGetLastError());
+    e->launches += 3;
+    // algorithmic: new column (2 R nt^2 t nt) + W_t (R nt nt^2) + D downdate (2 R nt^3)
+    flops = 2.0 * n_rows * nt * ((double)round * nt) + (double)n_rows * nt * nt +
+            2.0 * Rl * (double)nt * nt * nt;
+    e->update_flops += flops;
+  }
+  CU(cudaEventRecord(ev[4], e->s));
+  finish_row(e, row, s1, s2, g1, g2, bytes, flops, info);
+}
+
 void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   if (e->finished || (int)e->chosen.size() >= e->eff_budget)
     throw Fail{DSEL_E_STATE, "selection already finished"};
@@ -337,6 +516,13 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
 
   // ---- gains + local argmax ----
   CU(cudaEventRecord(ev[0], e->s));
+  if (e->ll && round == 0 && e->nloc > 0) {
+    const long long total = (long long)e->nloc * nt * nt;
+    ll_init_d_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 16), 256, 0, e->s>>>(
+        e->C, e->n, nt, e->nloc, e->G, e->rank, e->D);
+    CU(cudaGetLastError());
+    e->launches += 1;
+  }
   const int n_batch = e->n_cols_tab;
   run_gain(e, e->col_slot(), n_batch);
   GainTabs t = gain_tabs(e);
@@ -400,6 +586,10 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       CU(cudaMemcpyAsync(e->Lk, lsrc, sizeof(double) * nt * nt, cudaMemcpyDeviceToDevice, e->s));
     else
       Lk = lsrc;
+  }
+  if (e->ll) {
+    ll_tail(e, round, last, p, owner, q, Lk, ev, bytes, row, g1, g2, s1, s2, info);
+    return;
   }
   if (!last && !e->sym) {
     P = (owner == e->rank) ? e->C + (size_t)q * nt * e->n : e->Pbuf;
@@ -600,11 +790,11 @@ void destroy_impl(dsel_engine* e) {
   if (e->s) cudaStreamSynchronize(e->s);
   if (e->cs) cudaStreamSynchronize(e->cs);
   for (auto ev : e->ev) cudaEventDestroy(ev);
-  double* dptr[] = {e->C, e->K0, e->W, e->Wn, e->Wt, e->Wnt, e->Pbuf, e->Lk, e->Linv, e->Lscr, e->gains, e->hist,
+  double* dptr[] = {e->Wown, e->Wkn, e->D, e->cbuf, e->ldiag, e->C, e->K0, e->W, e->Wn, e->Wt, e->Wnt, e->Pbuf, e->Lk, e->Linv, e->Lscr, e->gains, e->hist,
                     e->kgain, e->stage, e->xbuf};
   for (double* d : dptr)
     if (d) cudaFree(d);
-  int* iptr[] = {e->status, e->kstatus, e->d_pos_sensor, e->d_slot_sensor, e->d_tab, e->d_sym};
+  int* iptr[] = {e->status, e->kstatus, e->d_pos_sensor, e->d_slot_sensor, e->d_tab, e->d_sym, e->d_iota};
   for (int* d : iptr)
     if (d) cudaFree(d);
   if (e->d_rec) cudaFree(e->d_rec);
@@ -640,7 +830,7 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     e->G = cfg->world_size;
     e->rank = cfg->rank;
     e->dev = cfg->device;
-    e->keep = cfg->keep_pristine != 0;
+    e->keep = cfg->keep_pristine != 0 && cfg->algorithm != 1;
     e->export_factor = cfg->export_factor != 0;
     e->tau = cfg->near_tie_tau > 0 ? cfg->near_tie_tau : 1e-9;
     // candidates (selector.hpp:142-151 check_candidates semantics)
@@ -690,14 +880,35 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     if (e->keep) e->K0 = dmalloc<double>(shard, tot);
     if (e->nt % 2) e->W = dmalloc<double>((size_t)e->n * e->ldw, tot);  // odd-nt update path
     e->mpad = round_up((int)e->n, ws::BR);
-    if (e->nt % 2 == 0) {
+    if (e->ll) {
+      // left-looking: no resident conditional covariance, no right-looking W
+    } else if (e->nt % 2 == 0) {
       e->Wt = dmalloc<double>((size_t)e->mpad * e->ldw, tot);
       e->Wnt = dmalloc<double>((size_t)e->mpad * e->ldw, tot);
     } else {
       e->Wn = dmalloc<double>((size_t)e->n * e->ldw, tot);
     }
-    e->sym = cfg->full_square == 0 && e->nt % 2 == 0;
-    if (e->G > 1 || e->sym) e->Pbuf = dmalloc<double>((size_t)e->n * e->nt, tot);
+    e->ll = cfg->algorithm == 1;
+    if (cfg->algorithm < 0 || cfg->algorithm > 1) throw Fail{DSEL_E_INVALID, "unknown algorithm"};
+    e->sym = cfg->full_square == 0 && e->nt % 2 == 0 && !e->ll;
+    if ((e->G > 1 || e->sym) && !e->ll) e->Pbuf = dmalloc<double>((size_t)e->n * e->nt, tot);
+    if (e->ll) {
+      const int B = std::max(e->eff_budget, 1);
+      e->own_mpad = round_up(std::max(e->nloc, 1) * e->nt, 128);
+      e->k_mpad = e->nt;
+      e->ldo = (long long)std::max(e->nloc, 1) * e->nt;
+      e->Wown = dmalloc<double>((size_t)e->own_mpad * B * e->ldw, tot);
+      e->Wkn = dmalloc<double>((size_t)e->k_mpad * B * e->ldw, tot);
+      e->D = dmalloc<double>((size_t)std::max(e->nloc, 1) * e->nt * e->nt, tot);
+      e->cbuf = dmalloc<double>((size_t)e->ldo * e->nt, tot);
+      e->ldiag = dmalloc<double>((size_t)B * e->nt * e->nt, tot);
+      e->d_iota = dmalloc<int>(std::max(e->nloc, 1), tot);
+      std::vector<int> iota(std::max(e->nloc, 1));
+      for (size_t i = 0; i < iota.size(); ++i) iota[i] = (int)i;
+      CU(cudaMemcpy(e->d_iota, iota.data(), sizeof(int) * iota.size(), cudaMemcpyHostToDevice));
+      CU(cudaMemsetAsync(e->Wown, 0, sizeof(double) * (size_t)e->own_mpad * B * e->ldw, e->s));
+      CU(cudaMemsetAsync(e->Wkn, 0, sizeof(double) * (size_t)e->k_mpad * B * e->ldw, e->s));
+    }
     {
       const size_t nct = (size_t)(e->nloc * e->nt + ws::BC - 1) / ws::BC + 2;
       const size_t nsym = nct + nct / ws_group + 4;
@@ -712,7 +923,7 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     e->kgain = dmalloc<double>(1, tot);
     e->kstatus = dmalloc<int>(1, tot);
     e->xbuf = dmalloc<double>((size_t)3 * (e->nloc + 1), tot);  // int tables, oversized
-    if (e->export_factor)
+    if (e->export_factor && !e->ll)
       e->hist = dmalloc<double>((size_t)std::max(e->nloc, 1) * std::max(e->eff_budget, 1) *
                                     e->nt * e->nt, tot);
     e->d_pos_sensor = dmalloc<int>(e->nc, tot);
@@ -1153,10 +1364,11 @@ int dsel_get_trace(dsel_engine* e, dsel_step_info* rows, int max_rows) {
 
 dsel_status dsel_reset(dsel_engine* e) {
   return guard(e, [&] {
-    if (!e->keep) throw Fail{DSEL_E_STATE, "dsel_reset requires keep_pristine"};
+    if (!e->keep && !e->ll) throw Fail{DSEL_E_STATE, "dsel_reset requires keep_pristine"};
     CU(cudaSetDevice(e->dev));
-    CU(cudaMemcpyAsync(e->C, e->K0, sizeof(double) * e->n * e->nloc * e->nt,
-                       cudaMemcpyDeviceToDevice, e->s));
+    if (!e->ll)  // the left-looking store is K itself and is never modified
+      CU(cudaMemcpyAsync(e->C, e->K0, sizeof(double) * e->n * e->nloc * e->nt,
+                         cudaMemcpyDeviceToDevice, e->s));
     e->alive.assign(e->nc, 1);
     e->n_alive = e->nc;
     e->chosen.clear();
@@ -1202,7 +1414,8 @@ dsel_status dsel_get_stats(dsel_engine* e, dsel_stats* st) {
 
 dsel_status dsel_export_factor(dsel_engine* e, double* host, int64_t ld) {
   return guard(e, [&] {
-    if (!e->export_factor) throw Fail{DSEL_E_STATE, "engine created without export_factor"};
+    if (!e->export_factor && !e->ll)
+      throw Fail{DSEL_E_STATE, "engine created without export_factor"};
     const int k = (int)e->chosen.size();
     const int nt = e->nt;
     if (ld < (int64_t)k * nt) throw Fail{DSEL_E_INVALID, "ld smaller than k*n_steps"};
@@ -1215,8 +1428,13 @@ dsel_status dsel_export_factor(dsel_engine* e, double* host, int64_t ld) {
       const int owner = p % e->G, q = p / e->G;
       const long long total = n2 * (i + 1);
       if (owner == e->rank) {
-        pack_factor_row_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 2048), 256, 0,
-                                 e->s>>>(e->hist + q * slot_stride, nt, i + 1, e->stage);
+        if (e->ll)
+          ll_pack_factor_row_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 2048), 256,
+                                      0, e->s>>>(e->Wown, e->own_mpad, q * nt, nt, e->ldw, i + 1,
+                                                 e->ldiag + (size_t)i * n2, e->stage);
+        else
+          pack_factor_row_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 2048), 256, 0,
+                                   e->s>>>(e->hist + q * slot_stride, nt, i + 1, e->stage);
         CU(cudaGetLastError());
       }
       if (e->G > 1) NC(ncclBroadcast(e->stage, e->stage, (size_t)total, ncclDouble, owner, e->comm, e->s));

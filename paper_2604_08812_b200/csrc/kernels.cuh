@@ -692,6 +692,11 @@ struct PanelArgs {
   double* hist;
   long long slot_stride, step_off;
   int G, rank;
+  // left-looking mode: append W_t into the tiled W_own at row
+  // out_slot[blk]*nt + (r - blk*nt) and k offset koff (null = unused)
+  double* Wown;
+  const int* out_slot;
+  int own_mpad, koff;
 };
 
 template <int VEC>
@@ -811,6 +816,11 @@ __global__ void __launch_bounds__(pw::THREADS, 2) panel_w_kernel(PanelArgs a) {
             if (c + 1 < nt) h[1] = v.y;
           }
         }
+        if (a.Wown) {
+          const int blk = r / nt;
+          const int orow = a.out_slot[blk] * nt + (r - blk * nt);
+          *reinterpret_cast<double2*>(a.Wown + wt_index(orow, a.koff + c, a.own_mpad)) = v;
+        }
         if (a.Wn)
           *reinterpret_cast<double2*>(a.Wn + (size_t)r * a.ldw + c) = make_double2(-v.x, -v.y);
         if (a.Wt) {
@@ -822,6 +832,228 @@ __global__ void __launch_bounds__(pw::THREADS, 2) panel_w_kernel(PanelArgs a) {
     }
   }
 }
+
+// ------------------------------------------------------------------------ //
+// Left-looking (W-resident) variant, SURVEY §8(f) row 1.                     //
+// Per round, for this rank's live candidates (rows of W_all it owns):        //
+//   c = K[own, k] - W_own[:, 0:t] W_k[0:t]^T        (ll_gemm_kernel, DMMA)    //
+//   W_t = c L_k^{-T}  appended to W_own             (panel_w_kernel)          //
+//   D_j -= W_t[j] W_t[j]^T  (gain inputs)           (ll_dupdate_kernel, DMMA) //
+// K[own_i, k] = K(k, own_i)^T is read from this rank's own K panels, so     //
+// only W_k (the chosen row block of W_all) crosses ranks.                   //
+// ------------------------------------------------------------------------ //
+namespace llg {
+constexpr int BM = 128, BN = 64, KC = 16, LDK = KC + 4, STAGES = 4, THREADS = 256;
+constexpr size_t SMEM = (size_t)STAGES * (BM + BN) * LDK * sizeof(double) + BM * sizeof(long long);
+}  // namespace llg
+
+struct LLGemmArgs {
+  const double* Wown;   // tiled (wt_index, mpad = own_mpad), rows = slot*nt + r
+  int own_mpad;
+  const double* Wkn;    // -W_k tiled, rows 0..nt-1, mpad = k_mpad
+  int k_mpad;
+  int n_k;              // k-chunks of 16 (t * ldw / 16)
+  const double* Kp;     // this rank's K panels, column-major, ld = ldk
+  long long ldk;
+  int pk;               // position of the chosen candidate
+  const int* row_slot;  // compact own live block h -> slot q
+  int nt, n_rows;       // n_rows = R_loc * nt
+  double* cout;         // c, column-major [c][row], ld = ldo
+  long long ldo;
+};
+
+__global__ void __launch_bounds__(llg::THREADS, 2) ll_gemm_kernel(LLGemmArgs a) {
+  using namespace llg;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sA = reinterpret_cast<double*>(smem_raw);  // [STAGES][BM][LDK]
+  double* sB = sA + STAGES * BM * LDK;                // [STAGES][BN][LDK]
+  long long* kbase = reinterpret_cast<long long*>(sB + STAGES * BN * LDK);  // [BM] K panel column
+  int* arow = reinterpret_cast<int*>(kbase);           // reused? no: separate below
+  (void)arow;
+  __shared__ int wrow[BM];
+  const int tid = threadIdx.x;
+  const int r0 = blockIdx.x * BM, c0 = blockIdx.y * BN;
+  const int nt = a.nt;
+  for (int i = tid; i < BM; i += THREADS) {
+    const int r = r0 + i;
+    if (r < a.n_rows) {
+      const int blk = r / nt, off = r - blk * nt;
+      const int q = a.row_slot[blk];
+      wrow[i] = q * nt + off;
+      kbase[i] = (long long)(q * nt + off) * a.ldk + (long long)a.pk * nt;
+    } else {
+      wrow[i] = -1;
+      kbase[i] = -1;
+    }
+  }
+  __syncthreads();
+  auto load_stage = [&](int stage, int kc) {
+    double* dA = sA + stage * BM * LDK;
+    double* dB = sB + stage * BN * LDK;
+    for (int idx = tid; idx < (BM + BN) * 8; idx += THREADS) {
+      const int row = idx >> 3, ch = idx & 7;
+      if (row < BM) {
+        const int w = wrow[row];
+        const bool ok = w >= 0;
+        // tiled source: 16 contiguous k per row per chunk, groups rotated by row
+        const int kk = ch * 2;
+        const double* src = a.Wown + wt_index(ok ? w : 0, kc + kk, a.own_mpad);
+        cp_async16(dA + row * LDK + kk, src, ok);
+      } else {
+        const int c = c0 + row - BM;
+        const bool ok = c < nt;
+        const int kk = ch * 2;
+        const double* src = a.Wkn + wt_index(ok ? c : 0, kc + kk, a.k_mpad);
+        cp_async16(dB + (row - BM) * LDK + kk, src, ok);
+      }
+    }
+  };
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+  double acc[4][4][2];
+  // accumulators <- K(own_i, k) = K panel column of own row, rows pk*nt + c
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const long long kb = kbase[wm + i * 8 + g];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = c0 + wn + j * 8 + 2 * t;
+      acc[i][j][0] = acc[i][j][1] = 0.0;
+      if (kb >= 0 && c < nt) {
+        const double* src = a.Kp + kb + c;
+        acc[i][j][0] = src[0];
+        if (c + 1 < nt) acc[i][j][1] = src[1];
+      }
+    }
+  }
+#pragma unroll
+  for (int s0 = 0; s0 < STAGES - 1; ++s0) {
+    if (s0 < a.n_k) load_stage(s0, s0 * KC);
+    cp_async_commit();
+  }
+  for (int kb = 0; kb < a.n_k; ++kb) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kb + STAGES - 1;
+      if (nk < a.n_k) load_stage(nk % STAGES, nk * KC);
+      cp_async_commit();
+    }
+    const double* tA = sA + (kb % STAGES) * BM * LDK;
+    const double* tB = sB + (kb % STAGES) * BN * LDK;
+#pragma unroll
+    for (int k4 = 0; k4 < KC / 4; ++k4) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) fa[i] = tA[(wm + i * 8 + g) * LDK + k4 * 4 + t];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) fb[j] = tB[(wn + j * 8 + g) * LDK + k4 * 4 + t];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j], fa[i], fb[j]);
+    }
+  }
+  cp_async_wait<0>();
+  // c column-major: rows r, columns c, c+1
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = r0 + wm + i * 8 + g;
+    if (r >= a.n_rows) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = c0 + wn + j * 8 + 2 * t;
+      if (c < nt) a.cout[(size_t)c * a.ldo + r] = acc[i][j][0];
+      if (c + 1 < nt) a.cout[(size_t)(c + 1) * a.ldo + r] = acc[i][j][1];
+    }
+  }
+}
+
+// D_h -= W_t[h] W_t[h]^T for every own live block h (lower 64x64 tiles of the
+// nt x nt block), W_t read from the tiled W_own at k offset koff.
+struct LLDArgs {
+  double* D;            // [slot][nt x nt] column-major
+  const double* Wown;
+  int own_mpad, koff, ldw;
+  const int* row_slot;  // compact own live block -> slot
+  int nt, n_tiles_1d;   // tiles per block dimension (ceil(nt/64))
+};
+
+__global__ void __launch_bounds__(256) ll_dupdate_kernel(LLDArgs a) {
+  constexpr int T = 64, KC = 16, LDK = KC + 4;
+  __shared__ __align__(16) double sA[T][LDK], sB[T][LDK];
+  const int h = blockIdx.y;
+  const int tt = blockIdx.x;
+  const int nti = a.n_tiles_1d;
+  const int ti = tt / nti, tj = tt - ti * nti;
+  if (tj > ti) return;  // lower tiles only
+  const int nt = a.nt, q = a.row_slot[h];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp & 3) * 16, wn = (warp >> 2) * 32;  // 8 warps: 4 x 2, warp tile 16 x 32
+  double acc[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int k0 = 0; k0 < a.ldw; k0 += KC) {
+    for (int idx = tid; idx < 2 * T * (KC / 2); idx += 256) {
+      const int which = idx / (T * (KC / 2));
+      const int rem = idx - which * T * (KC / 2);
+      const int row = rem / (KC / 2), ch = rem - row * (KC / 2);
+      const int rr = (which ? tj : ti) * T + row;
+      const bool ok = rr < nt;
+      const double* src = a.Wown + wt_index(q * nt + (ok ? rr : 0), a.koff + k0 + 2 * ch, a.own_mpad);
+      double2 v = ok ? *reinterpret_cast<const double2*>(src) : make_double2(0.0, 0.0);
+      double* dst = which ? &sB[row][2 * ch] : &sA[row][2 * ch];
+      dst[0] = v.x;
+      dst[1] = v.y;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k4 = 0; k4 < KC / 4; ++k4) {
+      double fa[2], fb[4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) fa[i] = sA[wm + i * 8 + g][k4 * 4 + t];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) fb[j] = sB[wn + j * 8 + g][k4 * 4 + t];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j], fa[i], fb[j]);
+    }
+    __syncthreads();
+  }
+  double* D = a.D + (size_t)q * nt * nt;  // column-major: (row, col) at col*nt + row
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int r = ti * T + wm + i * 8 + g;
+    if (r >= nt) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = tj * T + wn + j * 8 + 2 * t;
+      if (c < nt) D[(size_t)c * nt + r] -= acc[i][j][0];
+      if (c + 1 < nt) D[(size_t)(c + 1) * nt + r] -= acc[i][j][1];
+    }
+  }
+}
+
+// Owner: -W_k (rows slot_k*nt.., k chunks [0, n_k)) from W_own into the
+// broadcast buffer (tiled, rows 0..nt-1, mpad = k_mpad); L_k copied by caller.
+__global__ void ll_extract_wk_kernel(const double* Wown, int own_mpad, int row0, int nt, int kcols,
+                                     double* Wkn, int k_mpad) {
+  const long long total = (long long)nt * kcols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / kcols), k = (int)(e - (long long)r * kcols);
+    Wkn[wt_index(r, k, k_mpad)] = -Wown[wt_index(row0 + r, k, own_mpad)];
+  }
+}
+
+// Gain-kernel input for the left-looking mode: D blocks live in their own
+// buffer; the chol kernel reads them through (src_col, src_row) = (slot*nt, 0)
+// with lds = nt (column-major nt x nt per slot, slots side by side).
 
 // ------------------------------------------------------------------------ //
 // Gain kernel: batched nt x nt Cholesky + log-determinant (north-star (3)). //

@@ -108,7 +108,8 @@ class Engine:
     def __init__(self, n_sensors: int, n_steps: int, budget: int, candidates=None, device: int = 0,
                  world_size: int = 1, rank: int = 0, nccl_id: bytes | None = None,
                  keep_pristine: bool = False, export_factor: bool = False,
-                 near_tie_tau: float = 1e-9, storage: int = 0, full_square: bool = False):
+                 near_tie_tau: float = 1e-9, storage: int = 0, full_square: bool = False,
+                 algorithm: str = "right"):
         cfg = DselConfig()
         cfg.n_sensors, cfg.n_steps, cfg.budget = n_sensors, n_steps, budget
         self._cands = None
@@ -126,6 +127,9 @@ class Engine:
         cfg.export_factor = int(export_factor)
         cfg.near_tie_tau = near_tie_tau
         cfg.full_square = int(full_square)
+        if algorithm not in ("right", "left"):
+            raise InvalidConfig(1, "algorithm must be 'right' or 'left'")
+        cfg.algorithm = 1 if algorithm == "left" else 0
         h = C.c_void_p()
         _check(lib.dsel_create(C.byref(cfg), C.byref(h)), None)
         self.h = h

@@ -281,3 +281,47 @@ def test_c3mini_nt420_against_reference_golden(dsel, golden_dir):
             info = eng.step()
             assert info["chosen_index"] == s
             assert gain_close(info["gain"], g["gains"][rnd])
+
+
+# ---- left-looking W-resident variant ------------------ #
+@pytest.mark.parametrize("case", ["c1", "wave", "c3mini"])
+def test_left_looking_matches_reference(dsel, O, golden_dir, case):
+    g = json.load(open(os.path.join(golden_dir, f"{case}.json")))
+    if case == "wave":
+        k, nd, nt = O.read_kbf(os.path.join(golden_dir, "wave.kbf"))
+        eng = dsel.Engine(nd, nt, 12, algorithm="left")
+        eng.load_k(k)
+    else:
+        nd, nt, rk = g["n_sensors"], g["n_steps"], g["rank"]
+        eng = dsel.Engine(nd, nt, g["budget"], algorithm="left")
+        eng.gen_synthetic(dsel.synthetic_v(nd, nt, rk, g["seed"]), rk, g["sigma"])
+    with eng:
+        eng.run()
+        rows = eng.trace()
+        L = eng.export_factor(len(rows))
+    assert_trace_matches(rows, g["chosen"], g["gains"], g["objectives"])
+    if case == "wave":
+        dense = O.blocks_to_dense(k, nd, nt)
+        idx = np.concatenate([np.arange(s * nt, (s + 1) * nt) for s in g["chosen"]])
+        np.testing.assert_allclose(L @ L.T, dense[np.ix_(idx, idx)], rtol=1e-9, atol=1e-9)
+
+
+def test_left_looking_random_and_subsets(dsel, O, golden_dir):
+    cases = json.load(open(os.path.join(golden_dir, "random.json")))["cases"]
+    for c in cases:
+        nd, nt = c["n_sensors"], c["n_steps"]
+        k = O.random_hessian(nd, nt, c["gamma"], c["rank"], c["seed"])
+        eng = dsel.Engine(nd, nt, c["budget"], algorithm="left")
+        eng.load_k(k)
+        eng.run()
+        rows = eng.trace()
+        eng.close()
+        assert_trace_matches(rows, c["chosen"], c["gains"], c["objectives"])
+    nd, nt = 14, 6
+    k = O.random_hessian(nd, nt, 0.9, 60, 77)
+    cands = [0, 2, 3, 5, 7, 8, 11, 13]
+    want = O.greedy_select(k, nd, nt, 6, candidates=cands)
+    with dsel.Engine(nd, nt, 6, candidates=cands, algorithm="left") as eng:
+        eng.load_k(k)
+        eng.run()
+        assert_trace_matches(eng.trace(), want.chosen, want.gains, want.objectives)
