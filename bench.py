@@ -45,6 +45,19 @@ FP64_DMMA_PEAK_TFLOPS = 37.10
 FP64_CUBLAS_TFLOPS = 36.13
 
 
+ALGO_DESC = {
+    "right": "right-looking Schur update of the resident conditional covariance "
+             "(north star; block-lower symmetric storage)",
+    "left": "left-looking W-resident variant (SURVEY 8f row 1): K pristine, "
+            "c = K[:,k] - W W_k^T per round",
+}
+FLOP_MODEL = {
+    "right": "block-lower right-looking: sum_t 2*Nt^3*sum_{local live blocks h}(R_t - g_h) "
+             "(= Nt*n_t*(n_t+Nt) over all ranks)",
+    "left": "left-looking: sum_t [2*n_loc,t*Nt*(t*Nt) + n_loc,t*Nt^2 + 2*R_loc,t*Nt^3]",
+}
+
+
 def workload(name: str, n_gpus: int) -> dict:
     w = dict(CONFIGS[name])
     if name == "c3":
@@ -125,6 +138,17 @@ def barrier(world):
         dist.barrier()
 
 
+def allreduce_sum(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def allreduce_max(x: float, world: int) -> float:
     if world == 1:
         return x
@@ -160,63 +184,56 @@ def ncu_traffic(profile_dir: str):
 
 
 # ------------------------------------------------------------------------- #
-def our_arm(args, world, rank, local):
+def measure(d, args, world, rank, local, w, v, nid, algorithm, clock=True, want_k=False):
+    """One engine, one algorithm: device-timed time-to-k over K steps, then the
+    e2e (host K -> H2D -> select -> D2H) measurement. Returns a dict."""
     import numpy as np
 
-    import paper_2604_08812_b200 as d
-
-    w = workload(args.config, world)
     nd, nt, vrank, budget = w["nd"], w["nt"], w["rank"], w["budget"]
-    t0 = time.time()
-    v = d.synthetic_v(nd, nt, vrank, SEED, threads=max(1, (os.cpu_count() or 1) // world))
-    t_v = time.time() - t0
-    nid = broadcast_bytes(d.nccl_unique_id() if (world > 1 and rank == 0) else None, world)
     eng = d.Engine(nd, nt, budget, device=local, world_size=world, rank=rank, nccl_id=nid,
-                   keep_pristine=True, export_factor=True)
+                   keep_pristine=True, export_factor=True, algorithm=algorithm)
     t0 = time.time()
     eng.gen_synthetic(v, vrank, SIGMA)
     t_gen = time.time() - t0
-    del v
-
-    # ---- device-resident timing: K steps of a full selection ----
     times, upd_ms, upd_fl, launches, chosen = [], [], [], [], None
-    with ClockSampler(local) as clk:
-        for it in range(args.warmup + args.steps):
-            eng.reset()
-            barrier(world)
-            eng.run()
-            st = eng.stats()
-            t = allreduce_max(st["time_to_k_ms"] / 1e3, world)
-            if it >= args.warmup:
-                times.append(t)
-                upd_ms.append(st["update_ms"])
-                upd_fl.append(st["update_flops"])
-                launches.append(st["kernel_launches"])
-            rows = eng.trace()
-            chosen = [r["chosen_index"] for r in rows]
-    clocks = clk.summary()
-    value = sum(times) / len(times)
-    # dominant kernel: the rank-Nt Schur update (per-rank flops / per-rank kernel time)
+    clk = ClockSampler(local) if clock else None
+    if clk:
+        clk.__enter__()
+    for it in range(args.warmup + args.steps):
+        eng.reset()
+        barrier(world)
+        eng.run()
+        st = eng.stats()
+        t = allreduce_max(st["time_to_k_ms"] / 1e3, world)
+        if it >= args.warmup:
+            times.append(t)
+            upd_ms.append(st["update_ms"])
+            upd_fl.append(st["update_flops"])
+            launches.append(st["kernel_launches"])
+        chosen = [r["chosen_index"] for r in eng.trace()]
+    if clk:
+        clk.__exit__()
+    out = {"value": sum(times) / len(times), "chosen": chosen, "t_gen": t_gen,
+           "launches": int(sum(launches) / len(launches)),
+           "clocks": clk.summary() if clk else None}
     upd_t = sum(upd_ms) / 1e3
-    upd_tf = sum(upd_fl) / upd_t / 1e12 if upd_t > 0 else 0.0
-    upd_tf_all = allreduce_max(upd_tf, world)  # report the slowest-rank view below
-    tot_flops = sum(upd_fl) / len(upd_fl)
-    tot_flops_all = tot_flops * world  # every rank updates its own shard
-    e2e_tf = tot_flops_all / value / 1e12
-
-    # ---- e2e through the public API with host buffers ----
-    e2e = None
-    if not args.no_e2e:
+    out["upd_tf"] = sum(upd_fl) / upd_t / 1e12 if upd_t > 0 else 0.0
+    out["upd_tf_max"] = allreduce_max(out["upd_tf"], world)
+    out["flops_rank"] = sum(upd_fl) / len(upd_fl)
+    out["flops_all"] = allreduce_sum(out["flops_rank"], world)
+    out["e2e"] = None
+    hv = None
+    if not args.no_e2e or want_k:
         import torch
 
-        mine = [j for p, j in enumerate(range(nd)) if p % world == rank]
+        mine = [j for j in range(nd) if j % world == rank]
         row_elems = nd * nt * nt
-        host = torch.empty(nd * row_elems, dtype=torch.float64).pin_memory() if world == 1 else \
-            torch.empty(nd * row_elems, dtype=torch.float64).pin_memory()
+        host = torch.empty(nd * row_elems, dtype=torch.float64).pin_memory()
         eng.reset()
         hv = host.numpy()
         for j in mine:
             hv[j * row_elems:(j + 1) * row_elems] = eng.read_block_row(j)
+    if not args.no_e2e:
         e2e_times, h2d, d2h = [], 0, 0
         for it in range(max(1, args.warmup // 2) + args.steps):
             eng.reset()
@@ -233,21 +250,40 @@ def our_arm(args, world, rank, local):
                 h2d = st["h2d_bytes"]
                 d2h = st["d2h_bytes"] + res.size * 8
             assert [int(x) for x in res[:, 0]] == chosen
-        e2e = {"value": sum(e2e_times) / len(e2e_times), "unit": "s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
-        cpu_k = hv if (rank == 0 and world == 1) else None
-    else:
-        cpu_k = None
-
-    # ---- CPU baseline: the reference on a bounded sample (rank 0, N=1) ----
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        if cpu_k is None:
-            import numpy as np2
-
-            cpu_k = np2.concatenate([eng.read_block_row(j) for j in range(nd)])
-        cpu = cpu_reference(cpu_k, nd, nt, budget, chosen)
+        out["e2e"] = {"value": sum(e2e_times) / len(e2e_times), "unit": "s",
+                      "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+    out["host_k"] = hv if want_k else None
     eng.close()
+    return out
+
+
+def our_arm(args, world, rank, local):
+    import paper_2604_08812_b200 as d
+
+    w = workload(args.config, world)
+    nd, nt, vrank, budget = w["nd"], w["nt"], w["rank"], w["budget"]
+    t0 = time.time()
+    v = d.synthetic_v(nd, nt, vrank, SEED, threads=max(1, (os.cpu_count() or 1) // world))
+    t_v = time.time() - t0
+    nid = broadcast_bytes(d.nccl_unique_id() if (world > 1 and rank == 0) else None, world)
+    want_cpu = rank == 0 and world == 1 and not args.no_cpu
+    prim = measure(d, args, world, rank, local, w, v, nid, args.algorithm, want_k=want_cpu)
+    other = None
+    if not args.no_variants:
+        alt = "left" if args.algorithm == "right" else "right"
+        nid2 = broadcast_bytes(d.nccl_unique_id() if (world > 1 and rank == 0) else None, world)
+        other = measure(d, args, world, rank, local, w, v, nid2, alt, clock=False)
+        if other["chosen"] != prim["chosen"]:
+            raise RuntimeError("right- and left-looking sequences differ")
+    del v
+    value, chosen, clocks = prim["value"], prim["chosen"], prim["clocks"]
+    upd_tf, upd_tf_all = prim["upd_tf"], prim["upd_tf_max"]
+    tot_flops, tot_flops_all = prim["flops_rank"], prim["flops_all"]
+    e2e_tf = tot_flops_all / value / 1e12
+    e2e, t_gen, launches = prim["e2e"], prim["t_gen"], [prim["launches"]]
+    cpu = None
+    if want_cpu:
+        cpu = cpu_reference(prim["host_k"], nd, nt, budget, chosen)
 
     tr = ncu_traffic(os.path.join(ROOT, "profiles"))
     traffic = tr.get("traffic_bytes_per_launch") if tr else None
@@ -271,16 +307,17 @@ def our_arm(args, world, rank, local):
                                f"seed {SEED}, K resident in HBM",
                    "n_sensors": nd, "n_steps": nt, "budget": budget, "rank": vrank,
                    "parallelism": f"candidate-sharded x{world} (cyclic block columns), "
-                                  "NCCL allgather(argmax) + broadcast(panel)",
+                                  "NCCL allgather(argmax) + all-reduce/broadcast(panel)",
                    "l2": f"inputs {nd * nt * nd * nt * 8 / 1e9:.2f} GB >> 126 MB L2 (no flush needed)",
                    "chosen_first": chosen[:8]},
+        "algorithm": ALGO_DESC[args.algorithm],
         "schur_update": {"flops_per_step_per_rank": tot_flops,
                          "flops_per_step_all_ranks": tot_flops_all,
                          "kernel_tflops_per_gpu": round(upd_tf, 3),
                          "kernel_tflops_per_gpu_max_rank": round(upd_tf_all, 3),
                          "end_to_end_tflops_all_gpus": round(e2e_tf, 3),
                          "frac_of_fp64_peak_per_gpu": round(upd_tf / peak, 4),
-                         "flop_model": "full-square right-looking: sum_t 2*Nt*(R_t*Nt)*(R_loc,t*Nt)"},
+                         "flop_model": FLOP_MODEL[args.algorithm]},
         "roofline": {"bound": "tensor", "kernel": "schur_update_ws_kernel (DMMA.8x8x4, TMA bulk)",
                      "achieved": round(upd_tf, 3), "peak": peak, "unit": "TFLOP/s",
                      "frac": round(upd_tf / peak, 4),
@@ -297,6 +334,15 @@ def our_arm(args, world, rank, local):
         "clocks": clocks,
         "setup": {"v_host_s": round(t_v, 2), "k_gen_device_s": round(t_gen, 2)},
     }
+    if other is not None:
+        alt = "left" if args.algorithm == "right" else "right"
+        line["variant"] = {
+            "algorithm": ALGO_DESC[alt], "value": round(other["value"], 6), "unit": "s",
+            "e2e": other["e2e"], "same_sequence": True,
+            "update_tflops_per_gpu": round(other["upd_tf"], 3),
+            "frac_of_fp64_peak_per_gpu": round(other["upd_tf"] / peak, 4),
+            "flops_per_step_all_ranks": other["flops_all"], "flop_model": FLOP_MODEL[alt],
+            "gpu_launches": other["launches"]}
     if cpu is not None:
         line["cpu_baseline"] = cpu
     if rank == 0:
@@ -394,6 +440,10 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--algorithm", default="right", choices=["right", "left"],
+                    help="primary line (right = north-star Schur update)")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip measuring the other algorithm beside the primary")
     args = ap.parse_args()
     world, rank, local = dist_init()
     if args.impl == "reference":

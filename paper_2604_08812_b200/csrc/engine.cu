@@ -86,7 +86,8 @@ struct dsel_engine {
   int n_sms = 148;
   int mpad = 0;  // rows of the tiled W buffers
   bool ll = false;  // left-looking W-resident algorithm
-  double *Wown = nullptr, *Wkn = nullptr, *D = nullptr, *cbuf = nullptr, *ldiag = nullptr;
+  double *Wown = nullptr, *Wkn = nullptr, *D = nullptr, *cbuf = nullptr, *ldiag = nullptr,
+         *cpart = nullptr;
   int* d_iota = nullptr;
   int own_mpad = 0, k_mpad = 0;
   long long ldo = 0;
@@ -297,7 +298,7 @@ void run_gain(dsel_engine* e, const int* slots, int n_batch) {
       slots, n_batch, e->G, e->rank, e->nt, e->d_pos_sensor, t.src_col, t.src_row, t.sensor,
       e->ll ? 1 : 0);
   CU(cudaGetLastError());
-  CholArgs a;
+  CholArgs a{};
   a.src = e->ll ? e->D : e->C;
   a.lds = e->ll ? (long long)e->nt : e->n;
   a.src_col = t.src_col;
@@ -366,6 +367,10 @@ void sym_tables(dsel_engine* e) {
   CU(cudaMemcpyAsync(e->d_sym, e->h_sym, sizeof(int) * (size_t)(nct + ng + 1),
                      cudaMemcpyHostToDevice, e->s));
 }
+
+// left-looking split-K: one split per 64 k-chunks (1024 k), at most 8 splits;
+// depends only on the round, never on the rank count
+constexpr int kLLSplitChunks = 64, kLLMaxSplits = 8;
 
 void finish_row(dsel_engine* e, dsel_step_info& row, int s1, int s2, double g1, double g2,
                 uint64_t bytes, double flops, dsel_step_info* info) {
@@ -459,9 +464,21 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
     ga.n_rows = n_rows;
     ga.cout = e->cbuf;
     ga.ldo = e->ldo;
-    dim3 gg((n_rows + llg::BM - 1) / llg::BM, (nt + llg::BN - 1) / llg::BN);
+    ga.kc_split = kLLSplitChunks;
+    ga.n_splits = std::max(1, std::min(kLLMaxSplits, (ga.n_k + kLLSplitChunks - 1) / kLLSplitChunks));
+    ga.kc_split = std::max(ga.kc_split, (ga.n_k + ga.n_splits - 1) / ga.n_splits);
+    ga.part = e->cpart;
+    ga.part_stride = e->ldo * nt;
+    dim3 gg((n_rows + llg::BM - 1) / llg::BM, (nt + llg::BN - 1) / llg::BN, ga.n_splits);
     ll_gemm_kernel<<<gg, llg::THREADS, llg::SMEM, e->s>>>(ga);
     CU(cudaGetLastError());
+    if (ga.n_splits > 1) {
+      const long long total = (long long)nt * n_rows;
+      ll_reduce_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 8), 256, 0, e->s>>>(
+          e->cpart, ga.part_stride, ga.n_splits, nt, n_rows, e->ldo, e->cbuf);
+      CU(cudaGetLastError());
+      e->launches += 1;
+    }
     PanelArgs pa{};
     pa.P = e->cbuf;
     pa.ldp = e->ldo;
@@ -651,7 +668,7 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
     CU(cudaGetLastError());
     e->launches += 1;
     if (R > 0) {
-      PanelArgs pa;
+      PanelArgs pa{};
       pa.P = P;
       pa.ldp = e->n;
       pa.Linv = e->Linv;
@@ -693,7 +710,7 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   if (!last && R > 0 && Rl > 0) {
     const int n_rows = R * nt, n_cols = Rl * nt;
     if (nt % 2 == 0) {
-      UpdateWSArgs ua;
+      UpdateWSArgs ua{};
       ua.C = e->C;
       ua.ldc = e->n;
       ua.Wt = e->Wt;
@@ -717,7 +734,7 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       const int grid = (int)std::min<long long>(e->n_sms, ua.n_tiles);
       schur_update_ws_kernel<<<grid, ws::THREADS, ws::SMEM, e->s>>>(ua);
     } else {
-      UpdateArgs ua;
+      UpdateArgs ua{};
       ua.C = e->C;
       ua.ldc = e->n;
       ua.W = e->W;
@@ -790,7 +807,7 @@ void destroy_impl(dsel_engine* e) {
   if (e->s) cudaStreamSynchronize(e->s);
   if (e->cs) cudaStreamSynchronize(e->cs);
   for (auto ev : e->ev) cudaEventDestroy(ev);
-  double* dptr[] = {e->Wown, e->Wkn, e->D, e->cbuf, e->ldiag, e->C, e->K0, e->W, e->Wn, e->Wt, e->Wnt, e->Pbuf, e->Lk, e->Linv, e->Lscr, e->gains, e->hist,
+  double* dptr[] = {e->cpart, e->Wown, e->Wkn, e->D, e->cbuf, e->ldiag, e->C, e->K0, e->W, e->Wn, e->Wt, e->Wnt, e->Pbuf, e->Lk, e->Linv, e->Lscr, e->gains, e->hist,
                     e->kgain, e->stage, e->xbuf};
   for (double* d : dptr)
     if (d) cudaFree(d);
@@ -901,6 +918,11 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
       e->Wkn = dmalloc<double>((size_t)e->k_mpad * B * e->ldw, tot);
       e->D = dmalloc<double>((size_t)std::max(e->nloc, 1) * e->nt * e->nt, tot);
       e->cbuf = dmalloc<double>((size_t)e->ldo * e->nt, tot);
+      {
+        const int max_nk = (B * e->ldw) / 16;
+        const int ns = std::max(1, std::min(kLLMaxSplits, (max_nk + kLLSplitChunks - 1) / kLLSplitChunks));
+        if (ns > 1) e->cpart = dmalloc<double>((size_t)ns * e->ldo * e->nt, tot);
+      }
       e->ldiag = dmalloc<double>((size_t)B * e->nt * e->nt, tot);
       e->d_iota = dmalloc<int>(std::max(e->nloc, 1), tot);
       std::vector<int> iota(std::max(e->nloc, 1));
@@ -1270,7 +1292,7 @@ dsel_status dsel_gen_synthetic(dsel_engine* e, const double* v_host, int rank, d
     double* V = dmalloc<double>(vel, dummy);
     cudaError_t ce = cudaMemcpy(V, v_host, vel * sizeof(double), cudaMemcpyHostToDevice);
     if (ce == cudaSuccess && e->nloc > 0) {
-      GenArgs g;
+      GenArgs g{};
       g.V = V;
       g.rank = rank;
       g.noise2 = sigma * sigma;  // kaccess.hpp:88

@@ -860,6 +860,14 @@ struct LLGemmArgs {
   int nt, n_rows;       // n_rows = R_loc * nt
   double* cout;         // c, column-major [c][row], ld = ldo
   long long ldo;
+  // split-K (grid.z splits of kc_split chunks; split 0 carries the K init):
+  // with n_splits > 1 every split writes its partial to part + z*part_stride
+  // and ll_reduce_kernel sums them in split order (deterministic; the split
+  // count depends only on the round, so results are identical for any rank
+  // count)
+  int kc_split, n_splits;
+  double* part;
+  long long part_stride;
 };
 
 __global__ void __launch_bounds__(llg::THREADS, 2) ll_gemm_kernel(LLGemmArgs a) {
@@ -912,6 +920,10 @@ __global__ void __launch_bounds__(llg::THREADS, 2) ll_gemm_kernel(LLGemmArgs a) 
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
   double acc[4][4][2];
+  const int z = blockIdx.z;
+  const int kb0 = z * a.kc_split;
+  const int kb1 = min(a.n_k, kb0 + a.kc_split);
+  const int n_kl = max(0, kb1 - kb0);
   // accumulators <- K(own_i, k) = K panel column of own row, rows pk*nt + c
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -920,7 +932,7 @@ __global__ void __launch_bounds__(llg::THREADS, 2) ll_gemm_kernel(LLGemmArgs a) 
     for (int j = 0; j < 4; ++j) {
       const int c = c0 + wn + j * 8 + 2 * t;
       acc[i][j][0] = acc[i][j][1] = 0.0;
-      if (kb >= 0 && c < nt) {
+      if (z == 0 && kb >= 0 && c < nt) {
         const double* src = a.Kp + kb + c;
         acc[i][j][0] = src[0];
         if (c + 1 < nt) acc[i][j][1] = src[1];
@@ -929,15 +941,15 @@ __global__ void __launch_bounds__(llg::THREADS, 2) ll_gemm_kernel(LLGemmArgs a) 
   }
 #pragma unroll
   for (int s0 = 0; s0 < STAGES - 1; ++s0) {
-    if (s0 < a.n_k) load_stage(s0, s0 * KC);
+    if (s0 < n_kl) load_stage(s0, (kb0 + s0) * KC);
     cp_async_commit();
   }
-  for (int kb = 0; kb < a.n_k; ++kb) {
+  for (int kb = 0; kb < n_kl; ++kb) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     {
       const int nk = kb + STAGES - 1;
-      if (nk < a.n_k) load_stage(nk % STAGES, nk * KC);
+      if (nk < n_kl) load_stage(nk % STAGES, (kb0 + nk) * KC);
       cp_async_commit();
     }
     const double* tA = sA + (kb % STAGES) * BM * LDK;
@@ -956,7 +968,8 @@ __global__ void __launch_bounds__(llg::THREADS, 2) ll_gemm_kernel(LLGemmArgs a) 
     }
   }
   cp_async_wait<0>();
-  // c column-major: rows r, columns c, c+1
+  // c column-major: rows r, columns c, c+1 (or this split's partial)
+  double* out = a.n_splits > 1 ? a.part + (size_t)z * a.part_stride : a.cout;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int r = r0 + wm + i * 8 + g;
@@ -964,9 +977,23 @@ __global__ void __launch_bounds__(llg::THREADS, 2) ll_gemm_kernel(LLGemmArgs a) 
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int c = c0 + wn + j * 8 + 2 * t;
-      if (c < nt) a.cout[(size_t)c * a.ldo + r] = acc[i][j][0];
-      if (c + 1 < nt) a.cout[(size_t)(c + 1) * a.ldo + r] = acc[i][j][1];
+      if (c < nt) out[(size_t)c * a.ldo + r] = acc[i][j][0];
+      if (c + 1 < nt) out[(size_t)(c + 1) * a.ldo + r] = acc[i][j][1];
     }
+  }
+}
+
+// c = sum of the split partials, in split order
+__global__ void ll_reduce_kernel(const double* part, long long part_stride, int n_splits, int nt,
+                                 int n_rows, long long ldo, double* cout) {
+  const long long total = (long long)nt * n_rows;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e / n_rows), r = (int)(e - (long long)c * n_rows);
+    const size_t o = (size_t)c * ldo + r;
+    double v = part[o];
+    for (int z = 1; z < n_splits; ++z) v += part[(size_t)z * part_stride + o];
+    cout[o] = v;
   }
 }
 
