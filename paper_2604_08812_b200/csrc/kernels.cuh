@@ -416,6 +416,7 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
   uint64_t* tfull = bars + 2 * STAGES;    // [2]       maps + C tile landed (per map buffer)
   uint64_t* mempty = bars + 2 * STAGES + 2;  // [2]    consumers finished the tile's epilogue
   uint64_t* cempty = bars + 2 * STAGES + 4;  // [1]    consumers copied the C tile to registers
+  __shared__ int s_tflag[2];  // per map buffer: 1 = a tile is ready, 0 = no more tiles
   auto colbase_of = [&](int b) {
     return reinterpret_cast<long long*>(smem_raw + OFF_MAPS + b * MAPS_BYTES);
   };
@@ -467,6 +468,7 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
       const int ncv = min(BC, a.n_cols - c0);  // valid columns
       const int b = it & 1;
       if (it >= 2) mbar_wait(&mempty[b], ((it >> 1) - 1) & 1);
+      if (lane == 0) s_tflag[b] = 1;
       long long* colbase = colbase_of(b);
       int* rowphys = rowphys_of(b);
       int rp[BR / 32];
@@ -575,6 +577,15 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
       }
       ++it;
     }
+    // end of the tile stream: release the consumers with an empty tile
+    {
+      const int b = it & 1;
+      if (it >= 2) mbar_wait(&mempty[b], ((it >> 1) - 1) & 1);
+      if (lane == 0) {
+        s_tflag[b] = 0;
+        mbar_arrive(&tfull[b]);
+      }
+    }
     return;
   }
 
@@ -585,13 +596,10 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
   int stage = 0;
   unsigned fphase = 0;
   int it = 0;
-  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    {
-      int r0_, c0_;
-      if (!ws_tile(a, fr, gp, tile, r0_, c0_)) continue;
-    }
+  for (;;) {
     const int b = it & 1;
     mbar_wait(&tfull[b], (it >> 1) & 1);
+    if (!s_tflag[b]) break;  // the producer has no more tiles for this CTA
     double acc[4][4][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
