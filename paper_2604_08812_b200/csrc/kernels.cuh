@@ -1125,18 +1125,29 @@ __device__ __forceinline__ double fast_rsqrt(double p) {
 
 // Register-resident, compile-time-unrolled pieces of the panel factorization
 // (template recursion guarantees constant indices, so r[]/s[] stay in registers).
+// lane l owns row l of the (identity-padded) NB x NB diagonal block
+// One pivot of the warp-level diagonal-block factorization. Lane l owns row l
+// of the block in registers; column J is published through shared memory
+// (one store per lane, broadcast loads) and the trailing update runs on every
+// lane without predication (entries above the diagonal are scratch, never
+// stored), so each pivot costs ~2 shuffles + ~NB/2 paired loads + NB FMAs.
 template <int J, int C, int NB>
-__device__ __forceinline__ void diag_upd(double (&r)[NB], int lane) {
+__device__ __forceinline__ void diag_upd_s(double (&r)[NB], const double* col) {
   if constexpr (C < NB) {
-    const double lcj = __shfl_sync(0xffffffffu, r[J], C);
-    if (lane >= C) r[C] -= r[J] * lcj;
-    diag_upd<J, C + 1, NB>(r, lane);
+    if constexpr (C + 1 < NB && (C % 2) == 0) {
+      const double2 v = *reinterpret_cast<const double2*>(col + C);
+      r[C] -= r[J] * v.x;
+      r[C + 1] -= r[J] * v.y;
+      diag_upd_s<J, C + 2, NB>(r, col);
+    } else {
+      r[C] -= r[J] * col[C];
+      diag_upd_s<J, C + 1, NB>(r, col);
+    }
   }
 }
-// lane l owns row l of the (identity-padded) NB x NB diagonal block
 template <int J, int NB>
 __device__ __forceinline__ void diag_step(double (&r)[NB], int lane, int nb, double* dv, double* rdv,
-                                          int& fail) {
+                                          int& fail, double* colbuf) {
   if constexpr (J < NB) {
     const double piv = __shfl_sync(0xffffffffu, r[J], J);
     const bool bad = !(piv > 0.0) || !isfinite(piv);
@@ -1144,14 +1155,16 @@ __device__ __forceinline__ void diag_step(double (&r)[NB], int lane, int nb, dou
     const double p2 = bad ? 1.0 : piv;
     const double rd = fast_rsqrt(p2);
     const double d = p2 * rd;
-    if (lane == J) r[J] = d;
-    if (lane > J) r[J] *= rd;
+    r[J] = lane == J ? d : r[J] * rd;
     if (lane == 0 && J < nb) {
       dv[J] = d;
       rdv[J] = rd;
     }
-    diag_upd<J, J + 1, NB>(r, lane);
-    diag_step<J + 1, NB>(r, lane, nb, dv, rdv, fail);
+    double* col = colbuf + (J & 1) * 32;  // double-buffered: no WAR hazard with step J+1
+    col[lane] = r[J];
+    __syncwarp();
+    diag_upd_s<J, J + 1, NB>(r, col);
+    diag_step<J + 1, NB>(r, lane, nb, dv, rdv, fail, colbuf);
   }
 }
 template <int J, int C, int NB>
@@ -1184,6 +1197,7 @@ __global__ void __launch_bounds__(256, MINB) chol_logdet_kernel(CholArgs a) {
   double* Lc = S + NB * mp;                         // [NB][mp] staged factor columns
   double* diagv = Lc + NB * mp;                     // [nt] pivots sqrt
   __shared__ double rdiag[NB];                      // 1/d of the current panel
+  __shared__ __align__(16) double s_colbuf[64];     // diag factorization column broadcast
   __shared__ int s_fail;
   __shared__ double s_red[8];
   const int tid = threadIdx.x;
@@ -1226,19 +1240,25 @@ __global__ void __launch_bounds__(256, MINB) chol_logdet_kernel(CholArgs a) {
       __syncthreads();
       const int mt_n = (m + 7) >> 3;
       constexpr int NT8 = NB / 8;
-      for (int tt = warp; tt < mt_n * NT8; tt += 8) {
-        const int mt = tt / NT8, n8 = tt - mt * NT8;
-        double acc[2] = {0.0, 0.0};
+      // each warp owns an m8 row and all NB/8 n-tiles: independent DMMA chains
+      for (int mt = warp; mt < mt_n; mt += 8) {
+        double acc[NT8][2];
+#pragma unroll
+        for (int n8 = 0; n8 < NT8; ++n8) acc[n8][0] = acc[n8][1] = 0.0;
 #pragma unroll
         for (int k4 = 0; k4 < NB / 4; ++k4) {
           const double av = Lc[(k4 * 4 + t) * mp + mt * 8 + g];
-          const double bv = Lc[(k4 * 4 + t) * mp + n8 * 8 + g];
-          dmma884(acc, av, bv);
+#pragma unroll
+          for (int n8 = 0; n8 < NT8; ++n8) dmma884(acc[n8], av, Lc[(k4 * 4 + t) * mp + n8 * 8 + g]);
         }
-        const int i = mt * 8 + g, j0 = n8 * 8 + 2 * t;
+        const int i = mt * 8 + g;
         if (i < m) {
-          if (j0 < nb) S[j0 * mp + i] -= acc[0];
-          if (j0 + 1 < nb) S[(j0 + 1) * mp + i] -= acc[1];
+#pragma unroll
+          for (int n8 = 0; n8 < NT8; ++n8) {
+            const int j0 = n8 * 8 + 2 * t;
+            if (j0 < nb) S[j0 * mp + i] -= acc[n8][0];
+            if (j0 + 1 < nb) S[(j0 + 1) * mp + i] -= acc[n8][1];
+          }
         }
       }
     }
@@ -1254,7 +1274,7 @@ __global__ void __launch_bounds__(256, MINB) chol_logdet_kernel(CholArgs a) {
         r[c] = (lane < nb && c < nb) ? (c <= lane ? S[c * mp + lane] : 0.0)
                                      : (c == lane ? 1.0 : 0.0);
       int fail = -1;
-      diag_step<0, NB>(r, lane, nb, diagv + J0, rdiag, fail);
+      diag_step<0, NB>(r, lane, nb, diagv + J0, rdiag, fail, s_colbuf);
       if (lane < nb) {
 #pragma unroll
         for (int c = 0; c < NB; ++c)
