@@ -184,19 +184,11 @@ def ncu_traffic(profile_dir: str):
 
 
 # ------------------------------------------------------------------------- #
-def measure(d, args, world, rank, local, w, v, nid, algorithm, clock=True, want_k=False):
-    """One engine, one algorithm: device-timed time-to-k over K steps, then the
-    e2e (host K -> H2D -> select -> D2H) measurement. Returns a dict."""
-    import numpy as np
-
-    nd, nt, vrank, budget = w["nd"], w["nt"], w["rank"], w["budget"]
-    eng = d.Engine(nd, nt, budget, device=local, world_size=world, rank=rank, nccl_id=nid,
-                   keep_pristine=True, export_factor=True, algorithm=algorithm)
-    t0 = time.time()
-    eng.gen_synthetic(v, vrank, SIGMA)
-    t_gen = time.time() - t0
+def time_device(eng, args, world, clock_dev=None):
+    """K steps of a full selection with K resident in HBM (C restored between
+    steps, outside the timed region): device time-to-k, max over ranks."""
     times, upd_ms, upd_fl, launches, chosen = [], [], [], [], None
-    clk = ClockSampler(local) if clock else None
+    clk = ClockSampler(clock_dev) if clock_dev is not None else None
     if clk:
         clk.__enter__()
     for it in range(args.warmup + args.steps):
@@ -213,7 +205,7 @@ def measure(d, args, world, rank, local, w, v, nid, algorithm, clock=True, want_
         chosen = [r["chosen_index"] for r in eng.trace()]
     if clk:
         clk.__exit__()
-    out = {"value": sum(times) / len(times), "chosen": chosen, "t_gen": t_gen,
+    out = {"value": sum(times) / len(times), "chosen": chosen,
            "launches": int(sum(launches) / len(launches)),
            "clocks": clk.summary() if clk else None}
     upd_t = sum(upd_ms) / 1e3
@@ -221,40 +213,34 @@ def measure(d, args, world, rank, local, w, v, nid, algorithm, clock=True, want_
     out["upd_tf_max"] = allreduce_max(out["upd_tf"], world)
     out["flops_rank"] = sum(upd_fl) / len(upd_fl)
     out["flops_all"] = allreduce_sum(out["flops_rank"], world)
-    out["e2e"] = None
-    hv = None
-    if not args.no_e2e or want_k:
-        import torch
-
-        mine = [j for j in range(nd) if j % world == rank]
-        row_elems = nd * nt * nt
-        host = torch.empty(nd * row_elems, dtype=torch.float64).pin_memory()
-        eng.reset()
-        hv = host.numpy()
-        for j in mine:
-            hv[j * row_elems:(j + 1) * row_elems] = eng.read_block_row(j)
-    if not args.no_e2e:
-        e2e_times, h2d, d2h = [], 0, 0
-        for it in range(max(1, args.warmup // 2) + args.steps):
-            eng.reset()
-            barrier(world)
-            t0 = time.perf_counter()
-            eng.load_k(host)              # H2D of this rank's block rows (pinned)
-            eng.run()
-            rows = eng.trace()            # D2H of the selection result
-            res = np.array([[r["chosen_index"], r["gain"]] for r in rows])
-            t1 = time.perf_counter() - t0
-            st = eng.stats()
-            if it >= max(1, args.warmup // 2):
-                e2e_times.append(allreduce_max(t1, world))
-                h2d = st["h2d_bytes"]
-                d2h = st["d2h_bytes"] + res.size * 8
-            assert [int(x) for x in res[:, 0]] == chosen
-        out["e2e"] = {"value": sum(e2e_times) / len(e2e_times), "unit": "s",
-                      "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
-    out["host_k"] = hv if want_k else None
-    eng.close()
     return out
+
+
+def time_e2e(eng, args, world, host_rows, mine, chosen):
+    """Same selection through the public API from pinned host memory: H2D of
+    this rank's block rows (dsel_load_block_row) + selection + D2H of the
+    result, wall clock, max over ranks."""
+    import numpy as np
+
+    e2e_times, h2d, d2h = [], 0, 0
+    for it in range(max(1, args.warmup // 2) + args.steps):
+        eng.reset()
+        barrier(world)
+        t0 = time.perf_counter()
+        for idx, j in enumerate(mine):
+            eng.load_block_row(j, host_rows[idx])
+        eng.run()
+        rows = eng.trace()            # D2H of the selection result
+        res = np.array([[r["chosen_index"], r["gain"]] for r in rows])
+        t1 = time.perf_counter() - t0
+        st = eng.stats()
+        if it >= max(1, args.warmup // 2):
+            e2e_times.append(allreduce_max(t1, world))
+            h2d = st["h2d_bytes"]
+            d2h = st["d2h_bytes"] + res.size * 8
+        assert [int(x) for x in res[:, 0]] == chosen
+    return {"value": sum(e2e_times) / len(e2e_times), "unit": "s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
 
 def our_arm(args, world, rank, local):
@@ -265,25 +251,49 @@ def our_arm(args, world, rank, local):
     t0 = time.time()
     v = d.synthetic_v(nd, nt, vrank, SEED, threads=max(1, (os.cpu_count() or 1) // world))
     t_v = time.time() - t0
-    nid = broadcast_bytes(d.nccl_unique_id() if (world > 1 and rank == 0) else None, world)
-    want_cpu = rank == 0 and world == 1 and not args.no_cpu
-    prim = measure(d, args, world, rank, local, w, v, nid, args.algorithm, want_k=want_cpu)
-    other = None
-    if not args.no_variants:
-        alt = "left" if args.algorithm == "right" else "right"
-        nid2 = broadcast_bytes(d.nccl_unique_id() if (world > 1 and rank == 0) else None, world)
-        other = measure(d, args, world, rank, local, w, v, nid2, alt, clock=False)
-        if other["chosen"] != prim["chosen"]:
-            raise RuntimeError("right- and left-looking sequences differ")
+    algos = [args.algorithm] + ([] if args.no_variants else
+                                ["left" if args.algorithm == "right" else "right"])
+    engines, t_gen = {}, 0.0
+    for a in algos:  # every engine gets the same bit-exact K, then V is released
+        nid = broadcast_bytes(d.nccl_unique_id() if (world > 1 and rank == 0) else None, world)
+        engines[a] = d.Engine(nd, nt, budget, device=local, world_size=world, rank=rank,
+                              nccl_id=nid, keep_pristine=True, export_factor=True, algorithm=a)
+        t0 = time.time()
+        engines[a].gen_synthetic(v, vrank, SIGMA)
+        t_gen = max(t_gen, time.time() - t0)
     del v
+    res = {a: time_device(engines[a], args, world, local if a == args.algorithm else None)
+           for a in algos}
+    if len(algos) > 1 and res[algos[0]]["chosen"] != res[algos[1]]["chosen"]:
+        raise RuntimeError("right- and left-looking sequences differ")
+    want_cpu = rank == 0 and world == 1 and not args.no_cpu
+    mine = [j for j in range(nd) if j % world == rank]
+    host_rows = None
+    if not args.no_e2e or want_cpu:
+        import torch
+
+        row_elems = nd * nt * nt
+        host = torch.empty(len(mine) * row_elems, dtype=torch.float64).pin_memory()
+        hv = host.numpy()
+        eng0 = engines[algos[0]]
+        eng0.reset()
+        for idx, j in enumerate(mine):
+            hv[idx * row_elems:(idx + 1) * row_elems] = eng0.read_block_row(j)
+        host_rows = [host[idx * row_elems:(idx + 1) * row_elems] for idx in range(len(mine))]
+    for a in algos:
+        res[a]["e2e"] = None if args.no_e2e else time_e2e(engines[a], args, world, host_rows, mine,
+                                                          res[a]["chosen"])
+        engines[a].close()
+    prim = res[algos[0]]
+    other = res[algos[1]] if len(algos) > 1 else None
     value, chosen, clocks = prim["value"], prim["chosen"], prim["clocks"]
     upd_tf, upd_tf_all = prim["upd_tf"], prim["upd_tf_max"]
     tot_flops, tot_flops_all = prim["flops_rank"], prim["flops_all"]
     e2e_tf = tot_flops_all / value / 1e12
-    e2e, t_gen, launches = prim["e2e"], prim["t_gen"], [prim["launches"]]
+    e2e, launches = prim["e2e"], [prim["launches"]]
     cpu = None
     if want_cpu:
-        cpu = cpu_reference(prim["host_k"], nd, nt, budget, chosen)
+        cpu = cpu_reference(hv, nd, nt, budget, chosen)
 
     tr = ncu_traffic(os.path.join(ROOT, "profiles"))
     traffic = tr.get("traffic_bytes_per_launch") if tr else None
