@@ -189,6 +189,8 @@ typedef struct {
   double time_to_k_ms;
   double update_ms;
   double update_flops;
+  double io_ms;           /* storage=stream: H2D time of the streamed K columns */
+  double io_exposed_ms;   /* part of io_ms not hidden behind the GEMM */
 } dsel_stats;
 dsel_status dsel_get_stats(dsel_engine* e, dsel_stats* st);
 /* L_S (SelectionState::factor): row-major, (k*Nt) x (k*Nt) active window with

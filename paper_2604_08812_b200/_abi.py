@@ -56,7 +56,8 @@ class DselStats(C.Structure):
     _fields_ = [("rounds", C.c_int), ("kernel_launches", C.c_uint64), ("h2d_bytes", C.c_uint64),
                 ("d2h_bytes", C.c_uint64), ("nccl_bytes", C.c_uint64),
                 ("time_to_k_ms", C.c_double), ("update_ms", C.c_double),
-                ("update_flops", C.c_double)]
+                ("update_flops", C.c_double), ("io_ms", C.c_double),
+                ("io_exposed_ms", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -71,7 +71,7 @@ T* dmalloc(size_t count, uint64_t& total) {
   return static_cast<T*>(p);
 }
 
-constexpr int kEv = 5;
+constexpr int kEv = 8;  // 0-4 phases; 5,6 streamed H2D start/end (copy stream); 7 GEMM end
 
 }  // namespace
 
@@ -86,6 +86,13 @@ struct dsel_engine {
   int n_sms = 148;
   int mpad = 0;  // rows of the tiled W buffers
   bool ll = false;  // left-looking W-resident algorithm
+  // storage = STREAM (left-looking): K lives in pinned host memory only,
+  // hstore[position][own slot][nt][nt] = K(own_q, k); per round the chosen
+  // k's blocks are copied into Kk on the copy stream, overlapped with the GEMM
+  bool stream = false;
+  double *hstore = nullptr, *Kk = nullptr;
+  cudaEvent_t ev_kk0 = nullptr, ev_kk1 = nullptr;
+  std::vector<int> streamed_round;  // rounds whose ev[5..7] are valid
   double *Wown = nullptr, *Wkn = nullptr, *D = nullptr, *cbuf = nullptr, *ldiag = nullptr,
          *cpart = nullptr;
   int* d_iota = nullptr;
@@ -419,6 +426,15 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
   const int nt = e->nt;
   const long long n2 = (long long)nt * nt;
   const int kcols = round * e->ldw;  // W_all columns so far
+  if (e->stream && !last && e->nloc > 0) {
+    // the chosen column's blocks for this rank's rows, on the copy stream
+    CU(cudaEventRecord(ev[5], e->cs));
+    CU(cudaMemcpyAsync(e->Kk, e->hstore + (size_t)p * e->nloc * n2,
+                       sizeof(double) * (size_t)e->nloc * n2, cudaMemcpyHostToDevice, e->cs));
+    CU(cudaEventRecord(ev[6], e->cs));
+    e->streamed_round.push_back(round);
+    e->h2d_bytes += (uint64_t)e->nloc * n2 * sizeof(double);
+  }
   if (owner == e->rank) {
     CU(cudaMemcpyAsync(e->ldiag + (size_t)round * n2, Lk, sizeof(double) * n2,
                        cudaMemcpyDeviceToDevice, e->s));
@@ -456,7 +472,7 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
     ga.Wkn = e->Wkn;
     ga.k_mpad = e->k_mpad;
     ga.n_k = kcols / 16;
-    ga.Kp = e->C;
+    ga.Kp = e->stream ? nullptr : e->C;  // streaming: K added after the GEMM
     ga.ldk = e->n;
     ga.pk = p;
     ga.row_slot = e->col_slot();
@@ -472,7 +488,15 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
     dim3 gg((n_rows + llg::BM - 1) / llg::BM, (nt + llg::BN - 1) / llg::BN, ga.n_splits);
     ll_gemm_kernel<<<gg, llg::THREADS, llg::SMEM, e->s>>>(ga);
     CU(cudaGetLastError());
-    if (ga.n_splits > 1) {
+    if (e->stream) {
+      const long long total = (long long)nt * n_rows;
+      CU(cudaEventRecord(ev[7], e->s));
+      CU(cudaStreamWaitEvent(e->s, ev[6], 0));
+      ll_addk_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 8), 256, 0, e->s>>>(
+          e->cpart, ga.part_stride, ga.n_splits, e->Kk, e->col_slot(), nt, n_rows, e->ldo, e->cbuf);
+      CU(cudaGetLastError());
+      e->launches += 1;
+    } else if (ga.n_splits > 1) {
       const long long total = (long long)nt * n_rows;
       ll_reduce_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 8), 256, 0, e->s>>>(
           e->cpart, ga.part_stride, ga.n_splits, nt, n_rows, e->ldo, e->cbuf);
@@ -533,7 +557,17 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
 
   // ---- gains + local argmax ----
   CU(cudaEventRecord(ev[0], e->s));
-  if (e->ll && round == 0 && e->nloc > 0) {
+  if (e->stream && round == 0 && e->nloc > 0) {
+    // D[q] = K(own_q, own_q)^T = K(own_q, own_q) (symmetric), from the host store;
+    // store block is row-major, D is column-major: equal for a symmetric block
+    for (int qq = 0; qq < e->nloc; ++qq) {
+      const int pq = qq * e->G + e->rank;
+      CU(cudaMemcpyAsync(e->D + (size_t)qq * nt * nt,
+                         e->hstore + ((size_t)pq * e->nloc + qq) * nt * nt,
+                         sizeof(double) * nt * nt, cudaMemcpyHostToDevice, e->s));
+    }
+    e->h2d_bytes += (uint64_t)e->nloc * nt * nt * sizeof(double);
+  } else if (e->ll && round == 0 && e->nloc > 0) {
     const long long total = (long long)e->nloc * nt * nt;
     ll_init_d_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 16), 256, 0, e->s>>>(
         e->C, e->n, nt, e->nloc, e->G, e->rank, e->D);
@@ -819,6 +853,10 @@ void destroy_impl(dsel_engine* e) {
   if (e->h_recs) cudaFreeHost(e->h_recs);
   if (e->h_tab) cudaFreeHost(e->h_tab);
   if (e->h_sym) cudaFreeHost(e->h_sym);
+  if (e->hstore) cudaFreeHost(e->hstore);
+  if (e->Kk) cudaFree(e->Kk);
+  if (e->ev_kk0) cudaEventDestroy(e->ev_kk0);
+  if (e->ev_kk1) cudaEventDestroy(e->ev_kk1);
   if (e->h_stage) cudaFreeHost(e->h_stage);
   if (e->comm) ncclCommDestroy(e->comm);
   for (int b = 0; b < 2; ++b) {
@@ -836,8 +874,9 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
   if (cfg->budget < 0) throw Fail{DSEL_E_INVALID, "budget must be nonnegative"};
   if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size)
     throw Fail{DSEL_E_INVALID, "bad world_size/rank"};
-  if (cfg->storage == DSEL_STORAGE_STREAM)
-    throw Fail{DSEL_E_INVALID, "storage=stream (pinned-host panel streaming) is not available in this build"};
+  if (cfg->storage == DSEL_STORAGE_STREAM && cfg->algorithm != 1)
+    throw Fail{DSEL_E_INVALID, "storage=stream streams one K column per round and needs the "
+                               "left-looking W-resident algorithm (algorithm = 1, SURVEY 7.3-4)"};
   if (cfg->n_steps > 1024) throw Fail{DSEL_E_INVALID, "n_steps > 1024 is not supported by the gain kernel"};
   auto* e = new dsel_engine();
   try {
@@ -893,7 +932,7 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     }
     uint64_t& tot = e->dev_bytes;
     const size_t shard = (size_t)e->n * (size_t)e->nloc * e->nt;
-    e->C = dmalloc<double>(shard, tot);
+    if (!e->stream) e->C = dmalloc<double>(shard, tot);
     if (e->keep) e->K0 = dmalloc<double>(shard, tot);
     if (e->nt % 2) e->W = dmalloc<double>((size_t)e->n * e->ldw, tot);  // odd-nt update path
     e->mpad = round_up((int)e->n, ws::BR);
@@ -906,6 +945,7 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
       e->Wn = dmalloc<double>((size_t)e->n * e->ldw, tot);
     }
     e->ll = cfg->algorithm == 1;
+    e->stream = cfg->storage == DSEL_STORAGE_STREAM;
     if (cfg->algorithm < 0 || cfg->algorithm > 1) throw Fail{DSEL_E_INVALID, "unknown algorithm"};
     e->sym = cfg->full_square == 0 && e->nt % 2 == 0 && !e->ll;
     if ((e->G > 1 || e->sym) && !e->ll) e->Pbuf = dmalloc<double>((size_t)e->n * e->nt, tot);
@@ -961,7 +1001,13 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
       CU(cudaMemsetAsync(e->Wt, 0, sizeof(double) * (size_t)e->mpad * e->ldw, e->s));
       CU(cudaMemsetAsync(e->Wnt, 0, sizeof(double) * (size_t)e->mpad * e->ldw, e->s));
     }
-    CU(cudaMemsetAsync(e->C, 0, sizeof(double) * shard, e->s));
+    if (e->C) CU(cudaMemsetAsync(e->C, 0, sizeof(double) * shard, e->s));
+    if (e->stream) {
+      CU(cudaMallocHost(&e->hstore, sizeof(double) * (size_t)e->nc * std::max(e->nloc, 1) * e->nt * e->nt));
+      e->Kk = dmalloc<double>((size_t)std::max(e->nloc, 1) * e->nt * e->nt, tot);
+      CU(cudaEventCreate(&e->ev_kk0));
+      CU(cudaEventCreate(&e->ev_kk1));
+    }
     CU(cudaMemcpyAsync(e->d_pos_sensor, e->pos_sensor.data(), sizeof(int) * e->nc,
                        cudaMemcpyHostToDevice, e->s));
     if (e->nloc)
@@ -1000,8 +1046,32 @@ void ensure_stage(dsel_engine* e, size_t elems) {
 // Panel store ingest: H2D of one block row/column into device staging on the
 // copy stream (double-buffered, event-ordered), scatter into the panel on the
 // compute stream, so consecutive panels overlap copy and scatter.
+// Streaming store fill: block row j of an own candidate (as_column = false)
+// gives K(own_j, k) for every k; a block column j gives K(own_i, j) for every
+// own i (host-to-host copies into the pinned store).
+void store_fill(dsel_engine* e, int j, const double* host, bool as_column) {
+  const size_t n2 = (size_t)e->nt * e->nt;
+  const int p = e->sensor_pos[j];
+  if (p < 0) return;
+  if (!as_column) {
+    if (p % e->G != e->rank) return;
+    const int q = p / e->G;
+    for (int pk = 0; pk < e->nc; ++pk)
+      std::memcpy(e->hstore + ((size_t)pk * e->nloc + q) * n2, host + (size_t)e->pos_sensor[pk] * n2,
+                  n2 * sizeof(double));
+  } else {
+    for (int q = 0; q < e->nloc; ++q)
+      std::memcpy(e->hstore + ((size_t)p * e->nloc + q) * n2, host + (size_t)e->slot_sensor[q] * n2,
+                  n2 * sizeof(double));
+  }
+}
+
 void load_panel(dsel_engine* e, int j, const double* host, bool as_column) {
   if (j < 0 || j >= e->nd) throw Fail{DSEL_E_RANGE, "block index out of range"};
+  if (e->stream) {
+    store_fill(e, j, host, as_column);
+    return;
+  }
   const int p = e->sensor_pos[j];
   if (p < 0 || p % e->G != e->rank) return;
   const int q = p / e->G;
@@ -1136,6 +1206,15 @@ dsel_status dsel_load_block_col(dsel_engine* e, int j, const double* host_col) {
 
 dsel_status dsel_load_k(dsel_engine* e, const double* host_k) {
   return guard(e, [&] {
+    if (e->stream) {  // hstore[pk][q] = K(own_q, k): block (s_q, s_k) of the block-row-major K
+      const size_t n2 = (size_t)e->nt * e->nt;
+      for (int pk = 0; pk < e->nc; ++pk)
+        for (int q = 0; q < e->nloc; ++q)
+          std::memcpy(e->hstore + ((size_t)pk * e->nloc + q) * n2,
+                      host_k + ((size_t)e->slot_sensor[q] * e->nd + e->pos_sensor[pk]) * n2,
+                      n2 * sizeof(double));
+      return;
+    }
     const size_t row = (size_t)e->nd * e->nt * e->nt;
     for (int q = 0; q < e->nloc; ++q) {
       const int sidx = e->slot_sensor[q];
@@ -1261,6 +1340,14 @@ dsel_status dsel_read_block_row(dsel_engine* e, int j, double* host_row) {
     if (p < 0 || p % e->G != e->rank) throw Fail{DSEL_E_RANGE, "block row not owned by this rank"};
     const int q = p / e->G;
     const size_t elems = (size_t)e->nd * e->nt * e->nt;
+    if (e->stream) {  // K itself, from the pinned host store
+      const size_t n2 = (size_t)e->nt * e->nt;
+      std::memset(host_row, 0, elems * sizeof(double));
+      for (int pk = 0; pk < e->nc; ++pk)
+        std::memcpy(host_row + (size_t)e->pos_sensor[pk] * n2,
+                    e->hstore + ((size_t)pk * e->nloc + q) * n2, n2 * sizeof(double));
+      return;
+    }
     CU(cudaSetDevice(e->dev));
     ensure_stage(e, elems);
     CU(cudaMemsetAsync(e->stage, 0, elems * sizeof(double), e->s));
@@ -1291,7 +1378,7 @@ dsel_status dsel_gen_synthetic(dsel_engine* e, const double* v_host, int rank, d
     uint64_t dummy = 0;
     double* V = dmalloc<double>(vel, dummy);
     cudaError_t ce = cudaMemcpy(V, v_host, vel * sizeof(double), cudaMemcpyHostToDevice);
-    if (ce == cudaSuccess && e->nloc > 0) {
+    if (ce == cudaSuccess && e->nloc > 0 && !e->stream) {
       GenArgs g{};
       g.V = V;
       g.rank = rank;
@@ -1307,11 +1394,45 @@ dsel_status dsel_gen_synthetic(dsel_engine* e, const double* v_host, int rank, d
       synth_panel_kernel<<<grid, gen::THREADS, 0, e->s>>>(g);
       ce = cudaGetLastError();
       if (ce == cudaSuccess) ce = cudaStreamSynchronize(e->s);
+    } else if (ce == cudaSuccess && e->nloc > 0) {
+      // streaming store: one own panel at a time on the device, repacked to
+      // [position][nt][nt] and copied into its slot of the pinned host store
+      const size_t n2 = (size_t)e->nt * e->nt;
+      double* panel = nullptr;
+      double* packed = nullptr;
+      ce = cudaMalloc(&panel, sizeof(double) * (size_t)e->n * e->nt);
+      if (ce == cudaSuccess) ce = cudaMalloc(&packed, sizeof(double) * (size_t)e->nc * n2);
+      for (int q = 0; q < e->nloc && ce == cudaSuccess; ++q) {
+        GenArgs g{};
+        g.V = V;
+        g.rank = rank;
+        g.noise2 = sigma * sigma;
+        g.nt = e->nt;
+        g.row_sensor = e->d_pos_sensor;
+        g.n_rows = (int)e->n;
+        g.col_sensor = e->d_slot_sensor + q;
+        g.n_cols = e->nt;
+        g.C = panel;
+        g.ldc = e->n;
+        dim3 grid((g.n_rows + gen::BM - 1) / gen::BM, (g.n_cols + gen::BN - 1) / gen::BN);
+        synth_panel_kernel<<<grid, gen::THREADS, 0, e->s>>>(g);
+        const long long total = (long long)e->nc * n2;
+        stream_pack_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 16), 256, 0,
+                             e->s>>>(panel, e->n, e->nt, e->nc, packed);
+        ce = cudaGetLastError();
+        if (ce == cudaSuccess)
+          ce = cudaMemcpy2DAsync(e->hstore + (size_t)q * n2, (size_t)e->nloc * n2 * sizeof(double),
+                                 packed, n2 * sizeof(double), n2 * sizeof(double), e->nc,
+                                 cudaMemcpyDeviceToHost, e->s);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(e->s);
+      }
+      if (panel) cudaFree(panel);
+      if (packed) cudaFree(packed);
     }
     cudaFree(V);
     if (ce != cudaSuccess) throw Fail{DSEL_E_CUDA, std::string("synthetic K: ") + cudaGetErrorString(ce)};
     e->full_panels = true;
-    if (e->keep)
+    if (e->keep && e->C)
       CU(cudaMemcpyAsync(e->K0, e->C, sizeof(double) * e->n * e->nloc * e->nt,
                          cudaMemcpyDeviceToDevice, e->s));
     CU(cudaStreamSynchronize(e->s));
@@ -1399,6 +1520,7 @@ dsel_status dsel_reset(dsel_engine* e) {
     e->finished = false;
     e->launches = 0;
     e->update_flops = 0.0;
+    e->streamed_round.clear();
     e->h2d_bytes = e->d2h_bytes = e->nccl_bytes = 0;
     build_tables(e);
     CU(cudaStreamSynchronize(e->s));
@@ -1417,6 +1539,14 @@ dsel_status dsel_get_stats(dsel_engine* e, dsel_stats* st) {
     r.d2h_bytes = e->d2h_bytes;
     r.nccl_bytes = e->nccl_bytes;
     r.update_flops = e->update_flops;
+    for (int rd : e->streamed_round) {
+      float io = 0, exposed = 0;
+      const cudaEvent_t* ev = &e->ev[(size_t)rd * kEv];
+      CU(cudaEventElapsedTime(&io, ev[5], ev[6]));
+      CU(cudaEventElapsedTime(&exposed, ev[7], ev[6]));  // copy end after GEMM end -> exposed
+      r.io_ms += io;
+      r.io_exposed_ms += std::max(0.0f, exposed);
+    }
     if (r.rounds > 0) {
       float ms = 0;
       // first gain launch -> winner of the last round on the host (its D2H)

@@ -940,7 +940,7 @@ __global__ void __launch_bounds__(llg::THREADS, 2) ll_gemm_kernel(LLGemmArgs a) 
     for (int j = 0; j < 4; ++j) {
       const int c = c0 + wn + j * 8 + 2 * t;
       acc[i][j][0] = acc[i][j][1] = 0.0;
-      if (z == 0 && kb >= 0 && c < nt) {
+      if (z == 0 && a.Kp && kb >= 0 && c < nt) {
         const double* src = a.Kp + kb + c;
         acc[i][j][0] = src[0];
         if (c + 1 < nt) acc[i][j][1] = src[1];
@@ -1071,6 +1071,45 @@ __global__ void __launch_bounds__(256) ll_dupdate_kernel(LLDArgs a) {
       if (c < nt) D[(size_t)c * nt + r] -= acc[i][j][0];
       if (c + 1 < nt) D[(size_t)(c + 1) * nt + r] -= acc[i][j][1];
     }
+  }
+}
+
+// Streaming (out-of-HBM) store, left-looking: the blocks K(own_q, k) of the
+// round's chosen candidate k arrive by H2D into Kk ([slot][nt][nt] row-major)
+// while the GEMM computes -W_own W_k^T; this adds them (and sums split-K
+// partials in split order when present): c[col][row] += Kk[q][r][col].
+__global__ void ll_addk_kernel(const double* part, long long part_stride, int n_splits,
+                               const double* Kk, const int* row_slot, int nt, int n_rows,
+                               long long ldo, double* cout) {
+  const long long total = (long long)nt * n_rows;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e / n_rows), r = (int)(e - (long long)c * n_rows);
+    const size_t o = (size_t)c * ldo + r;
+    double v;
+    if (n_splits > 1) {
+      v = part[o];
+      for (int z = 1; z < n_splits; ++z) v += part[(size_t)z * part_stride + o];
+    } else {
+      v = cout[o];
+    }
+    const int blk = r / nt, rr = r - blk * nt;
+    cout[o] = v + Kk[((size_t)row_slot[blk] * nt + rr) * nt + c];
+  }
+}
+
+// Streaming store staging: device panel of own slot q (column-major, n rows)
+// -> host-store order [position][q][r][c] = K(own_q, k)[r][c] for this slot.
+__global__ void stream_pack_kernel(const double* panel, long long ldp, int nt, int n_cand,
+                                   double* out /* [n_cand][nt][nt] for this slot */) {
+  const long long total = (long long)n_cand * nt * nt;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int pk = (int)(e / ((long long)nt * nt));
+    const long long w = e - (long long)pk * nt * nt;
+    const int r = (int)(w / nt), c = (int)(w - (long long)r * nt);
+    // K(own_q, k)[r][c] = K[q-block row r][k col c] = K[k*nt + c][q*nt + r] (symmetric)
+    out[e] = panel[(size_t)r * ldp + (size_t)pk * nt + c];
   }
 }
 

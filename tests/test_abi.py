@@ -88,4 +88,6 @@ def test_invalid_config_rejected_before_device_work():
     with pytest.raises(d.IndexOutOfRange):
         d.Engine(8, 2, 2, candidates=[1, 8])
     with pytest.raises(d.InvalidConfig):
-        d.Engine(8, 2, 2, storage=2)
+        d.Engine(8, 2, 2, storage=2)               # streaming needs the left-looking algorithm
+    with pytest.raises(d.InvalidConfig):
+        d.Engine(8, 2, 2, algorithm="middle")
