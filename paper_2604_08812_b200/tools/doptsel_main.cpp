@@ -7,6 +7,7 @@
 // available here, so flags and JSON are hand-rolled.
 //
 //   doptsel select <kbf> --budget B [--mode schur|gpu] [--gpus G] [--workers N]
+//                  [--algorithm right|left] [--storage auto|hbm|stream]
 //                  [--seed S] [--pipeline on|off] [--precision f64]
 //                  [--config cfg | --noise-logdets file] [--kbf-rows] [--out DIR]
 //   doptsel select --synthetic nd,nt,rank,sigma,seed --budget B ...
@@ -67,6 +68,7 @@ struct SelectArgs {
   std::string kbf, out = ".", mode = "schur", precision = "f64", pipeline = "on", config,
                    noise_file, synthetic;
   int budget = -1, workers = 1, gpus = 1;
+  std::string algorithm = "right", storage = "auto";
   unsigned long long seed = 0;
   bool kbf_rows = false;
 };
@@ -230,6 +232,10 @@ int run_select(const SelectArgs& a) {
     cfg.rank = r;
     cfg.nccl_id = nid.data();
     cfg.near_tie_tau = 1e-9;
+    cfg.algorithm = a.algorithm == "left" ? 1 : 0;
+    cfg.storage = a.storage == "stream" ? DSEL_STORAGE_STREAM
+                                        : (a.storage == "hbm" ? DSEL_STORAGE_HBM : DSEL_STORAGE_AUTO);
+    if (cfg.storage == DSEL_STORAGE_STREAM) cfg.algorithm = 1;  // streaming is left-looking
     dsel_engine* e = nullptr;
     out.st = dsel_create(&cfg, &e);
     if (out.st != DSEL_OK) {
@@ -358,6 +364,7 @@ int run_select(const SelectArgs& a) {
 
 int usage() {
   std::cerr << "usage: doptsel select <kbf> --budget B [--mode schur|gpu] [--gpus G] [--workers N]\n"
+               "                      [--algorithm right|left] [--storage auto|hbm|stream]\n"
                "                      [--seed S] [--pipeline on|off] [--precision f64]\n"
                "                      [--config cfg | --noise-logdets file] [--kbf-rows] [--out DIR]\n"
                "       doptsel select --synthetic nd,nt,rank,sigma,seed --budget B [...]\n";
@@ -400,6 +407,13 @@ int main(int argc, char** argv) {
       else if (s == "--noise-logdets") a.noise_file = val();
       else if (s == "--synthetic") a.synthetic = val();
       else if (s == "--kbf-rows") a.kbf_rows = true;
+      else if (s == "--algorithm") {
+        a.algorithm = val();
+        if (a.algorithm != "right" && a.algorithm != "left") return usage();
+      } else if (s == "--storage") {
+        a.storage = val();
+        if (a.storage != "auto" && a.storage != "hbm" && a.storage != "stream") return usage();
+      }
       else if (s == "--out") a.out = val();
       else if (!s.empty() && s[0] == '-') return usage();
       else if (a.kbf.empty()) a.kbf = s;

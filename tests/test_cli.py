@@ -87,3 +87,14 @@ def test_select_kbf_row_layout_matches(tmp_path):
             str(tmp_path / "o"))
     assert r.returncode == 0, r.stderr
     assert json.load(open(tmp_path / "o" / "selection.json"))["chosen"] == w["chosen"]
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not gpu_available(), reason="needs a CUDA GPU")
+@pytest.mark.parametrize("extra", [["--algorithm", "left"], ["--storage", "stream"]])
+def test_select_variants(tmp_path, extra):
+    w = json.load(open(os.path.join(GOLD, "wave.json")))
+    r = run("select", os.path.join(GOLD, "wave.kbf"), "--budget", "12", *extra, "--out",
+            str(tmp_path / "o"))
+    assert r.returncode == 0, r.stderr
+    assert json.load(open(tmp_path / "o" / "selection.json"))["chosen"] == w["chosen"]
