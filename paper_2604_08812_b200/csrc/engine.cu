@@ -96,6 +96,8 @@ struct dsel_engine {
   double *Wown = nullptr, *Wkn = nullptr, *D = nullptr, *cbuf = nullptr, *ldiag = nullptr,
          *cpart = nullptr;
   int* d_iota = nullptr;
+  int* d_pk = nullptr;  // chosen position (left-looking row map of the re-targeted update)
+  int* h_pk = nullptr;  // pinned
   int own_mpad = 0, k_mpad = 0;
   long long ldo = 0;
   bool sym = true;  // block-lower-triangle (symmetric) update
@@ -466,42 +468,74 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
   CU(cudaEventRecord(ev[3], e->s));
   if (!last && Rl > 0) {
     const int n_rows = Rl * nt;
-    LLGemmArgs ga;
-    ga.Wown = e->Wown;
-    ga.own_mpad = e->own_mpad;
-    ga.Wkn = e->Wkn;
-    ga.k_mpad = e->k_mpad;
-    ga.n_k = kcols / 16;
-    ga.Kp = e->stream ? nullptr : e->C;  // streaming: K added after the GEMM
-    ga.ldk = e->n;
-    ga.pk = p;
-    ga.row_slot = e->col_slot();
-    ga.nt = nt;
-    ga.n_rows = n_rows;
-    ga.cout = e->cbuf;
-    ga.ldo = e->ldo;
-    ga.kc_split = kLLSplitChunks;
-    ga.n_splits = std::max(1, std::min(kLLMaxSplits, (ga.n_k + kLLSplitChunks - 1) / kLLSplitChunks));
-    ga.kc_split = std::max(ga.kc_split, (ga.n_k + ga.n_splits - 1) / ga.n_splits);
-    ga.part = e->cpart;
-    ga.part_stride = e->ldo * nt;
-    dim3 gg((n_rows + llg::BM - 1) / llg::BM, (nt + llg::BN - 1) / llg::BN, ga.n_splits);
-    ll_gemm_kernel<<<gg, llg::THREADS, llg::SMEM, e->s>>>(ga);
-    CU(cudaGetLastError());
-    if (e->stream) {
-      const long long total = (long long)nt * n_rows;
-      CU(cudaEventRecord(ev[7], e->s));
-      CU(cudaStreamWaitEvent(e->s, ev[6], 0));
-      ll_addk_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 8), 256, 0, e->s>>>(
-          e->cpart, ga.part_stride, ga.n_splits, e->Kk, e->col_slot(), nt, n_rows, e->ldo, e->cbuf);
+    if (!e->stream && nt % 2 == 0) {
+      // the warp-specialized TMA update kernel, re-targeted: r-side = W_k
+      // (c' rows), c-side = this rank's live rows of W_own, accumulators
+      // start from K(own, k) (the pristine panels), output to cbuf
+      *e->h_pk = p;
+      CU(cudaMemcpyAsync(e->d_pk, e->h_pk, sizeof(int), cudaMemcpyHostToDevice, e->s));
+      UpdateWSArgs ua{};
+      ua.C = e->C;
+      ua.ldc = e->n;
+      ua.Wt = e->Wkn;
+      ua.Wnt = e->Wown;
+      ua.mpad = e->k_mpad;
+      ua.n_k = kcols / 16;
+      ua.row_pos = e->d_pk;          // single "block": p_k -> rows p_k*nt + c'
+      ua.col_slot = e->col_slot();
+      ua.col_g = e->col_slot();      // c-side W rows are slot*nt + off
+      ua.nt = nt;
+      ua.n_rows = nt;
+      ua.n_cols = n_rows;
+      ua.n_row_tiles = (nt + ws::BR - 1) / ws::BR;
+      ua.n_col_tiles = (n_rows + ws::BC - 1) / ws::BC;
+      ua.group = ws_group;
+      ua.sym = 0;
+      ua.n_tiles = ua.n_row_tiles * ua.n_col_tiles;
+      ua.cout = e->cbuf;
+      ua.ldo = e->ldo;
+      ua.mpad_c = e->own_mpad;
+      const int grid = (int)std::min<long long>(e->n_sms, ua.n_tiles);
+      schur_update_ws_kernel<<<grid, ws::THREADS, ws::SMEM, e->s>>>(ua);
       CU(cudaGetLastError());
-      e->launches += 1;
-    } else if (ga.n_splits > 1) {
-      const long long total = (long long)nt * n_rows;
-      ll_reduce_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 8), 256, 0, e->s>>>(
-          e->cpart, ga.part_stride, ga.n_splits, nt, n_rows, e->ldo, e->cbuf);
+    } else {
+      LLGemmArgs ga;
+      ga.Wown = e->Wown;
+      ga.own_mpad = e->own_mpad;
+      ga.Wkn = e->Wkn;
+      ga.k_mpad = e->k_mpad;
+      ga.n_k = kcols / 16;
+      ga.Kp = e->stream ? nullptr : e->C;  // streaming: K added after the GEMM
+      ga.ldk = e->n;
+      ga.pk = p;
+      ga.row_slot = e->col_slot();
+      ga.nt = nt;
+      ga.n_rows = n_rows;
+      ga.cout = e->cbuf;
+      ga.ldo = e->ldo;
+      ga.kc_split = kLLSplitChunks;
+      ga.n_splits = std::max(1, std::min(kLLMaxSplits, (ga.n_k + kLLSplitChunks - 1) / kLLSplitChunks));
+      ga.kc_split = std::max(ga.kc_split, (ga.n_k + ga.n_splits - 1) / ga.n_splits);
+      ga.part = e->cpart;
+      ga.part_stride = e->ldo * nt;
+      dim3 gg((n_rows + llg::BM - 1) / llg::BM, (nt + llg::BN - 1) / llg::BN, ga.n_splits);
+      ll_gemm_kernel<<<gg, llg::THREADS, llg::SMEM, e->s>>>(ga);
       CU(cudaGetLastError());
-      e->launches += 1;
+      if (e->stream) {
+        const long long total = (long long)nt * n_rows;
+        CU(cudaEventRecord(ev[7], e->s));
+        CU(cudaStreamWaitEvent(e->s, ev[6], 0));
+        ll_addk_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 8), 256, 0, e->s>>>(
+            e->cpart, ga.part_stride, ga.n_splits, e->Kk, e->col_slot(), nt, n_rows, e->ldo, e->cbuf);
+        CU(cudaGetLastError());
+        e->launches += 1;
+      } else if (ga.n_splits > 1) {
+        const long long total = (long long)nt * n_rows;
+        ll_reduce_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 8), 256, 0, e->s>>>(
+            e->cpart, ga.part_stride, ga.n_splits, nt, n_rows, e->ldo, e->cbuf);
+        CU(cudaGetLastError());
+        e->launches += 1;
+      }
     }
     PanelArgs pa{};
     pa.P = e->cbuf;
@@ -845,7 +879,8 @@ void destroy_impl(dsel_engine* e) {
                     e->kgain, e->stage, e->xbuf};
   for (double* d : dptr)
     if (d) cudaFree(d);
-  int* iptr[] = {e->status, e->kstatus, e->d_pos_sensor, e->d_slot_sensor, e->d_tab, e->d_sym, e->d_iota};
+  int* iptr[] = {e->status, e->kstatus, e->d_pos_sensor, e->d_slot_sensor, e->d_tab, e->d_sym, e->d_iota, e->d_pk};
+  if (e->h_pk) cudaFreeHost(e->h_pk);
   for (int* d : iptr)
     if (d) cudaFree(d);
   if (e->d_rec) cudaFree(e->d_rec);
@@ -952,7 +987,7 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     if (e->ll) {
       const int B = std::max(e->eff_budget, 1);
       e->own_mpad = round_up(std::max(e->nloc, 1) * e->nt, 128);
-      e->k_mpad = e->nt;
+      e->k_mpad = round_up(e->nt, ws::BR);  // whole 128-row r-side tiles stay inside the buffer
       e->ldo = (long long)std::max(e->nloc, 1) * e->nt;
       e->Wown = dmalloc<double>((size_t)e->own_mpad * B * e->ldw, tot);
       e->Wkn = dmalloc<double>((size_t)e->k_mpad * B * e->ldw, tot);
@@ -965,6 +1000,8 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
       }
       e->ldiag = dmalloc<double>((size_t)B * e->nt * e->nt, tot);
       e->d_iota = dmalloc<int>(std::max(e->nloc, 1), tot);
+      e->d_pk = dmalloc<int>(1, tot);
+      CU(cudaMallocHost(&e->h_pk, sizeof(int)));
       std::vector<int> iota(std::max(e->nloc, 1));
       for (size_t i = 0; i < iota.size(); ++i) iota[i] = (int)i;
       CU(cudaMemcpy(e->d_iota, iota.data(), sizeof(int) * iota.size(), cudaMemcpyHostToDevice));

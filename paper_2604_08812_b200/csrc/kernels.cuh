@@ -304,13 +304,14 @@ constexpr int CP = BR + 8;  // C tile column pitch (doubles): conflict-free LDS.
 constexpr size_t OFF_R = 0;
 constexpr size_t OFF_C = OFF_R + (size_t)STAGES * SC * BR * KC * 8;
 constexpr size_t OFF_CT = OFF_C + (size_t)STAGES * SC * BC * KC * 8;
-constexpr size_t OFF_MAPS = OFF_CT + (size_t)BC * CP * 8;                // 2 x {colbase[BC], rowphys[BR]}
-constexpr size_t MAPS_BYTES = (size_t)BC * 8 + BR * 4;
+constexpr size_t OFF_MAPS = OFF_CT + (size_t)BC * CP * 8;  // 2 x {colbase[BC], rowphys[BR], cshift[BC]}
+constexpr size_t MAPS_BYTES = (size_t)BC * 8 + BR * 4 + BC * 4;
 constexpr size_t OFF_RUNS = OFF_MAPS + 2 * MAPS_BYTES;                   // producer scratch
 constexpr size_t OFF_BAR = OFF_RUNS + (size_t)(2 * BC + BR + 8) * 8;
 constexpr int MAX_SYM_CT = 1024;  // column tiles whose schedule fits in shared memory
 constexpr size_t OFF_SYM = OFF_BAR + 16 * 8;
 constexpr size_t SMEM = OFF_SYM + (size_t)(MAX_SYM_CT + MAX_SYM_CT / 16 + 4) * 4;
+static_assert(SMEM <= 232448 - 64, "ws kernel shared memory");
 }  // namespace ws
 
 __host__ __device__ __forceinline__ size_t wt_index(int row, int k, int mpad) {
@@ -339,6 +340,11 @@ struct UpdateWSArgs {
   const int* gprefix;
   int n_groups;
   int n_tiles;
+  // left-looking reuse: results go to cout (column-major [r-side][c-side],
+  // ld = ldo) instead of back into C (the pristine K panels)
+  double* cout;
+  long long ldo;
+  int mpad_c;  // rows per chunk of the c-side tiled buffer (0: same as mpad)
 };
 
 // tile id -> (r0, c0); false when the tile lies above the block diagonal.
@@ -404,6 +410,33 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
+// One 16-deep k-chunk of the consumer mainloop. The tiled layout rotates a
+// row's 4-double groups by (buffer row % 4). r-side smem rows are buffer rows
+// r0 + i (r0 % 4 == 0), so their rotation is (k4 + g). A c-side smem row i
+// holds buffer row cw[i]; when cw[i] != i (mod 4) (candidate blocks of
+// nt = 2 (mod 4) landing at shifted positions) SHIFT adds the per-row delta.
+template <bool SHIFT>
+__device__ __forceinline__ void ws_chunk(double (&acc)[4][4][2], const double* tR, const double* tC,
+                                         int g, int t, int wr, int wc, const int (&dsh)[4]) {
+  using namespace ws;
+  const double* bC = tC + (wc + g) * KC + t;
+  const double* bR = tR + (wr + g) * KC + t;
+#pragma unroll
+  for (int k4 = 0; k4 < KC / 4; ++k4) {
+    const int sw = ((k4 + g) & 3) << 2;
+    double fa[4], fb[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      fa[i] = SHIFT ? bC[i * 8 * KC + (((k4 + g + dsh[i]) & 3) << 2)] : bC[i * 8 * KC + sw];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) fb[j] = bR[j * 8 * KC + sw];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma884(acc[i][j], fa[i], fb[j]);
+  }
+}
+
 __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateWSArgs a) {
   using namespace ws;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -417,11 +450,16 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
   uint64_t* mempty = bars + 2 * STAGES + 2;  // [2]    consumers finished the tile's epilogue
   uint64_t* cempty = bars + 2 * STAGES + 4;  // [1]    consumers copied the C tile to registers
   __shared__ int s_tflag[2];  // per map buffer: 1 = a tile is ready, 0 = no more tiles
+  __shared__ int s_tile_r0[2], s_tile_c0[2];  // tile origin per map buffer (left-looking output)
+  __shared__ int s_cshift[2];                  // per map buffer: some c-side row has a rotation delta
   auto colbase_of = [&](int b) {
     return reinterpret_cast<long long*>(smem_raw + OFF_MAPS + b * MAPS_BYTES);
   };
   auto rowphys_of = [&](int b) {
     return reinterpret_cast<int*>(smem_raw + OFF_MAPS + b * MAPS_BYTES + BC * 8);
+  };
+  auto cshift_of = [&](int b) {
+    return reinterpret_cast<int*>(smem_raw + OFF_MAPS + b * MAPS_BYTES + BC * 8 + BR * 4);
   };
   int* cw = reinterpret_cast<int*>(smem_raw + OFF_RUNS);        // [BC] W row of each c column
   int* runs = cw + BC;                                          // row runs: start,len pairs
@@ -457,6 +495,7 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
   if (warp == CONSUMERS / 32) {
     // =============================== producer ===============================
     int* rrun = runs;            // [BR+1] row-run starts (then the end)
+    const int mpad_c = a.mpad_c ? a.mpad_c : a.mpad;
     int* crun = runs + BR + 1;   // [BC+1] c-side run starts (then the end)
     int stage = 0;
     unsigned ephase = 0;
@@ -468,9 +507,14 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
       const int ncv = min(BC, a.n_cols - c0);  // valid columns
       const int b = it & 1;
       if (it >= 2) mbar_wait(&mempty[b], ((it >> 1) - 1) & 1);
-      if (lane == 0) s_tflag[b] = 1;
+      if (lane == 0) {
+        s_tflag[b] = 1;
+        s_tile_r0[b] = r0;
+        s_tile_c0[b] = c0;
+      }
       long long* colbase = colbase_of(b);
       int* rowphys = rowphys_of(b);
+      int* cshift = cshift_of(b);
       int rp[BR / 32];
 #pragma unroll
       for (int m = 0; m < BR / 32; ++m) {
@@ -499,6 +543,14 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
           cwl[m] = 0;  // columns past the edge read W row 0 (never stored)
         }
         cw[i] = cwl[m];
+        cshift[i] = (cwl[m] - i) & 3;
+      }
+      {
+        bool any = false;
+#pragma unroll
+        for (int m = 0; m < BC / 32; ++m) any |= ((cwl[m] - lane - 32 * m) & 3) != 0;
+        any = __any_sync(0xffffffffu, any);
+        if (lane == 0) s_cshift[b] = any;
       }
       __syncwarp();
       // run starts via ballots: a run breaks where the source row is not the
@@ -567,7 +619,7 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
           const int c = q / ncr, qq = q - c * ncr;
           const int i0 = crun[qq], len = crun[qq + 1] - i0;
           bulk_g2s(sCc + (stage * SC + c) * BC * KC + i0 * KC,
-                   a.Wnt + ((size_t)(kb0 + c) * a.mpad + cw[i0]) * KC, (unsigned)len * KC * 8u,
+                   a.Wnt + ((size_t)(kb0 + c) * mpad_c + cw[i0]) * KC, (unsigned)len * KC * 8u,
                    &full[stage]);
         }
         if (++stage == STAGES) {
@@ -612,6 +664,13 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
       }
     __syncwarp();
     if (lane == 0) mbar_arrive(cempty);
+    const bool shifted = s_cshift[b];
+    int dsh[4];
+    {
+      const int* cs = cshift_of(b);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dsh[i] = shifted ? cs[wc + i * 8 + g] : 0;
+    }
     for (int kb0 = 0; kb0 < a.n_k; kb0 += SC) {
       const int sc = min(SC, a.n_k - kb0);
       mbar_wait(&full[stage], fphase);
@@ -620,23 +679,8 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
         if (c < sc) {
           const double* tR = sR + (stage * SC + c) * BR * KC;
           const double* tC = sCc + (stage * SC + c) * BC * KC;
-          // rows wc+8i+g / wr+8j+g are == g (mod 4): the swizzle offset only
-          // depends on (k4 + g), so each fragment is base + compile-time offset
-          const double* bC = tC + (wc + g) * KC + t;
-          const double* bR = tR + (wr + g) * KC + t;
-#pragma unroll
-          for (int k4 = 0; k4 < KC / 4; ++k4) {
-            const int sw = ((k4 + g) & 3) << 2;
-            double fa[4], fb[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) fa[i] = bC[i * 8 * KC + sw];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) fb[j] = bR[j * 8 * KC + sw];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-              for (int j = 0; j < 4; ++j) dmma884(acc[i][j], fa[i], fb[j]);
-          }
+          if (shifted) ws_chunk<true>(acc, tR, tC, g, t, wr, wc, dsh);
+          else ws_chunk<false>(acc, tR, tC, g, t, wr, wc, dsh);
         }
       }
       __syncwarp();
@@ -648,16 +692,33 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
     }
     const long long* colbase = colbase_of(b);
     const int* rowphys = rowphys_of(b);
+    if (a.cout) {
+      // left-looking: c[c-side row][r-side col] into the column-major output
+      const int r0o = s_tile_r0[b], c0o = s_tile_c0[b];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const long long cb = colbase[wc + i * 8 + g];
-      if (cb < 0) continue;
-      double* col = a.C + cb;
+      for (int i = 0; i < 4; ++i) {
+        if (colbase[wc + i * 8 + g] < 0) continue;
+        const int crow = c0o + wc + i * 8 + g;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int p0 = rowphys[wr + j * 8 + 2 * t];
-        if (p0 < 0) continue;
-        __stcs(reinterpret_cast<double2*>(col + p0), make_double2(acc[i][j][0], acc[i][j][1]));
+        for (int j = 0; j < 4; ++j) {
+          const int rl = wr + j * 8 + 2 * t;
+          if (rowphys[rl] < 0) continue;
+          a.cout[(size_t)(r0o + rl) * a.ldo + crow] = acc[i][j][0];
+          if (rowphys[rl + 1] >= 0) a.cout[(size_t)(r0o + rl + 1) * a.ldo + crow] = acc[i][j][1];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const long long cb = colbase[wc + i * 8 + g];
+        if (cb < 0) continue;
+        double* col = a.C + cb;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int p0 = rowphys[wr + j * 8 + 2 * t];
+          if (p0 < 0) continue;
+          __stcs(reinterpret_cast<double2*>(col + p0), make_double2(acc[i][j][0], acc[i][j][1]));
+        }
       }
     }
     __syncwarp();
@@ -884,8 +945,6 @@ __global__ void __launch_bounds__(llg::THREADS, 2) ll_gemm_kernel(LLGemmArgs a) 
   double* sA = reinterpret_cast<double*>(smem_raw);  // [STAGES][BM][LDK]
   double* sB = sA + STAGES * BM * LDK;                // [STAGES][BN][LDK]
   long long* kbase = reinterpret_cast<long long*>(sB + STAGES * BN * LDK);  // [BM] K panel column
-  int* arow = reinterpret_cast<int*>(kbase);           // reused? no: separate below
-  (void)arow;
   __shared__ int wrow[BM];
   const int tid = threadIdx.x;
   const int r0 = blockIdx.x * BM, c0 = blockIdx.y * BN;

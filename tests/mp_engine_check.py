@@ -22,6 +22,38 @@ torch.cuda.set_device(local)
 dist.init_process_group("gloo")
 nid = [d.nccl_unique_id() if rank == 0 else None]
 dist.broadcast_object_list(nid, src=0)
+if which == "random":
+    # reference random_hessian cases (odd nt, nt = 2 (mod 4): shifted c-side
+    # tiles) on every algorithm / storage variant; all ranks must agree
+    from oracle import oracle as O  # checker only
+    cases = json.load(open(os.path.join(ROOT, "tests", "golden", "random.json")))["cases"]
+    extra = [dict(n_sensors=40, n_steps=6, gamma=0.9, rank=150, seed=11, budget=12),
+             dict(n_sensors=33, n_steps=10, gamma=1.1, rank=200, seed=12, budget=9)]
+    bad = 0
+    for c in cases + extra:
+        nd, nt = c["n_sensors"], c["n_steps"]
+        k = O.random_hessian(nd, nt, c["gamma"], c["rank"], c["seed"])
+        if "chosen" not in c:
+            w = O.greedy_select(k, nd, nt, c["budget"])
+            c = dict(c, chosen=list(w.chosen), gains=list(w.gains))
+        for kw in (dict(), dict(full_square=True), dict(algorithm="left")):
+            cid = [d.nccl_unique_id() if rank == 0 else None]  # one id per communicator
+            dist.broadcast_object_list(cid, src=0)
+            eng = d.Engine(nd, nt, c["budget"], device=local, world_size=world, rank=rank,
+                           nccl_id=cid[0], **kw)
+            eng.load_k(k)
+            eng.run()
+            rows = eng.trace()
+            eng.close()
+            ok = [r["chosen_index"] for r in rows] == list(c["chosen"])
+            for r, g in zip(rows, c["gains"]):
+                ok = ok and abs(r["gain"] - g) <= 1e-9 * max(abs(g), 1.0)
+            if not ok:
+                bad += 1
+                print(f"rank {rank} MISMATCH nd={nd} nt={nt} {kw}", flush=True)
+    print(f"rank {rank}/{world} random: {'OK' if not bad else 'MISMATCH'}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(1 if bad else 0)
 gold = json.load(open(os.path.join(ROOT, "tests", "golden", f"{which}.json")))
 if which == "wave":
     from oracle import oracle as O  # checker only: parses the KBF fixture

@@ -317,6 +317,14 @@ def test_left_looking_random_and_subsets(dsel, O, golden_dir):
         rows = eng.trace()
         eng.close()
         assert_trace_matches(rows, c["chosen"], c["gains"], c["objectives"])
+    # nt = 2 (mod 4): own rows land in the update tile at shifted positions
+    for (nd, nt, rk, seed, B) in [(40, 6, 150, 11, 12), (33, 10, 200, 12, 9), (70, 2, 90, 3, 20)]:
+        k = O.random_hessian(nd, nt, 1.0, rk, seed)
+        want = O.greedy_select(k, nd, nt, B)
+        with dsel.Engine(nd, nt, B, algorithm="left") as eng:
+            eng.load_k(k)
+            eng.run()
+            assert_trace_matches(eng.trace(), want.chosen, want.gains, want.objectives)
     nd, nt = 14, 6
     k = O.random_hessian(nd, nt, 0.9, 60, 77)
     cands = [0, 2, 3, 5, 7, 8, 11, 13]
