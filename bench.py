@@ -170,12 +170,13 @@ def broadcast_bytes(b: bytes | None, world: int) -> bytes:
     return obj[0]
 
 
-def ncu_traffic(profile_dir: str):
+def ncu_traffic(profile_dir: str, algorithm: str):
     """dram bytes per update-kernel launch from a committed `ncu --set full`
-    capture summary (profiles/*update*_dram.json), else None."""
+    capture summary (profiles/*update_dram*<algorithm>*.json), else None."""
     import glob
 
-    for p in sorted(glob.glob(os.path.join(profile_dir, "*update*dram*.json")), reverse=True):
+    pat = "*update_dram_ll*.json" if algorithm == "left" else "*update_dram.json"
+    for p in sorted(glob.glob(os.path.join(profile_dir, pat)), reverse=True):
         try:
             return json.load(open(p))
         except Exception:
@@ -216,10 +217,13 @@ def time_device(eng, args, world, clock_dev=None):
     return out
 
 
-def time_e2e(eng, args, world, host_rows, mine, chosen):
-    """Same selection through the public API from pinned host memory: H2D of
-    this rank's block rows (dsel_load_block_row) + selection + D2H of the
-    result, wall clock, max over ranks."""
+def time_e2e(eng, args, world, host_rows, mine, chosen, attach=None):
+    """Same selection through the public API from pinned host memory, wall
+    clock, max over ranks. Resident store: H2D of this rank's block rows
+    (dsel_load_block_row) + selection + D2H of the result. attach (streaming
+    left-looking): dsel_attach_host_rows over the same pinned rows, then the
+    engine copies only the blocks each round reads (diagonal once, the chosen
+    column's own blocks per round) -- inside the timed region."""
     import numpy as np
 
     e2e_times, h2d, d2h = [], 0, 0
@@ -227,8 +231,11 @@ def time_e2e(eng, args, world, host_rows, mine, chosen):
         eng.reset()
         barrier(world)
         t0 = time.perf_counter()
-        for idx, j in enumerate(mine):
-            eng.load_block_row(j, host_rows[idx])
+        if attach is not None:
+            eng.attach_host_rows(attach)
+        else:
+            for idx, j in enumerate(mine):
+                eng.load_block_row(j, host_rows[idx])
         eng.run()
         rows = eng.trace()            # D2H of the selection result
         res = np.array([[r["chosen_index"], r["gain"]] for r in rows])
@@ -281,8 +288,24 @@ def our_arm(args, world, rank, local):
             hv[idx * row_elems:(idx + 1) * row_elems] = eng0.read_block_row(j)
         host_rows = [host[idx * row_elems:(idx + 1) * row_elems] for idx in range(len(mine))]
     for a in algos:
-        res[a]["e2e"] = None if args.no_e2e else time_e2e(engines[a], args, world, host_rows, mine,
-                                                          res[a]["chosen"])
+        if args.no_e2e:
+            res[a]["e2e"] = None
+        elif a == "left":
+            engines[a].close()
+            # K stays in host memory; the streaming engine reads what each round needs
+            nid = broadcast_bytes(d.nccl_unique_id() if (world > 1 and rank == 0) else None, world)
+            with d.Engine(nd, nt, budget, device=local, world_size=world, rank=rank, nccl_id=nid,
+                          export_factor=True, algorithm="left", storage=2) as es:
+                res[a]["e2e"] = time_e2e(es, args, world, host_rows, mine, res[a]["chosen"],
+                                         attach=host)
+                res[a]["e2e"]["path"] = ("dsel_attach_host_rows(pinned own block rows) + dsel_run "
+                                         "(streaming store: diagonal blocks once + the chosen "
+                                         "column's own blocks per round, copy stream overlapped "
+                                         "with the column GEMM) + trace D2H")
+        else:
+            res[a]["e2e"] = time_e2e(engines[a], args, world, host_rows, mine, res[a]["chosen"])
+            res[a]["e2e"]["path"] = ("dsel_load_block_row x own rows (pinned; H2D of the "
+                                     "block-lower half) + dsel_run + trace D2H")
         engines[a].close()
     prim = res[algos[0]]
     other = res[algos[1]] if len(algos) > 1 else None
@@ -295,7 +318,7 @@ def our_arm(args, world, rank, local):
     if want_cpu:
         cpu = cpu_reference(hv, nd, nt, budget, chosen)
 
-    tr = ncu_traffic(os.path.join(ROOT, "profiles"))
+    tr = ncu_traffic(os.path.join(ROOT, "profiles"), args.algorithm)
     traffic = tr.get("traffic_bytes_per_launch") if tr else None
     peak = FP64_DMMA_PEAK_TFLOPS
     line = {

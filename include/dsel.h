@@ -130,6 +130,19 @@ dsel_status dsel_load_block_col(dsel_engine* e, int j, const double* host_col);
 /* Whole K in DataSpaceHessian / KBF payload order (n_sensors^2 blocks,
  * block-row-major, hessian.hpp:17-84): loads every owned panel. */
 dsel_status dsel_load_k(dsel_engine* e, const double* host_k);
+/* Streaming store (storage = DSEL_STORAGE_STREAM) without a copy: the caller's
+ * whole K (dsel_load_k layout) stays in host memory and the engine reads, per
+ * round, only the blocks (i, k) of the chosen k for its own candidates i plus
+ * the diagonal blocks once -- what the reference reads through KAccess
+ * read_test_column / read_block (kaccess.hpp:27-35, selector.hpp:200-214).
+ * Pinned memory (cudaHostAlloc / registered) is used in place; pageable memory
+ * is registered read-only until dsel_destroy or the next load/attach. The
+ * buffer must outlive the selection. */
+dsel_status dsel_attach_host_k(dsel_engine* e, const double* host_k);
+/* Same over this rank's block rows only: the dsel_load_block_row rows of the
+ * candidates this rank owns (candidate positions p with p % world_size == rank),
+ * stacked in candidate order -- the per-rank shard of the KBF payload. */
+dsel_status dsel_attach_host_rows(dsel_engine* e, const double* host_rows);
 /* KBF store (`doptsel select <kbf>`, KStoreReader, kstore.hpp:22-186): validates
  * the header and size like KStoreReader (E_CORRUPT / E_IO) and loads this
  * rank's panels with parallel pread into pinned buffers, overlapped with the

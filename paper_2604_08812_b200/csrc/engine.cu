@@ -91,6 +91,11 @@ struct dsel_engine {
   // k's blocks are copied into Kk on the copy stream, overlapped with the GEMM
   bool stream = false;
   double *hstore = nullptr, *Kk = nullptr;
+  // dsel_attach_host_k: the caller's block-row-major K in (pinned) host
+  // memory is the store; blocks are read in place, only those a round needs
+  const double* hk_user = nullptr;
+  bool hk_rows = false;  // hk_user holds only this rank's block rows (slot order)
+  void* hk_registered = nullptr;  // cudaHostRegister'ed by the engine (pageable input)
   cudaEvent_t ev_kk0 = nullptr, ev_kk1 = nullptr;
   std::vector<int> streamed_round;  // rounds whose ev[5..7] are valid
   double *Wown = nullptr, *Wkn = nullptr, *D = nullptr, *cbuf = nullptr, *ldiag = nullptr,
@@ -431,8 +436,29 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
   if (e->stream && !last && e->nloc > 0) {
     // the chosen column's blocks for this rank's rows, on the copy stream
     CU(cudaEventRecord(ev[5], e->cs));
-    CU(cudaMemcpyAsync(e->Kk, e->hstore + (size_t)p * e->nloc * n2,
-                       sizeof(double) * (size_t)e->nloc * n2, cudaMemcpyHostToDevice, e->cs));
+    if (e->hk_user) {
+      // blocks (s_q, s_k) of the caller's K: one strided copy when the own
+      // slots are evenly spaced sensors (cyclic ownership of all sensors)
+      const int ks = e->pos_sensor[p];
+      const size_t row = (size_t)e->nd * n2;
+      auto rix = [&](int qq) { return e->hk_rows ? qq : e->slot_sensor[qq]; };
+      const int s0 = rix(0);
+      const int ds = e->nloc > 1 ? rix(1) - s0 : 1;
+      bool even = ds > 0;
+      for (int qq = 1; qq < e->nloc && even; ++qq) even = rix(qq) == s0 + qq * ds;
+      if (even) {
+        CU(cudaMemcpy2DAsync(e->Kk, sizeof(double) * n2, e->hk_user + (size_t)s0 * row + (size_t)ks * n2,
+                             sizeof(double) * row * ds, sizeof(double) * n2, e->nloc,
+                             cudaMemcpyHostToDevice, e->cs));
+      } else {
+        for (int qq = 0; qq < e->nloc; ++qq)
+          CU(cudaMemcpyAsync(e->Kk + (size_t)qq * n2, e->hk_user + (size_t)rix(qq) * row + (size_t)ks * n2,
+                             sizeof(double) * n2, cudaMemcpyHostToDevice, e->cs));
+      }
+    } else {
+      CU(cudaMemcpyAsync(e->Kk, e->hstore + (size_t)p * e->nloc * n2,
+                         sizeof(double) * (size_t)e->nloc * n2, cudaMemcpyHostToDevice, e->cs));
+    }
     CU(cudaEventRecord(ev[6], e->cs));
     e->streamed_round.push_back(round);
     e->h2d_bytes += (uint64_t)e->nloc * n2 * sizeof(double);
@@ -468,14 +494,14 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
   CU(cudaEventRecord(ev[3], e->s));
   if (!last && Rl > 0) {
     const int n_rows = Rl * nt;
-    if (!e->stream && nt % 2 == 0) {
+    if (nt % 2 == 0) {
       // the warp-specialized TMA update kernel, re-targeted: r-side = W_k
       // (c' rows), c-side = this rank's live rows of W_own, accumulators
       // start from K(own, k) (the pristine panels), output to cbuf
       *e->h_pk = p;
       CU(cudaMemcpyAsync(e->d_pk, e->h_pk, sizeof(int), cudaMemcpyHostToDevice, e->s));
       UpdateWSArgs ua{};
-      ua.C = e->C;
+      ua.C = e->stream ? nullptr : e->C;  // streaming: accumulate from 0, K added below
       ua.ldc = e->n;
       ua.Wt = e->Wkn;
       ua.Wnt = e->Wown;
@@ -498,6 +524,15 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
       const int grid = (int)std::min<long long>(e->n_sms, ua.n_tiles);
       schur_update_ws_kernel<<<grid, ws::THREADS, ws::SMEM, e->s>>>(ua);
       CU(cudaGetLastError());
+      if (e->stream) {
+        const long long total = (long long)nt * n_rows;
+        CU(cudaEventRecord(ev[7], e->s));
+        CU(cudaStreamWaitEvent(e->s, ev[6], 0));
+        ll_addk_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 8), 256, 0, e->s>>>(
+            nullptr, 0, 1, e->Kk, e->col_slot(), nt, n_rows, e->ldo, e->cbuf);
+        CU(cudaGetLastError());
+        e->launches += 1;
+      }
     } else {
       LLGemmArgs ga;
       ga.Wown = e->Wown;
@@ -589,6 +624,8 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   cudaEvent_t* ev = &e->ev[(size_t)round * kEv];
   const bool last = round + 1 == e->eff_budget;
 
+  if (e->stream && e->nloc > 0 && !e->hstore && !e->hk_user)
+    throw Fail{DSEL_E_STATE, "no K loaded (streaming store)"};
   // ---- gains + local argmax ----
   CU(cudaEventRecord(ev[0], e->s));
   if (e->stream && round == 0 && e->nloc > 0) {
@@ -596,9 +633,12 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
     // store block is row-major, D is column-major: equal for a symmetric block
     for (int qq = 0; qq < e->nloc; ++qq) {
       const int pq = qq * e->G + e->rank;
-      CU(cudaMemcpyAsync(e->D + (size_t)qq * nt * nt,
-                         e->hstore + ((size_t)pq * e->nloc + qq) * nt * nt,
-                         sizeof(double) * nt * nt, cudaMemcpyHostToDevice, e->s));
+      const int sq = e->slot_sensor[qq];
+      const double* src =
+          e->hk_user ? e->hk_user + ((size_t)(e->hk_rows ? qq : sq) * e->nd + sq) * nt * nt
+                     : e->hstore + ((size_t)pq * e->nloc + qq) * nt * nt;
+      CU(cudaMemcpyAsync(e->D + (size_t)qq * nt * nt, src, sizeof(double) * nt * nt,
+                         cudaMemcpyHostToDevice, e->s));
     }
     e->h2d_bytes += (uint64_t)e->nloc * nt * nt * sizeof(double);
   } else if (e->ll && round == 0 && e->nloc > 0) {
@@ -889,6 +929,7 @@ void destroy_impl(dsel_engine* e) {
   if (e->h_tab) cudaFreeHost(e->h_tab);
   if (e->h_sym) cudaFreeHost(e->h_sym);
   if (e->hstore) cudaFreeHost(e->hstore);
+  if (e->hk_registered) cudaHostUnregister(e->hk_registered);
   if (e->Kk) cudaFree(e->Kk);
   if (e->ev_kk0) cudaEventDestroy(e->ev_kk0);
   if (e->ev_kk1) cudaEventDestroy(e->ev_kk1);
@@ -1040,7 +1081,6 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     }
     if (e->C) CU(cudaMemsetAsync(e->C, 0, sizeof(double) * shard, e->s));
     if (e->stream) {
-      CU(cudaMallocHost(&e->hstore, sizeof(double) * (size_t)e->nc * std::max(e->nloc, 1) * e->nt * e->nt));
       e->Kk = dmalloc<double>((size_t)std::max(e->nloc, 1) * e->nt * e->nt, tot);
       CU(cudaEventCreate(&e->ev_kk0));
       CU(cudaEventCreate(&e->ev_kk1));
@@ -1086,8 +1126,21 @@ void ensure_stage(dsel_engine* e, size_t elems) {
 // Streaming store fill: block row j of an own candidate (as_column = false)
 // gives K(own_j, k) for every k; a block column j gives K(own_i, j) for every
 // own i (host-to-host copies into the pinned store).
+void ensure_hstore(dsel_engine* e) {
+  if (e->hk_registered) {
+    cudaHostUnregister(e->hk_registered);
+    e->hk_registered = nullptr;
+  }
+  e->hk_user = nullptr;  // loading data detaches a caller's K
+  if (!e->hstore) {
+    CU(cudaSetDevice(e->dev));
+    CU(cudaMallocHost(&e->hstore, sizeof(double) * (size_t)e->nc * std::max(e->nloc, 1) * e->nt * e->nt));
+  }
+}
+
 void store_fill(dsel_engine* e, int j, const double* host, bool as_column) {
   const size_t n2 = (size_t)e->nt * e->nt;
+  ensure_hstore(e);
   const int p = e->sensor_pos[j];
   if (p < 0) return;
   if (!as_column) {
@@ -1241,10 +1294,47 @@ dsel_status dsel_load_block_col(dsel_engine* e, int j, const double* host_col) {
   return guard(e, [&] { load_panel(e, j, host_col, true); });
 }
 
+void attach_host(dsel_engine* e, const double* host_k, bool rows) {
+  if (!e->stream) throw Fail{DSEL_E_INVALID, "attach_host_k needs storage = DSEL_STORAGE_STREAM"};
+  if (!host_k) throw Fail{DSEL_E_INVALID, "null K"};
+  CU(cudaSetDevice(e->dev));
+  if (e->hk_registered) {
+    cudaHostUnregister(e->hk_registered);
+    e->hk_registered = nullptr;
+  }
+  const size_t bytes = sizeof(double) * (size_t)(rows ? e->nloc : e->nd) * e->nd * e->nt * e->nt;
+  e->hk_user = nullptr;
+  if (bytes == 0) return;
+  cudaPointerAttributes at{};
+  const cudaError_t ae = cudaPointerGetAttributes(&at, host_k);
+  if (ae != cudaSuccess || at.type != cudaMemoryTypeHost) {
+    cudaGetLastError();
+    // pageable: pin in place (read-only) so the per-round copies are DMA
+    void* base = const_cast<double*>(host_k);
+    CU(cudaHostRegister(base, bytes, cudaHostRegisterReadOnly));
+    e->hk_registered = base;
+  }
+  if (e->hstore) {  // the caller's K replaces a filled store
+    cudaFreeHost(e->hstore);
+    e->hstore = nullptr;
+  }
+  e->hk_user = host_k;
+  e->hk_rows = rows;
+}
+
+dsel_status dsel_attach_host_k(dsel_engine* e, const double* host_k) {
+  return guard(e, [&] { attach_host(e, host_k, false); });
+}
+
+dsel_status dsel_attach_host_rows(dsel_engine* e, const double* host_rows) {
+  return guard(e, [&] { attach_host(e, host_rows, true); });
+}
+
 dsel_status dsel_load_k(dsel_engine* e, const double* host_k) {
   return guard(e, [&] {
     if (e->stream) {  // hstore[pk][q] = K(own_q, k): block (s_q, s_k) of the block-row-major K
       const size_t n2 = (size_t)e->nt * e->nt;
+      ensure_hstore(e);
       for (int pk = 0; pk < e->nc; ++pk)
         for (int q = 0; q < e->nloc; ++q)
           std::memcpy(e->hstore + ((size_t)pk * e->nloc + q) * n2,
@@ -1380,9 +1470,12 @@ dsel_status dsel_read_block_row(dsel_engine* e, int j, double* host_row) {
     if (e->stream) {  // K itself, from the pinned host store
       const size_t n2 = (size_t)e->nt * e->nt;
       std::memset(host_row, 0, elems * sizeof(double));
+      if (!e->hstore && !e->hk_user) throw Fail{DSEL_E_STATE, "no K loaded"};
       for (int pk = 0; pk < e->nc; ++pk)
         std::memcpy(host_row + (size_t)e->pos_sensor[pk] * n2,
-                    e->hstore + ((size_t)pk * e->nloc + q) * n2, n2 * sizeof(double));
+                    e->hk_user ? e->hk_user + ((size_t)(e->hk_rows ? q : j) * e->nd + e->pos_sensor[pk]) * n2
+                               : e->hstore + ((size_t)pk * e->nloc + q) * n2,
+                    n2 * sizeof(double));
       return;
     }
     CU(cudaSetDevice(e->dev));
@@ -1435,6 +1528,7 @@ dsel_status dsel_gen_synthetic(dsel_engine* e, const double* v_host, int rank, d
       // streaming store: one own panel at a time on the device, repacked to
       // [position][nt][nt] and copied into its slot of the pinned host store
       const size_t n2 = (size_t)e->nt * e->nt;
+      ensure_hstore(e);
       double* panel = nullptr;
       double* packed = nullptr;
       ce = cudaMalloc(&panel, sizeof(double) * (size_t)e->n * e->nt);

@@ -596,9 +596,13 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
       __syncwarp();
       // C tile -> sCt once consumers copied the previous tile to registers
       if (it >= 1) mbar_wait(cempty, (it - 1) & 1);
-      if (lane == 0) mbar_expect_tx(&tfull[b], (unsigned)(nrv * ncv) * 8u);
+      if (!a.C) {  // accumulate from zero (streaming left-looking: K added afterwards)
+        if (lane == 0) mbar_arrive(&tfull[b]);
+      } else {
+        if (lane == 0) mbar_expect_tx(&tfull[b], (unsigned)(nrv * ncv) * 8u);
+      }
       __syncwarp();
-      for (int p = lane; p < ncv * nrr; p += 32) {
+      for (int p = lane; a.C && p < ncv * nrr; p += 32) {
         const int c = p / nrr, q = p - c * nrr;
         const int i0 = rrun[q], len = rrun[q + 1] - i0;
         bulk_g2s(sCt + c * CP + i0, a.C + colbase[c] + rowphys[i0], (unsigned)len * 8u, &tfull[b]);
@@ -653,12 +657,14 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
     mbar_wait(&tfull[b], (it >> 1) & 1);
     if (!s_tflag[b]) break;  // the producer has no more tiles for this CTA
     double acc[4][4][2];
+    const bool cz = a.C == nullptr;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const double2 v =
-            *reinterpret_cast<const double2*>(sCt + (wc + i * 8 + g) * CP + wr + j * 8 + 2 * t);
+            cz ? make_double2(0.0, 0.0)
+               : *reinterpret_cast<const double2*>(sCt + (wc + i * 8 + g) * CP + wr + j * 8 + 2 * t);
         acc[i][j][0] = v.x;
         acc[i][j][1] = v.y;
       }

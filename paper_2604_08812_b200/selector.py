@@ -166,6 +166,19 @@ class Engine:
         """Whole K, block-row-major (DataSpaceHessian / KBF payload order)."""
         _check(lib.dsel_load_k(self.h, _host_ptr(k)), self.h)
 
+    def attach_host_k(self, k) -> None:
+        """Streaming store over the caller's K (same layout as load_k) in host
+        memory, read in place: per round only the chosen column's blocks for
+        this rank's candidates cross PCIe. The engine keeps a reference."""
+        _check(lib.dsel_attach_host_k(self.h, _host_ptr(k)), self.h)
+        self._hk = k
+
+    def attach_host_rows(self, rows) -> None:
+        """attach_host_k over this rank's own block rows only (candidates at
+        positions p % world_size == rank, stacked in candidate order)."""
+        _check(lib.dsel_attach_host_rows(self.h, _host_ptr(rows)), self.h)
+        self._hk = rows
+
     def load_kbf(self, path: str, exact_columns: bool = True, threads: int = 0) -> None:
         """KBF store (kstore.hpp:22-186) -> this engine's panels."""
         _check(lib.dsel_load_kbf(self.h, path.encode(), int(exact_columns), threads), self.h)

@@ -367,3 +367,41 @@ def test_streaming_store_matches_reference(dsel, O, golden_dir):
             eng.load_block_row(j, np.ascontiguousarray(kb[j]))
         eng.run()
         assert_trace_matches(eng.trace(), c["chosen"], c["gains"], c["objectives"])
+
+
+def test_streaming_attached_host_k(dsel, O, golden_dir):
+    """dsel_attach_host_k: the caller's K is the store (pageable -> registered in
+    place, or pinned); per round only the chosen column's own blocks cross PCIe."""
+    import torch
+
+    c1 = json.load(open(os.path.join(golden_dir, "c1.json")))
+    k = O.synthetic_k(64, 32, 2048, 1.0, 2024)          # pageable numpy
+    with dsel.Engine(64, 32, 16, algorithm="left", storage=2) as eng:
+        eng.attach_host_k(k)
+        eng.run()
+        rows = eng.trace()
+        st = eng.stats()
+    assert_trace_matches(rows, c1["chosen"], c1["gains"], c1["objectives"])
+    n2 = 32 * 32 * 8
+    want_bytes = 64 * n2 + 15 * 64 * n2                  # diagonal + one column per round
+    assert want_bytes <= st["h2d_bytes"] <= want_bytes + 4096
+    kp = torch.from_numpy(k).pin_memory()                # pinned: used in place
+    with dsel.Engine(64, 32, 16, algorithm="left", storage=2) as eng:
+        eng.attach_host_k(kp)
+        eng.run()
+        assert_trace_matches(eng.trace(), c1["chosen"], c1["gains"], c1["objectives"])
+        eng.reset()
+        eng.run()                                        # rerun over the same attached K
+        assert_trace_matches(eng.trace(), c1["chosen"], c1["gains"], c1["objectives"])
+    # candidate subset (uneven slot spacing) and nt = 2 (mod 4)
+    nd, nt = 30, 6
+    k = O.random_hessian(nd, nt, 1.0, 100, 21)
+    cands = [0, 1, 2, 4, 7, 8, 11, 13, 17, 18, 22, 25, 29]
+    want = O.greedy_select(k, nd, nt, 7, candidates=cands)
+    with dsel.Engine(nd, nt, 7, candidates=cands, algorithm="left", storage=2) as eng:
+        eng.attach_host_k(k)
+        eng.run()
+        assert_trace_matches(eng.trace(), want.chosen, want.gains, want.objectives)
+    with pytest.raises(dsel.InvalidConfig):
+        with dsel.Engine(8, 2, 2) as eng:
+            eng.attach_host_k(np.zeros(8 * 8 * 4))       # needs storage = stream
