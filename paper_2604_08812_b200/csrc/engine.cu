@@ -96,13 +96,11 @@ struct dsel_engine {
   const double* hk_user = nullptr;
   bool hk_rows = false;  // hk_user holds only this rank's block rows (slot order)
   void* hk_registered = nullptr;  // cudaHostRegister'ed by the engine (pageable input)
-  cudaEvent_t ev_kk0 = nullptr, ev_kk1 = nullptr;
+  cudaEvent_t ev_tab = nullptr;  // this round's table upload done (orders the column copy after it)
   std::vector<int> streamed_round;  // rounds whose ev[5..7] are valid
   double *Wown = nullptr, *Wkn = nullptr, *D = nullptr, *cbuf = nullptr, *ldiag = nullptr,
          *cpart = nullptr;
   int* d_iota = nullptr;
-  int* d_pk = nullptr;  // chosen position (left-looking row map of the re-targeted update)
-  int* h_pk = nullptr;  // pinned
   int own_mpad = 0, k_mpad = 0;
   long long ldo = 0;
   bool sym = true;  // block-lower-triangle (symmetric) update
@@ -358,6 +356,33 @@ void set_smem_limits(int dev) {
 
 constexpr int ws_group = 16;
 
+// Wave balancing for a persistent launch over n_tiles equal tiles of n_k
+// k-chunks: the first n_full tiles run whole, the rest are split into s
+// k-ranges. Picks (n_full, s) minimising the modelled time: waves of whole
+// tiles + the split tail + the partial-plane round trip (write + reduce).
+void ws_balance(int n_tiles, int n_k, int sms, int max_s, int& n_full, int& split_s) {
+  n_full = n_tiles;
+  split_s = 1;
+  if (max_s <= 1 || n_tiles <= 0 || n_k < 2) return;
+  const double t_chunk = 1.1e-6, t_tile0 = 2.0e-6;           // per k-chunk / per tile (s)
+  const double t_plane = (double)ws::BR * ws::BC * 8 * 2 / 6.0e12;  // partial write + read
+  const double t_full = n_k * t_chunk + t_tile0;
+  double best = ((n_tiles + sms - 1) / sms) * t_full;
+  for (int f = 0; f * sms < n_tiles; ++f) {
+    const int rem = n_tiles - f * sms;
+    for (int sp = 2; sp <= std::min(max_s, n_k); ++sp) {
+      const int units = rem * sp;
+      const double t = f * t_full + ((units + sms - 1) / sms) * ((double)n_k / sp * t_chunk + t_tile0) +
+                       (double)units * t_plane + 4e-6;
+      if (t < best * 0.98) {
+        best = t;
+        n_full = f * sms;
+        split_s = sp;
+      }
+    }
+  }
+}
+
 // Block-lower tile schedule of the update (symmetric storage): first needed row
 // tile per column tile and the tile-id prefix per 16-column-tile group.
 void sym_tables(dsel_engine* e) {
@@ -425,6 +450,32 @@ void launch_trinv(dsel_engine* e, const double* Lk) {
   e->launches += 1;
 }
 
+// Block (own slot qq, sensor col) of the caller-attached host K.
+const double* user_block(const dsel_engine* e, int qq, int col) {
+  const size_t n2 = (size_t)e->nt * e->nt;
+  const size_t r = e->hk_rows ? (size_t)qq : (size_t)e->slot_sensor[qq];
+  return e->hk_user + (r * e->nd + col) * n2;
+}
+
+// nloc host blocks src(qq) -> dst[qq] (nt x nt each): one strided 2-D copy
+// when the sources are evenly spaced (cyclic ownership), else one per block.
+template <class Src>
+void h2d_blocks(dsel_engine* e, double* dst, Src src, cudaStream_t st) {
+  const size_t n2b = sizeof(double) * e->nt * e->nt;
+  if (e->nloc == 0) return;
+  const char* b0 = reinterpret_cast<const char*>(src(0));
+  const long long d = e->nloc > 1 ? reinterpret_cast<const char*>(src(1)) - b0 : (long long)n2b;
+  bool even = d >= (long long)n2b && d < (1ll << 31);  // 2-D copy pitch limit
+  for (int qq = 2; qq < e->nloc && even; ++qq)
+    even = reinterpret_cast<const char*>(src(qq)) - b0 == (long long)qq * d;
+  if (even) {
+    CU(cudaMemcpy2DAsync(dst, n2b, b0, (size_t)d, n2b, e->nloc, cudaMemcpyHostToDevice, st));
+  } else {
+    for (int qq = 0; qq < e->nloc; ++qq)
+      CU(cudaMemcpyAsync(dst + (size_t)qq * e->nt * e->nt, src(qq), n2b, cudaMemcpyHostToDevice, st));
+  }
+}
+
 // Left-looking round tail: W_k + L_k from the owner, then this rank's rows of
 // the new conditional column, W_t, and the D (gain input) downdate.
 void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, const double* Lk,
@@ -433,36 +484,6 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
   const int nt = e->nt;
   const long long n2 = (long long)nt * nt;
   const int kcols = round * e->ldw;  // W_all columns so far
-  if (e->stream && !last && e->nloc > 0) {
-    // the chosen column's blocks for this rank's rows, on the copy stream
-    CU(cudaEventRecord(ev[5], e->cs));
-    if (e->hk_user) {
-      // blocks (s_q, s_k) of the caller's K: one strided copy when the own
-      // slots are evenly spaced sensors (cyclic ownership of all sensors)
-      const int ks = e->pos_sensor[p];
-      const size_t row = (size_t)e->nd * n2;
-      auto rix = [&](int qq) { return e->hk_rows ? qq : e->slot_sensor[qq]; };
-      const int s0 = rix(0);
-      const int ds = e->nloc > 1 ? rix(1) - s0 : 1;
-      bool even = ds > 0;
-      for (int qq = 1; qq < e->nloc && even; ++qq) even = rix(qq) == s0 + qq * ds;
-      if (even) {
-        CU(cudaMemcpy2DAsync(e->Kk, sizeof(double) * n2, e->hk_user + (size_t)s0 * row + (size_t)ks * n2,
-                             sizeof(double) * row * ds, sizeof(double) * n2, e->nloc,
-                             cudaMemcpyHostToDevice, e->cs));
-      } else {
-        for (int qq = 0; qq < e->nloc; ++qq)
-          CU(cudaMemcpyAsync(e->Kk + (size_t)qq * n2, e->hk_user + (size_t)rix(qq) * row + (size_t)ks * n2,
-                             sizeof(double) * n2, cudaMemcpyHostToDevice, e->cs));
-      }
-    } else {
-      CU(cudaMemcpyAsync(e->Kk, e->hstore + (size_t)p * e->nloc * n2,
-                         sizeof(double) * (size_t)e->nloc * n2, cudaMemcpyHostToDevice, e->cs));
-    }
-    CU(cudaEventRecord(ev[6], e->cs));
-    e->streamed_round.push_back(round);
-    e->h2d_bytes += (uint64_t)e->nloc * n2 * sizeof(double);
-  }
   if (owner == e->rank) {
     CU(cudaMemcpyAsync(e->ldiag + (size_t)round * n2, Lk, sizeof(double) * n2,
                        cudaMemcpyDeviceToDevice, e->s));
@@ -488,18 +509,36 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
   e->alive[p] = 0;
   e->n_alive -= 1;
   build_tables(e);
+  if (e->stream) CU(cudaEventRecord(e->ev_tab, e->s));
   const int Rl = e->n_cols_tab;
   double flops = 0.0;
   if (!last) launch_trinv(e, Lk);
   CU(cudaEventRecord(ev[3], e->s));
+  // H2D copies share the copy engine: the column copy waits for this round's
+  // table upload on e->s, which would otherwise queue behind it (~0.5 ms)
+  if (e->stream && !last && e->nloc > 0 && Rl > 0) {
+    // the chosen column's blocks for this rank's rows, on the copy stream
+    CU(cudaStreamWaitEvent(e->cs, e->ev_tab, 0));
+    CU(cudaEventRecord(ev[5], e->cs));
+    if (e->hk_user) {
+      // blocks (s_q, s_k) of the caller's K: one strided copy when the own
+      // slots are evenly spaced sensors (cyclic ownership of all sensors)
+      const int ks = e->pos_sensor[p];
+      h2d_blocks(e, e->Kk, [&](int qq) { return user_block(e, qq, ks); }, e->cs);
+    } else {
+      CU(cudaMemcpyAsync(e->Kk, e->hstore + (size_t)p * e->nloc * n2,
+                         sizeof(double) * (size_t)e->nloc * n2, cudaMemcpyHostToDevice, e->cs));
+    }
+    CU(cudaEventRecord(ev[6], e->cs));
+    e->streamed_round.push_back(round);
+    e->h2d_bytes += (uint64_t)e->nloc * n2 * sizeof(double);
+  }
   if (!last && Rl > 0) {
     const int n_rows = Rl * nt;
     if (nt % 2 == 0) {
       // the warp-specialized TMA update kernel, re-targeted: r-side = W_k
       // (c' rows), c-side = this rank's live rows of W_own, accumulators
       // start from K(own, k) (the pristine panels), output to cbuf
-      *e->h_pk = p;
-      CU(cudaMemcpyAsync(e->d_pk, e->h_pk, sizeof(int), cudaMemcpyHostToDevice, e->s));
       UpdateWSArgs ua{};
       ua.C = e->stream ? nullptr : e->C;  // streaming: accumulate from 0, K added below
       ua.ldc = e->n;
@@ -507,7 +546,8 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
       ua.Wnt = e->Wown;
       ua.mpad = e->k_mpad;
       ua.n_k = kcols / 16;
-      ua.row_pos = e->d_pk;          // single "block": p_k -> rows p_k*nt + c'
+      ua.row_pos = nullptr;          // single "block": p_k -> rows p_k*nt + c'
+      ua.row_pos_k = p;
       ua.col_slot = e->col_slot();
       ua.col_g = e->col_slot();      // c-side W rows are slot*nt + off
       ua.nt = nt;
@@ -521,9 +561,21 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
       ua.cout = e->cbuf;
       ua.ldo = e->ldo;
       ua.mpad_c = e->own_mpad;
-      const int grid = (int)std::min<long long>(e->n_sms, ua.n_tiles);
+      // wave balancing: the tiles past the last full wave are split along k
+      ws_balance(ua.n_tiles, ua.n_k, e->n_sms, e->cpart ? kLLMaxSplits : 1, ua.n_full, ua.split_s);
+      ua.part = e->cpart;
+      ua.part_stride = (long long)e->ldo * nt;
+      const int n_units = ua.n_full + (ua.n_tiles - ua.n_full) * ua.split_s;
+      const int grid = std::min(e->n_sms, n_units);
       schur_update_ws_kernel<<<grid, ws::THREADS, ws::SMEM, e->s>>>(ua);
       CU(cudaGetLastError());
+      if (ua.split_s > 1) {
+        const long long total = (long long)(ua.n_tiles - ua.n_full) * ws::BR * ws::BC;
+        ws_split_reduce_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 8), 256, 0,
+                                 e->s>>>(ua);
+        CU(cudaGetLastError());
+        e->launches += 1;
+      }
       if (e->stream) {
         const long long total = (long long)nt * n_rows;
         CU(cudaEventRecord(ev[7], e->s));
@@ -631,15 +683,10 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   if (e->stream && round == 0 && e->nloc > 0) {
     // D[q] = K(own_q, own_q)^T = K(own_q, own_q) (symmetric), from the host store;
     // store block is row-major, D is column-major: equal for a symmetric block
-    for (int qq = 0; qq < e->nloc; ++qq) {
-      const int pq = qq * e->G + e->rank;
-      const int sq = e->slot_sensor[qq];
-      const double* src =
-          e->hk_user ? e->hk_user + ((size_t)(e->hk_rows ? qq : sq) * e->nd + sq) * nt * nt
-                     : e->hstore + ((size_t)pq * e->nloc + qq) * nt * nt;
-      CU(cudaMemcpyAsync(e->D + (size_t)qq * nt * nt, src, sizeof(double) * nt * nt,
-                         cudaMemcpyHostToDevice, e->s));
-    }
+    h2d_blocks(e, e->D, [&](int qq) {
+      return e->hk_user ? user_block(e, qq, e->slot_sensor[qq])
+                        : e->hstore + ((size_t)(qq * e->G + e->rank) * e->nloc + qq) * nt * nt;
+    }, e->s);
     e->h2d_bytes += (uint64_t)e->nloc * nt * nt * sizeof(double);
   } else if (e->ll && round == 0 && e->nloc > 0) {
     const long long total = (long long)e->nloc * nt * nt;
@@ -839,6 +886,8 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       ua.gprefix = e->d_sym + ua.n_col_tiles;
       ua.n_groups = (ua.n_col_tiles + ws_group - 1) / ws_group;
       ua.n_tiles = e->sym ? e->sym_tiles : ua.n_row_tiles * ua.n_col_tiles;
+      ua.n_full = ua.n_tiles;
+      ua.split_s = 1;
       const int grid = (int)std::min<long long>(e->n_sms, ua.n_tiles);
       schur_update_ws_kernel<<<grid, ws::THREADS, ws::SMEM, e->s>>>(ua);
     } else {
@@ -919,8 +968,7 @@ void destroy_impl(dsel_engine* e) {
                     e->kgain, e->stage, e->xbuf};
   for (double* d : dptr)
     if (d) cudaFree(d);
-  int* iptr[] = {e->status, e->kstatus, e->d_pos_sensor, e->d_slot_sensor, e->d_tab, e->d_sym, e->d_iota, e->d_pk};
-  if (e->h_pk) cudaFreeHost(e->h_pk);
+  int* iptr[] = {e->status, e->kstatus, e->d_pos_sensor, e->d_slot_sensor, e->d_tab, e->d_sym, e->d_iota};
   for (int* d : iptr)
     if (d) cudaFree(d);
   if (e->d_rec) cudaFree(e->d_rec);
@@ -931,8 +979,7 @@ void destroy_impl(dsel_engine* e) {
   if (e->hstore) cudaFreeHost(e->hstore);
   if (e->hk_registered) cudaHostUnregister(e->hk_registered);
   if (e->Kk) cudaFree(e->Kk);
-  if (e->ev_kk0) cudaEventDestroy(e->ev_kk0);
-  if (e->ev_kk1) cudaEventDestroy(e->ev_kk1);
+  if (e->ev_tab) cudaEventDestroy(e->ev_tab);
   if (e->h_stage) cudaFreeHost(e->h_stage);
   if (e->comm) ncclCommDestroy(e->comm);
   for (int b = 0; b < 2; ++b) {
@@ -1037,12 +1084,12 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
       {
         const int max_nk = (B * e->ldw) / 16;
         const int ns = std::max(1, std::min(kLLMaxSplits, (max_nk + kLLSplitChunks - 1) / kLLSplitChunks));
-        if (ns > 1) e->cpart = dmalloc<double>((size_t)ns * e->ldo * e->nt, tot);
+        // split-K planes: odd-nt GEMM (ns) / wave-balanced TMA GEMM (kLLMaxSplits)
+        const int np = e->nt % 2 ? ns : kLLMaxSplits;
+        if (np > 1) e->cpart = dmalloc<double>((size_t)np * e->ldo * e->nt, tot);
       }
       e->ldiag = dmalloc<double>((size_t)B * e->nt * e->nt, tot);
       e->d_iota = dmalloc<int>(std::max(e->nloc, 1), tot);
-      e->d_pk = dmalloc<int>(1, tot);
-      CU(cudaMallocHost(&e->h_pk, sizeof(int)));
       std::vector<int> iota(std::max(e->nloc, 1));
       for (size_t i = 0; i < iota.size(); ++i) iota[i] = (int)i;
       CU(cudaMemcpy(e->d_iota, iota.data(), sizeof(int) * iota.size(), cudaMemcpyHostToDevice));
@@ -1082,8 +1129,7 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     if (e->C) CU(cudaMemsetAsync(e->C, 0, sizeof(double) * shard, e->s));
     if (e->stream) {
       e->Kk = dmalloc<double>((size_t)std::max(e->nloc, 1) * e->nt * e->nt, tot);
-      CU(cudaEventCreate(&e->ev_kk0));
-      CU(cudaEventCreate(&e->ev_kk1));
+      CU(cudaEventCreateWithFlags(&e->ev_tab, cudaEventDisableTiming));
     }
     CU(cudaMemcpyAsync(e->d_pos_sensor, e->pos_sensor.data(), sizeof(int) * e->nc,
                        cudaMemcpyHostToDevice, e->s));

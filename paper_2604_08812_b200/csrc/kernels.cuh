@@ -326,7 +326,8 @@ struct UpdateWSArgs {
   const double* Wnt;  // -W tiled (c-side)
   int mpad;           // rows of the tiled buffers (multiple of BR)
   int n_k;            // k-chunks (ldw / 16)
-  const int* row_pos;
+  const int* row_pos;  // nullptr: every r-side row is in block row_pos_k
+  int row_pos_k;
   const int* col_slot;
   const int* col_g;
   int nt;
@@ -345,7 +346,32 @@ struct UpdateWSArgs {
   double* cout;
   long long ldo;
   int mpad_c;  // rows per chunk of the c-side tiled buffer (0: same as mpad)
+  // wave balancing (left-looking output only): tiles [0, n_full) run whole;
+  // each tile >= n_full is split into split_s k-ranges (units), unit z
+  // writes its partial to part + z * part_stride (cout layout), split 0
+  // carrying the C init; ws_split_reduce_kernel sums them in z order.
+  // Host default: n_full = n_tiles, split_s = 1 (no split units).
+  int n_full, split_s;
+  double* part;
+  long long part_stride;
 };
+
+// unit -> (tile, split z, k-chunk range)
+__device__ __forceinline__ void ws_unit(const UpdateWSArgs& a, int unit, int& tile, int& z, int& kb_lo,
+                                        int& kb_hi) {
+  if (unit < a.n_full) {
+    tile = unit;
+    z = -1;
+    kb_lo = 0;
+    kb_hi = a.n_k;
+    return;
+  }
+  const int v = unit - a.n_full;
+  tile = a.n_full + v / a.split_s;
+  z = v - (v / a.split_s) * a.split_s;
+  kb_lo = (int)((long long)a.n_k * z / a.split_s);
+  kb_hi = (int)((long long)a.n_k * (z + 1) / a.split_s);
+}
 
 // tile id -> (r0, c0); false when the tile lies above the block diagonal.
 // fr / gp: first_rt and gprefix staged in shared memory (binary search).
@@ -452,6 +478,7 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
   __shared__ int s_tflag[2];  // per map buffer: 1 = a tile is ready, 0 = no more tiles
   __shared__ int s_tile_r0[2], s_tile_c0[2];  // tile origin per map buffer (left-looking output)
   __shared__ int s_cshift[2];                  // per map buffer: some c-side row has a rotation delta
+  __shared__ int s_tile_z[2], s_tile_nk[2];    // split index (-1: whole tile) and k-chunk count
   auto colbase_of = [&](int b) {
     return reinterpret_cast<long long*>(smem_raw + OFF_MAPS + b * MAPS_BYTES);
   };
@@ -464,7 +491,7 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
   int* cw = reinterpret_cast<int*>(smem_raw + OFF_RUNS);        // [BC] W row of each c column
   int* runs = cw + BC;                                          // row runs: start,len pairs
   const int nt = a.nt;
-  const int n_tiles = a.n_tiles;
+  const int n_units = a.n_full + (a.n_tiles - a.n_full) * a.split_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // tile schedule (symmetric mode) in shared memory
@@ -500,9 +527,11 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
     int stage = 0;
     unsigned ephase = 0;
     int it = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      int r0, c0;
+    for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
+      int r0, c0, tile, uz, kb_lo, kb_hi;
+      ws_unit(a, unit, tile, uz, kb_lo, kb_hi);
       if (!ws_tile(a, fr, gp, tile, r0, c0)) continue;
+      const bool cinit = a.C && uz <= 0;  // split units > 0 start from zero
       const int nrv = min(BR, a.n_rows - r0);  // valid rows of the tile
       const int ncv = min(BC, a.n_cols - c0);  // valid columns
       const int b = it & 1;
@@ -511,6 +540,8 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
         s_tflag[b] = 1;
         s_tile_r0[b] = r0;
         s_tile_c0[b] = c0;
+        s_tile_z[b] = uz;
+        s_tile_nk[b] = kb_hi - kb_lo;
       }
       long long* colbase = colbase_of(b);
       int* rowphys = rowphys_of(b);
@@ -522,7 +553,7 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
         const int r = r0 + i;
         if (i < nrv) {
           const int blk = r / nt;
-          rp[m] = a.row_pos[blk] * nt + (r - blk * nt);
+          rp[m] = (a.row_pos ? a.row_pos[blk] : a.row_pos_k) * nt + (r - blk * nt);
         } else {
           rp[m] = -1;
         }
@@ -596,21 +627,21 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
       __syncwarp();
       // C tile -> sCt once consumers copied the previous tile to registers
       if (it >= 1) mbar_wait(cempty, (it - 1) & 1);
-      if (!a.C) {  // accumulate from zero (streaming left-looking: K added afterwards)
+      if (!cinit) {  // accumulate from zero (streaming left-looking: K added afterwards)
         if (lane == 0) mbar_arrive(&tfull[b]);
       } else {
         if (lane == 0) mbar_expect_tx(&tfull[b], (unsigned)(nrv * ncv) * 8u);
       }
       __syncwarp();
-      for (int p = lane; a.C && p < ncv * nrr; p += 32) {
+      for (int p = lane; cinit && p < ncv * nrr; p += 32) {
         const int c = p / nrr, q = p - c * nrr;
         const int i0 = rrun[q], len = rrun[q + 1] - i0;
         bulk_g2s(sCt + c * CP + i0, a.C + colbase[c] + rowphys[i0], (unsigned)len * 8u, &tfull[b]);
       }
       // operand k-chunks, SC per stage: r-side one contiguous tile per chunk,
       // c-side one copy per run per chunk
-      for (int kb0 = 0; kb0 < a.n_k; kb0 += SC) {
-        const int sc = min(SC, a.n_k - kb0);
+      for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += SC) {
+        const int sc = min(SC, kb_hi - kb0);
         if (lane == 0) {
           mbar_wait(&empty[stage], ephase ^ 1);
           mbar_expect_tx(&full[stage], (unsigned)(sc * (BR + BC) * KC * 8));
@@ -657,7 +688,8 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
     mbar_wait(&tfull[b], (it >> 1) & 1);
     if (!s_tflag[b]) break;  // the producer has no more tiles for this CTA
     double acc[4][4][2];
-    const bool cz = a.C == nullptr;
+    const int uz = s_tile_z[b], unk = s_tile_nk[b];
+    const bool cz = a.C == nullptr || uz > 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -677,8 +709,8 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
 #pragma unroll
       for (int i = 0; i < 4; ++i) dsh[i] = shifted ? cs[wc + i * 8 + g] : 0;
     }
-    for (int kb0 = 0; kb0 < a.n_k; kb0 += SC) {
-      const int sc = min(SC, a.n_k - kb0);
+    for (int kb0 = 0; kb0 < unk; kb0 += SC) {
+      const int sc = min(SC, unk - kb0);
       mbar_wait(&full[stage], fphase);
 #pragma unroll
       for (int c = 0; c < SC; ++c) {
@@ -700,7 +732,9 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
     const int* rowphys = rowphys_of(b);
     if (a.cout) {
       // left-looking: c[c-side row][r-side col] into the column-major output
+      // (split units: their partial plane)
       const int r0o = s_tile_r0[b], c0o = s_tile_c0[b];
+      double* const out = uz < 0 ? a.cout : a.part + (size_t)uz * a.part_stride;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         if (colbase[wc + i * 8 + g] < 0) continue;
@@ -709,8 +743,8 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
         for (int j = 0; j < 4; ++j) {
           const int rl = wr + j * 8 + 2 * t;
           if (rowphys[rl] < 0) continue;
-          a.cout[(size_t)(r0o + rl) * a.ldo + crow] = acc[i][j][0];
-          if (rowphys[rl + 1] >= 0) a.cout[(size_t)(r0o + rl + 1) * a.ldo + crow] = acc[i][j][1];
+          out[(size_t)(r0o + rl) * a.ldo + crow] = acc[i][j][0];
+          if (rowphys[rl + 1] >= 0) out[(size_t)(r0o + rl + 1) * a.ldo + crow] = acc[i][j][1];
         }
       }
     } else {
@@ -730,6 +764,29 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
     __syncwarp();
     if (lane == 0) mbar_arrive(&mempty[b]);
     ++it;
+  }
+}
+
+// Split units of the balanced left-looking GEMM: cout = sum_z part_z over
+// the tiles >= n_full, z in order (deterministic for a given rank count).
+__global__ void ws_split_reduce_kernel(UpdateWSArgs a) {
+  using namespace ws;
+  const int n_split_tiles = a.n_tiles - a.n_full;
+  const long long per = (long long)BR * BC;
+  const long long total = per * n_split_tiles;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int tl = (int)(e / per);
+    const int w = (int)(e - (long long)tl * per);
+    const int cl = w % BC, rl = w / BC;  // consecutive threads: consecutive c (contiguous in cout)
+    int r0, c0;
+    ws_tile(a, nullptr, nullptr, a.n_full + tl, r0, c0);
+    const int r = r0 + rl, c = c0 + cl;
+    if (r >= a.n_rows || c >= a.n_cols) continue;
+    const size_t o = (size_t)r * a.ldo + c;
+    double v = a.part[o];
+    for (int z = 1; z < a.split_s; ++z) v += a.part[(size_t)z * a.part_stride + o];
+    a.cout[o] = v;
   }
 }
 
