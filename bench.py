@@ -473,9 +473,10 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--algorithm", default="left", choices=["right", "left"],
-                    help="primary line (left: fewest flops, fastest time-to-k; right: the "
-                         "resident conditional-covariance update, measured as the variant)")
+    ap.add_argument("--algorithm", default="right", choices=["right", "left"],
+                    help="primary line (right = the north-star resident conditional-covariance "
+                         "Schur update; the left-looking variant (SURVEY 8f row 1) is reported "
+                         "beside it in the same line under 'variant')")
     ap.add_argument("--no-variants", action="store_true",
                     help="skip measuring the other algorithm beside the primary")
     args = ap.parse_args()
