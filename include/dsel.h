@@ -143,6 +143,14 @@ dsel_status dsel_attach_host_k(dsel_engine* e, const double* host_k);
  * candidates this rank owns (candidate positions p with p % world_size == rank),
  * stacked in candidate order -- the per-rank shard of the KBF payload. */
 dsel_status dsel_attach_host_rows(dsel_engine* e, const double* host_rows);
+/* K = sigma^2 I + V V^T formed on the device for scales where V (n x rank)
+ * cannot be materialized on the host. V[i][r] ~ N(0,1) from
+ * a counter-based Philox4x32-10 stream keyed by (seed, global row, r/2) with
+ * Box-Muller -- NOT the reference RNG stream, so the K differs from
+ * SyntheticKAccess; it is identical for every world_size. Accumulated by the
+ * Schur update kernel (W = +V, 512 rank columns per launch; block-lower tiles
+ * only under symmetric storage). HBM store only; n_steps even. */
+dsel_status dsel_gen_synthetic_device(dsel_engine* e, int rank, double sigma, uint64_t seed);
 /* KBF store (`doptsel select <kbf>`, KStoreReader, kstore.hpp:22-186): validates
  * the header and size like KStoreReader (E_CORRUPT / E_IO) and loads this
  * rank's panels with parallel pread into pinned buffers, overlapped with the

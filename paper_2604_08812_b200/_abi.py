@@ -20,7 +20,7 @@ STATUS_NAMES = {0: "DSEL_OK", 1: "DSEL_E_INVALID", 2: "DSEL_E_RANGE", 3: "DSEL_E
 EXPORTS = ["dsel_abi_version", "dsel_fold_records", "dsel_nccl_unique_id", "dsel_create", "dsel_destroy",
            "dsel_last_error", "dsel_sync", "dsel_device_bytes", "dsel_load_block_row",
            "dsel_load_block_col", "dsel_load_k", "dsel_attach_host_k", "dsel_attach_host_rows", "dsel_load_kbf", "dsel_read_block_row", "dsel_synthetic_v",
-           "dsel_gen_synthetic", "dsel_step", "dsel_step_forced", "dsel_run", "dsel_peek_gains",
+           "dsel_gen_synthetic", "dsel_gen_synthetic_device", "dsel_step", "dsel_step_forced", "dsel_run", "dsel_peek_gains",
            "dsel_get_trace", "dsel_reset", "dsel_get_stats", "dsel_export_factor"]
 
 
@@ -84,6 +84,7 @@ def _load():
     L.dsel_load_block_col.argtypes = [vp, C.c_int, vp]
     L.dsel_load_k.argtypes = [vp, vp]
     L.dsel_attach_host_k.argtypes = [vp, vp]
+    L.dsel_gen_synthetic_device.argtypes = [vp, C.c_int, C.c_double, C.c_uint64]
     L.dsel_attach_host_rows.argtypes = [vp, vp]
     L.dsel_load_kbf.argtypes = [vp, C.c_char_p, C.c_int, C.c_int]
     L.dsel_read_block_row.argtypes = [vp, C.c_int, vp]

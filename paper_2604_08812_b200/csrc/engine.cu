@@ -108,6 +108,7 @@ struct dsel_engine {
   int* d_sym = nullptr;  // [first_rt per column tile | group prefix]
   int* h_sym = nullptr;  // pinned
   int sym_tiles = 0;
+  double gen_flops = 0.0;  // last dsel_gen_synthetic_device (K formation on the update kernel)
   bool keep = false, export_factor = false;
   double tau = 1e-9;
   std::vector<int> pos_sensor, sensor_pos, slot_sensor;
@@ -1609,6 +1610,77 @@ dsel_status dsel_gen_synthetic(dsel_engine* e, const double* v_host, int rank, d
     cudaFree(V);
     if (ce != cudaSuccess) throw Fail{DSEL_E_CUDA, std::string("synthetic K: ") + cudaGetErrorString(ce)};
     e->full_panels = true;
+    if (e->keep && e->C)
+      CU(cudaMemcpyAsync(e->K0, e->C, sizeof(double) * e->n * e->nloc * e->nt,
+                         cudaMemcpyDeviceToDevice, e->s));
+    CU(cudaStreamSynchronize(e->s));
+  });
+}
+
+dsel_status dsel_gen_synthetic_device(dsel_engine* e, int rank, double sigma, uint64_t seed) {
+  return guard(e, [&] {
+    if (rank < 1) throw Fail{DSEL_E_INVALID, "bad synthetic rank"};
+    if (e->stream) throw Fail{DSEL_E_INVALID, "gen_synthetic_device fills the HBM panel store"};
+    if (e->nt % 2) throw Fail{DSEL_E_INVALID, "gen_synthetic_device needs an even n_steps"};
+    if (!e->trace.empty()) throw Fail{DSEL_E_STATE, "gen_synthetic_device after selection started"};
+    CU(cudaSetDevice(e->dev));
+    const int nt = e->nt;
+    build_tables(e);
+    const int R = e->n_rows_tab, Rl = e->n_cols_tab;
+    const int n_rows = R * nt, n_cols = Rl * nt;
+    const bool sym = e->sym;
+    if (sym) sym_tables(e);
+    CU(cudaMemsetAsync(e->C, 0, sizeof(double) * e->n * e->nloc * nt, e->s));
+    if (e->nloc > 0) {
+      const long long total = (long long)e->nloc * nt;
+      add_diag_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 1024), 256, 0, e->s>>>(
+          e->C, e->n, nt, e->nloc, e->G, e->rank, sigma * sigma);
+      CU(cudaGetLastError());
+    }
+    constexpr int kch = 512;  // rank columns per update launch
+    const int mpad = round_up(std::max(n_rows, 1), ws::BR);
+    double* Vt = nullptr;
+    CU(cudaMalloc(&Vt, sizeof(double) * (size_t)mpad * kch));
+    cudaError_t ce = cudaSuccess;
+    double gen_flops = 0.0;
+    for (int k0 = 0; k0 < rank && ce == cudaSuccess && Rl > 0; k0 += kch) {
+      const long long total = (long long)mpad * (kch / 2);
+      gen_v_tiled_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 32), 256, 0, e->s>>>(
+          Vt, mpad, kch, k0, rank, e->row_pos(), e->d_pos_sensor, n_rows, nt, (unsigned long long)seed);
+      // C += V V^T: the update kernel with W = +V on both sides
+      UpdateWSArgs ua{};
+      ua.C = e->C;
+      ua.ldc = e->n;
+      ua.Wt = Vt;
+      ua.Wnt = Vt;
+      ua.mpad = mpad;
+      ua.n_k = kch / ws::KC;
+      ua.row_pos = e->row_pos();
+      ua.col_slot = e->col_slot();
+      ua.col_g = e->col_g();
+      ua.nt = nt;
+      ua.n_rows = n_rows;
+      ua.n_cols = n_cols;
+      ua.n_row_tiles = (n_rows + ws::BR - 1) / ws::BR;
+      ua.n_col_tiles = (n_cols + ws::BC - 1) / ws::BC;
+      ua.group = ws_group;
+      ua.sym = sym;
+      ua.first_rt = e->d_sym;
+      ua.gprefix = sym ? e->d_sym + ua.n_col_tiles : nullptr;
+      ua.n_groups = (ua.n_col_tiles + ws_group - 1) / ws_group;
+      ua.n_tiles = sym ? e->sym_tiles : ua.n_row_tiles * ua.n_col_tiles;
+      ua.n_full = ua.n_tiles;
+      ua.split_s = 1;
+      const int grid = (int)std::min<long long>(e->n_sms, ua.n_tiles);
+      schur_update_ws_kernel<<<grid, ws::THREADS, ws::SMEM, e->s>>>(ua);
+      ce = cudaGetLastError();
+      gen_flops += 2.0 * kch * (sym ? 0.5 * (double)n_rows * (n_cols + nt) : (double)n_rows * n_cols);
+    }
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(e->s);
+    cudaFree(Vt);
+    if (ce != cudaSuccess) throw Fail{DSEL_E_CUDA, std::string("device synthetic K: ") + cudaGetErrorString(ce)};
+    e->gen_flops = gen_flops;
+    e->full_panels = !sym;
     if (e->keep && e->C)
       CU(cudaMemcpyAsync(e->K0, e->C, sizeof(double) * e->n * e->nloc * e->nt,
                          cudaMemcpyDeviceToDevice, e->s));

@@ -1813,6 +1813,87 @@ namespace gen {
 constexpr int BM = 64, BN = 64, KT = 16, THREADS = 256;
 }
 
+// ------------------------------------------------------------------------ //
+// Device-side synthetic K for scales where V cannot live on the host         //
+// (C4/C5, V = 165 GB at rank 81,920). V[i][r] ~ N(0,1) from a    //
+// counter-based Philox4x32-10 stream keyed by (seed, global row i, r/2) and   //
+// Box-Muller, so any rank regenerates any rows. NOT the reference RNG stream  //
+// (glibc libm bits are not reproducible on the device): parity at this scale  //
+// is GPU-vs-oracle on the K the GPU formed (read back), as 8(d) prescribes.   //
+// K = sigma^2 I + V V^T is accumulated by the Schur update kernel itself      //
+// (W = +V chunks, same tile schedule), 512 rank columns per launch.           //
+// ------------------------------------------------------------------------ //
+__host__ __device__ __forceinline__ void philox4x32_10(unsigned (&c)[4], unsigned k0, unsigned k1) {
+  for (int r = 0; r < 10; ++r) {
+    const unsigned long long p0 = 0xD2511F53ull * c[0], p1 = 0xCD9E8D57ull * c[2];
+    const unsigned hi0 = (unsigned)(p0 >> 32), lo0 = (unsigned)p0;
+    const unsigned hi1 = (unsigned)(p1 >> 32), lo1 = (unsigned)p1;
+    const unsigned n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+// two N(0,1) values for columns (2*cp, 2*cp+1) of global row gi
+__host__ __device__ __forceinline__ void philox_normal2(unsigned long long seed, long long gi, long long cp,
+                                                        double& z0, double& z1) {
+  unsigned c[4] = {(unsigned)gi, (unsigned)((unsigned long long)gi >> 32), (unsigned)cp,
+                   (unsigned)((unsigned long long)cp >> 32)};
+  philox4x32_10(c, (unsigned)seed, (unsigned)(seed >> 32));
+  const unsigned long long a = ((unsigned long long)c[0] << 32) | c[1];
+  const unsigned long long b = ((unsigned long long)c[2] << 32) | c[3];
+  const double u1 = ((double)(a >> 11) + 1.0) * (1.0 / 9007199254740992.0);  // (0, 1]
+  const double u2 = (double)(b >> 11) * (1.0 / 9007199254740992.0);          // [0, 1)
+  const double r = sqrt(-2.0 * log(u1));
+  double sn, cs;
+#ifdef __CUDA_ARCH__
+  sincospi(2.0 * u2, &sn, &cs);
+#else
+  sn = sin(6.283185307179586 * u2);
+  cs = cos(6.283185307179586 * u2);
+#endif
+  z0 = r * cs;
+  z1 = r * sn;
+}
+
+// V chunk (rank columns [k0, k0 + kch)) of the compact live rows, tiled
+// (wt_index, mpad rows); columns >= rank are zero.
+__global__ void gen_v_tiled_kernel(double* Vt, int mpad, int kch, int k0, int rank, const int* row_pos,
+                                   const int* pos_sensor, int n_rows, int nt, unsigned long long seed) {
+  const long long half = kch / 2;
+  const long long total = (long long)mpad * half;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / half);
+    const int k = 2 * (int)(e - (long long)r * half);
+    double z0 = 0.0, z1 = 0.0;
+    if (r < n_rows) {
+      const int blk = r / nt;
+      const long long gi = (long long)pos_sensor[row_pos[blk]] * nt + (r - blk * nt);
+      philox_normal2(seed, gi, (k0 + k) >> 1, z0, z1);
+      if (k0 + k >= rank) z0 = 0.0;
+      if (k0 + k + 1 >= rank) z1 = 0.0;
+    }
+    Vt[wt_index(r, k, mpad)] = z0;
+    Vt[wt_index(r, k + 1, mpad)] = z1;
+  }
+}
+
+// C = sigma^2 on the diagonal of every own slot's diagonal block (C zeroed first)
+__global__ void add_diag_kernel(double* C, long long ldc, int nt, int nloc, int G, int rank, double v) {
+  const long long total = (long long)nloc * nt;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(e / nt), c = (int)(e - (long long)q * nt);
+    const long long p = (long long)q * G + rank;
+    C[((long long)q * nt + c) * ldc + p * nt + c] += v;
+  }
+}
+
 struct GenArgs {
   const double* V;       // (nd*nt) x rank row-major, sensor-major rows
   int rank;

@@ -193,6 +193,11 @@ class Engine:
         v = np.ascontiguousarray(v, dtype=np.float64)
         _check(lib.dsel_gen_synthetic(self.h, _ptr(v), rank, sigma), self.h)
 
+    def gen_synthetic_device(self, rank: int, sigma: float, seed: int) -> None:
+        """K = sigma^2 I + V V^T with V from the device Philox stream (not the
+        reference RNG; for C4/C5 scales where V cannot live on the host)."""
+        _check(lib.dsel_gen_synthetic_device(self.h, rank, sigma, seed), self.h)
+
     def read_block_row(self, j: int) -> np.ndarray:
         out = np.empty(self.n_sensors * self.n_steps * self.n_steps)
         _check(lib.dsel_read_block_row(self.h, j, _ptr(out)), self.h)

@@ -54,6 +54,30 @@ if which == "random":
     print(f"rank {rank}/{world} random: {'OK' if not bad else 'MISMATCH'}", flush=True)
     dist.destroy_process_group()
     sys.exit(1 if bad else 0)
+if which == "device":
+    # K formed on every rank by the update kernel from the device Philox V; the
+    # sequence must match the oracle on the same K (numpy V) at any world size
+    from oracle import oracle as O  # checker only
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from philox_ref import philox_v
+    nd, nt, rk, B, seed = 48, 16, 400, 12, 5
+    v = philox_v(nd, nt, rk, seed)
+    want = O.greedy_select(O.dense_to_blocks(0.25 * np.eye(nd * nt) + v @ v.T, nd, nt), nd, nt, B)
+    bad = 0
+    for kw in (dict(), dict(algorithm="left")):
+        cid = [d.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(cid, src=0)
+        with d.Engine(nd, nt, B, device=local, world_size=world, rank=rank, nccl_id=cid[0], **kw) as eng:
+            eng.gen_synthetic_device(rk, 0.5, seed)
+            eng.run()
+            rows = eng.trace()
+        ok = [r["chosen_index"] for r in rows] == list(want.chosen)
+        for r, g in zip(rows, want.gains):
+            ok = ok and abs(r["gain"] - g) <= 1e-9 * max(abs(g), 1.0)
+        bad += not ok
+    print(f"rank {rank}/{world} device: {'OK' if not bad else 'MISMATCH'}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(1 if bad else 0)
 gold = json.load(open(os.path.join(ROOT, "tests", "golden", f"{which}.json")))
 if which == "wave":
     from oracle import oracle as O  # checker only: parses the KBF fixture

@@ -405,3 +405,33 @@ def test_streaming_attached_host_k(dsel, O, golden_dir):
     with pytest.raises(dsel.InvalidConfig):
         with dsel.Engine(8, 2, 2) as eng:
             eng.attach_host_k(np.zeros(8 * 8 * 4))       # needs storage = stream
+
+
+# ---- device-side synthetic K (C4/C5 scales: V never on the host) -------- #
+from philox_ref import philox_v  # noqa: E402
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(full_square=True), dict(algorithm="left")])
+def test_device_synthetic_k_and_selection(dsel, O, kw):
+    """K formed on the device by the update kernel (Philox V) equals sigma^2 I + V V^T
+    to rounding, and the selection on it matches the oracle run on the same K."""
+    nd, nt, rank, B, seed = 40, 16, 300, 10, 77
+    with dsel.Engine(nd, nt, B, **kw) as eng:
+        eng.gen_synthetic_device(rank, 0.5, seed)
+        k = np.concatenate([eng.read_block_row(j) for j in range(nd)])
+        eng.run()
+        rows = eng.trace()
+    v = philox_v(nd, nt, rank, seed)
+    want_dense = 0.25 * np.eye(nd * nt) + v @ v.T
+    dense = O.blocks_to_dense(k, nd, nt)
+    if not kw:   # block-lower store: compare the lower block triangle
+        for i in range(nd):
+            for j in range(i + 1):
+                sl = np.s_[i * nt:(i + 1) * nt, j * nt:(j + 1) * nt]
+                np.testing.assert_allclose(dense[sl], want_dense[sl], rtol=1e-12, atol=1e-11)
+        dense = np.tril(dense) + np.tril(dense, -1).T
+        k = np.ascontiguousarray(dense.reshape(nd, nt, nd, nt).transpose(0, 2, 1, 3)).reshape(-1)
+    else:
+        np.testing.assert_allclose(dense, want_dense, rtol=1e-12, atol=1e-11)
+    want = O.greedy_select(k, nd, nt, B)
+    assert_trace_matches(rows, want.chosen, want.gains, want.objectives)
