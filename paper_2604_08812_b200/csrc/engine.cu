@@ -1144,6 +1144,16 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
       ncclUniqueId id;
       std::memcpy(&id, cfg->nccl_id, sizeof(id));
       NC(ncclCommInitRank(&e->comm, e->G, id, e->rank));
+      // establish NCCL's peer connections now (lazily done by the first call of
+      // each collective), so round 1 of the first selection is not charged for it
+      double* wb = e->Pbuf ? e->Pbuf : e->Lk;
+      const size_t wn = std::min<size_t>(e->Pbuf ? (size_t)e->n * e->nt : (size_t)e->nt * e->nt, 1 << 20);
+      NC(ncclGroupStart());
+      NC(ncclAllGather(e->d_rec, e->d_recs, sizeof(ArgRec), ncclUint8, e->comm, e->s));
+      NC(ncclGroupEnd());
+      NC(ncclAllReduce(wb, wb, wn, ncclDouble, ncclSum, e->comm, e->s));
+      NC(ncclBroadcast(wb, wb, wn, ncclDouble, 0, e->comm, e->s));
+      CU(cudaMemsetAsync(wb, 0, sizeof(double) * wn, e->s));
     }
     build_tables(e);
     CU(cudaStreamSynchronize(e->s));
@@ -1617,15 +1627,16 @@ dsel_status dsel_gen_synthetic(dsel_engine* e, const double* v_host, int rank, d
   });
 }
 
+static void reset_state(dsel_engine* e);
+
 dsel_status dsel_gen_synthetic_device(dsel_engine* e, int rank, double sigma, uint64_t seed) {
   return guard(e, [&] {
     if (rank < 1) throw Fail{DSEL_E_INVALID, "bad synthetic rank"};
     if (e->stream) throw Fail{DSEL_E_INVALID, "gen_synthetic_device fills the HBM panel store"};
     if (e->nt % 2) throw Fail{DSEL_E_INVALID, "gen_synthetic_device needs an even n_steps"};
-    if (!e->trace.empty()) throw Fail{DSEL_E_STATE, "gen_synthetic_device after selection started"};
     CU(cudaSetDevice(e->dev));
     const int nt = e->nt;
-    build_tables(e);
+    reset_state(e);  // K is rewritten whole: a new selection starts
     const int R = e->n_rows_tab, Rl = e->n_cols_tab;
     const int n_rows = R * nt, n_cols = Rl * nt;
     const bool sym = e->sym;
@@ -1754,6 +1765,21 @@ int dsel_get_trace(dsel_engine* e, dsel_step_info* rows, int max_rows) {
   }
 }
 
+// selection state back to "nothing chosen" (the store is handled by the caller)
+static void reset_state(dsel_engine* e) {
+  e->alive.assign(e->nc, 1);
+  e->n_alive = e->nc;
+  e->chosen.clear();
+  e->trace.clear();
+  e->objective = 0.0;
+  e->finished = false;
+  e->launches = 0;
+  e->update_flops = 0.0;
+  e->streamed_round.clear();
+  e->h2d_bytes = e->d2h_bytes = e->nccl_bytes = 0;
+  build_tables(e);
+}
+
 dsel_status dsel_reset(dsel_engine* e) {
   return guard(e, [&] {
     if (!e->keep && !e->ll) throw Fail{DSEL_E_STATE, "dsel_reset requires keep_pristine"};
@@ -1761,17 +1787,7 @@ dsel_status dsel_reset(dsel_engine* e) {
     if (!e->ll)  // the left-looking store is K itself and is never modified
       CU(cudaMemcpyAsync(e->C, e->K0, sizeof(double) * e->n * e->nloc * e->nt,
                          cudaMemcpyDeviceToDevice, e->s));
-    e->alive.assign(e->nc, 1);
-    e->n_alive = e->nc;
-    e->chosen.clear();
-    e->trace.clear();
-    e->objective = 0.0;
-    e->finished = false;
-    e->launches = 0;
-    e->update_flops = 0.0;
-    e->streamed_round.clear();
-    e->h2d_bytes = e->d2h_bytes = e->nccl_bytes = 0;
-    build_tables(e);
+    reset_state(e);
     CU(cudaStreamSynchronize(e->s));
   });
 }
