@@ -151,6 +151,29 @@ dsel_status dsel_attach_host_rows(dsel_engine* e, const double* host_rows);
  * Schur update kernel (W = +V, 512 rank columns per launch; block-lower tiles
  * only under symmetric storage). HBM store only; n_steps even. */
 dsel_status dsel_gen_synthetic_device(dsel_engine* e, int rank, double sigma, uint64_t seed);
+/* ---- K formation from an LTI wave problem (assemble_k, hessian.hpp:91-144) ----
+ * K = Gamma_noise + F W Gamma_prior W F^T assembled on the GPU, bit-identical to
+ * the reference (sequential non-FMA sums in its loop order, exact block
+ * symmetrization). Tables are row-major: impulse[s][j][tau] (lti.hpp:82-87),
+ * spatial[i][j] (materialized prior, lti.hpp:245-251), mask[j][t] (or NULL),
+ * cost_weights[s] (or NULL). */
+typedef struct dsel_lti {
+  int n_params, n_sensors, n_steps;
+  double noise_sigma;
+  const double* impulse;
+  const double* spatial;
+  const double* mask;
+  const double* cost_weights;
+} dsel_lti;
+/* Parse a reference problem config (config.hpp:17-164) and build its wave
+ * problem (make_wave_problem, lti.hpp:163-176) on the host. Arrays in *out are
+ * owned by *owner; release with dsel_lti_free. DSEL_E_INVALID / DSEL_E_IO. */
+dsel_status dsel_lti_from_config(const char* path, dsel_lti* out, void** owner);
+void dsel_lti_free(void* owner);
+/* Assemble this rank's panels of K from the problem (HBM store; resets the
+ * selection). noise_logdets (n_sensors, may be NULL) receives n_steps *
+ * log(w_c gamma^2) per sensor (noise_block_logdets, hessian.hpp:149-154). */
+dsel_status dsel_assemble_lti(dsel_engine* e, const dsel_lti* problem, double* noise_logdets);
 /* KBF store (`doptsel select <kbf>`, KStoreReader, kstore.hpp:22-186): validates
  * the header and size like KStoreReader (E_CORRUPT / E_IO) and loads this
  * rank's panels with parallel pread into pinned buffers, overlapped with the

@@ -91,6 +91,7 @@ def ref():
         R.ref_greedy_select.argtypes = [_dp, C.c_int, C.c_int, _ip, C.c_int, C.c_int, _ip, _dp,
                                         _dp, _ip, _ip, _ip]
         R.ref_wave_kbf.argtypes = [C.c_char_p, _dp]
+        R.ref_build_kbf.argtypes = [C.c_char_p, C.c_char_p, _dp]
         R.ref_write_kbf.argtypes = [_dp, C.c_int, C.c_int, C.c_char_p]
         R.ref_kbf_select.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_uint64, _ip, _dp, _dp,
                                      _ip, _ip, _ip]
@@ -265,6 +266,13 @@ def ref_replay(k, nd, nt, sequence) -> np.ndarray:
 def ref_wave_kbf(path: str) -> np.ndarray:
     nl = np.zeros(32)
     _check_ref(ref().ref_wave_kbf(path.encode(), nl))
+    return nl
+
+
+def ref_build_kbf(config_path: str, out_path: str, n_sensors: int) -> np.ndarray:
+    """Reference `doptsel build` (assemble_k -> write_kbf); returns noise log-dets."""
+    nl = np.zeros(n_sensors)
+    _check_ref(ref().ref_build_kbf(config_path.encode(), out_path.encode(), nl))
     return nl
 
 

@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "doptsel/bench.hpp"
+#include "doptsel/config.hpp"
 #include "doptsel/hessian.hpp"
 #include "doptsel/kaccess.hpp"
 #include "doptsel/kstore.hpp"
@@ -182,6 +183,26 @@ int ref_wave_kbf(const char* path, double* noise_logdets) {
     write_kbf(k, path);
     const std::vector<double> nl = noise_block_logdets(k);
     std::copy(nl.begin(), nl.end(), noise_logdets);
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+// `doptsel build <config> <out.kbf>` (doptsel_main.cpp:63-75): config ->
+// problem_from_config -> weights_from_config -> assemble_k -> write_kbf.
+// noise_logdets (n_sensors entries, may be null) from noise_block_logdets.
+int ref_build_kbf(const char* config_path, const char* out_path, double* noise_logdets) {
+  try {
+    const ProblemConfig cfg = load_problem_config(config_path);
+    const LtiProblem problem = problem_from_config(cfg);
+    const WeightSpec weights = weights_from_config(cfg);
+    const DataSpaceHessian k = assemble_k(problem, &weights);
+    write_kbf(k, out_path);
+    if (noise_logdets) {
+      const std::vector<double> nl = noise_block_logdets(k);
+      std::copy(nl.begin(), nl.end(), noise_logdets);
+    }
     return 0;
   } catch (...) {
     return map_exception();

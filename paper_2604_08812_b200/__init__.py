@@ -5,10 +5,11 @@ This package is the thin host mirror of the reference selection interface.
 """
 from ._abi import LIB_PATH, lib  # noqa: F401  (raises ImportError if the library is missing)
 from .selector import (CorruptFile, DselError, Engine, IoError, GpuOptions, IndexOutOfRange,  # noqa: F401
+                       LtiProblem,
                        InfeasibleRound, InvalidConfig, ParallelRunReport, SelectionState,
                        SelectionTrace, TraceRow, WorkerFailure, gpu_greedy_select,
                        fold_records, nccl_unique_id, synthetic_v)
 
-__all__ = ["Engine", "GpuOptions", "gpu_greedy_select", "synthetic_v", "nccl_unique_id", "fold_records",
+__all__ = ["Engine", "LtiProblem", "GpuOptions", "gpu_greedy_select", "synthetic_v", "nccl_unique_id", "fold_records",
            "DselError", "IoError", "CorruptFile", "InvalidConfig", "IndexOutOfRange", "InfeasibleRound", "WorkerFailure",
            "SelectionState", "SelectionTrace", "ParallelRunReport", "TraceRow", "LIB_PATH"]

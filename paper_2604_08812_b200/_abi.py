@@ -20,7 +20,8 @@ STATUS_NAMES = {0: "DSEL_OK", 1: "DSEL_E_INVALID", 2: "DSEL_E_RANGE", 3: "DSEL_E
 EXPORTS = ["dsel_abi_version", "dsel_fold_records", "dsel_nccl_unique_id", "dsel_create", "dsel_destroy",
            "dsel_last_error", "dsel_sync", "dsel_device_bytes", "dsel_load_block_row",
            "dsel_load_block_col", "dsel_load_k", "dsel_attach_host_k", "dsel_attach_host_rows", "dsel_load_kbf", "dsel_read_block_row", "dsel_synthetic_v",
-           "dsel_gen_synthetic", "dsel_gen_synthetic_device", "dsel_step", "dsel_step_forced", "dsel_run", "dsel_peek_gains",
+           "dsel_gen_synthetic", "dsel_gen_synthetic_device", "dsel_lti_from_config", "dsel_lti_free",
+           "dsel_assemble_lti", "dsel_step", "dsel_step_forced", "dsel_run", "dsel_peek_gains",
            "dsel_get_trace", "dsel_reset", "dsel_get_stats", "dsel_export_factor"]
 
 
@@ -50,6 +51,12 @@ class DselStepInfo(C.Structure):
 class DselArgRec(C.Structure):
     _fields_ = [("g1", C.c_double), ("g2", C.c_double), ("s1", C.c_int), ("s2", C.c_int),
                 ("n_eval", C.c_int), ("n_inf", C.c_int)]
+
+
+class DselLti(C.Structure):
+    _fields_ = [("n_params", C.c_int), ("n_sensors", C.c_int), ("n_steps", C.c_int),
+                ("noise_sigma", C.c_double), ("impulse", C.c_void_p), ("spatial", C.c_void_p),
+                ("mask", C.c_void_p), ("cost_weights", C.c_void_p)]
 
 
 class DselStats(C.Structure):
@@ -86,6 +93,10 @@ def _load():
     L.dsel_attach_host_k.argtypes = [vp, vp]
     L.dsel_gen_synthetic_device.argtypes = [vp, C.c_int, C.c_double, C.c_uint64]
     L.dsel_attach_host_rows.argtypes = [vp, vp]
+    L.dsel_lti_from_config.argtypes = [C.c_char_p, C.POINTER(DselLti), C.POINTER(vp)]
+    L.dsel_lti_free.argtypes = [vp]
+    L.dsel_lti_free.restype = None
+    L.dsel_assemble_lti.argtypes = [vp, C.POINTER(DselLti), vp]
     L.dsel_load_kbf.argtypes = [vp, C.c_char_p, C.c_int, C.c_int]
     L.dsel_read_block_row.argtypes = [vp, C.c_int, vp]
     L.dsel_synthetic_v.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, vp, C.c_int]
@@ -103,6 +114,7 @@ def _load():
     L.dsel_fold_records.restype = None
     for name in EXPORTS:
         if name not in ("dsel_destroy", "dsel_last_error", "dsel_device_bytes", "dsel_fold_records",
+                        "dsel_lti_free",
                         "dsel_get_trace", "dsel_abi_version"):
             getattr(L, name).restype = C.c_int
     return L

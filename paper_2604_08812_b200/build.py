@@ -66,7 +66,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
     o = os.path.join(OUT, "engine.o")
     _run(nv + ["-c", os.path.join(CSRC, "engine.cu"), "-o", o])
     objs.append(o)
-    for cpp in ("host_rng.cpp", "kbf.cpp"):
+    for cpp in ("host_rng.cpp", "lti.cpp", "kbf.cpp"):
         src = os.path.join(CSRC, cpp)
         if not os.path.exists(src):
             continue

@@ -31,6 +31,7 @@
 
 #include "dsel.h"
 #include "kernels.cuh"
+#include "lti.h"
 
 using namespace dsel;
 
@@ -1692,6 +1693,86 @@ dsel_status dsel_gen_synthetic_device(dsel_engine* e, int rank, double sigma, ui
     if (ce != cudaSuccess) throw Fail{DSEL_E_CUDA, std::string("device synthetic K: ") + cudaGetErrorString(ce)};
     e->gen_flops = gen_flops;
     e->full_panels = !sym;
+    if (e->keep && e->C)
+      CU(cudaMemcpyAsync(e->K0, e->C, sizeof(double) * e->n * e->nloc * e->nt,
+                         cudaMemcpyDeviceToDevice, e->s));
+    CU(cudaStreamSynchronize(e->s));
+  });
+}
+
+// ---- K formation from an LTI wave problem ------------ //
+struct LtiOwner {
+  LtiHost h;
+};
+
+dsel_status dsel_lti_from_config(const char* path, dsel_lti* out, void** owner) {
+  return guard(nullptr, [&] {
+    if (!path || !out || !owner) throw Fail{DSEL_E_INVALID, "null argument"};
+    auto* o = new LtiOwner();
+    std::string err;
+    const int rc = lti_from_config(path, o->h, err);
+    if (rc != 0) {
+      delete o;
+      throw Fail{rc == 7 ? DSEL_E_IO : DSEL_E_INVALID, err};
+    }
+    out->n_params = o->h.n_params;
+    out->n_sensors = o->h.n_sensors;
+    out->n_steps = o->h.n_steps;
+    out->noise_sigma = o->h.noise_sigma;
+    out->impulse = o->h.impulse.data();
+    out->spatial = o->h.spatial.data();
+    out->mask = o->h.mask.empty() ? nullptr : o->h.mask.data();
+    out->cost_weights = o->h.cost.empty() ? nullptr : o->h.cost.data();
+    *owner = o;
+  });
+}
+
+void dsel_lti_free(void* owner) { delete static_cast<LtiOwner*>(owner); }
+
+dsel_status dsel_assemble_lti(dsel_engine* e, const dsel_lti* lp, double* noise_logdets) {
+  return guard(e, [&] {
+    if (!lp || !lp->impulse || !lp->spatial) throw Fail{DSEL_E_INVALID, "null LTI problem"};
+    if (lp->n_sensors != e->nd || lp->n_steps != e->nt)
+      throw Fail{DSEL_E_INVALID, "LTI problem dimensions differ from the engine's"};
+    if (lp->n_params < 1 || !(lp->noise_sigma > 0.0)) throw Fail{DSEL_E_INVALID, "bad LTI problem"};
+    if (e->stream) throw Fail{DSEL_E_INVALID, "assemble_lti fills the HBM panel store"};
+    CU(cudaSetDevice(e->dev));
+    const int nd = e->nd, nt = e->nt, nm = lp->n_params;
+    const size_t n = (size_t)nd * nt;
+    const double gamma2 = lp->noise_sigma * lp->noise_sigma;
+    if (noise_logdets)  // noise_block_logdets (hessian.hpp:149-154)
+      for (int i = 0; i < nd; ++i)
+        noise_logdets[i] = nt * std::log((lp->cost_weights ? lp->cost_weights[i] : 1.0) * gamma2);
+    reset_state(e);
+    const size_t nh = (size_t)nd * nm * nt, ns = (size_t)nm * nm, nmask = lp->mask ? (size_t)nm * nt : 0;
+    const size_t nvf = n * nm * nt, np1 = (size_t)nt * nd * nt, np2 = n * nt;
+    double* buf = nullptr;
+    CU(cudaMalloc(&buf, sizeof(double) * (nh + ns + nmask + nvf + np1 + np2)));
+    double *h = buf, *sp = h + nh, *mk = lp->mask ? sp + ns : nullptr, *vf = sp + ns + nmask,
+           *p1 = vf + nvf, *p2 = p1 + np1;
+    cudaError_t ce = cudaMemcpyAsync(h, lp->impulse, sizeof(double) * nh, cudaMemcpyHostToDevice, e->s);
+    if (ce == cudaSuccess)
+      ce = cudaMemcpyAsync(sp, lp->spatial, sizeof(double) * ns, cudaMemcpyHostToDevice, e->s);
+    if (ce == cudaSuccess && mk)
+      ce = cudaMemcpyAsync(mk, lp->mask, sizeof(double) * nmask, cudaMemcpyHostToDevice, e->s);
+    auto grid = [](long long total) { return (unsigned)std::min<long long>((total + 255) / 256, 148 * 64); };
+    if (ce == cudaSuccess) {  // the prior field of every column
+      lti_field_kernel<<<grid((long long)nvf), 256, 0, e->s>>>(h, sp, mk, nm, nt, 0, (int)n, vf);
+      ce = cudaGetLastError();
+    }
+    for (int q = 0; q < e->nloc && ce == cudaSuccess; ++q) {
+      const int js = e->slot_sensor[q];
+      lti_response_kernel<<<grid((long long)np1), 256, 0, e->s>>>(h, vf, 0, nm, nt, js * nt, nt, 0, nd, p1);
+      lti_response_kernel<<<grid((long long)np2), 256, 0, e->s>>>(h, vf, 0, nm, nt, 0, (int)n, js, 1, p2);
+      const double wc = lp->cost_weights ? lp->cost_weights[js] : 1.0;
+      lti_panel_kernel<<<grid((long long)e->nc * nt * nt), 256, 0, e->s>>>(
+          p1, p2, nd, nt, js, wc * gamma2, e->d_pos_sensor, e->nc, e->C + (size_t)q * nt * e->n, e->n);
+      ce = cudaGetLastError();
+    }
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(e->s);
+    cudaFree(buf);
+    if (ce != cudaSuccess) throw Fail{DSEL_E_CUDA, std::string("assemble_lti: ") + cudaGetErrorString(ce)};
+    e->full_panels = true;
     if (e->keep && e->C)
       CU(cudaMemcpyAsync(e->K0, e->C, sizeof(double) * e->n * e->nloc * e->nt,
                          cudaMemcpyDeviceToDevice, e->s));

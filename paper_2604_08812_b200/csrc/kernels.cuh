@@ -1894,6 +1894,92 @@ __global__ void add_diag_kernel(double* C, long long ldc, int nt, int nloc, int 
   }
 }
 
+// ------------------------------------------------------------------------ //
+// K formation from an LTI wave problem (assemble_k, hessian.hpp:91-144),     //
+// bit-exact: every sum runs sequentially in the reference loop order with   //
+// non-contracted __dmul_rn/__dadd_rn.                                         //
+// Column (js, tp) of the prior term pushes a unit impulse through the adjoint //
+// (exactly f[j][t] = h[js][j][tp-t], t <= tp), the masked prior and forward.  //
+// ------------------------------------------------------------------------ //
+// field of columns [c0, c0 + n_cols): vf[c][i][t] (nm x nt per column)
+__global__ void lti_field_kernel(const double* h, const double* spatial, const double* mask, int nm,
+                                 int nt, int c0, int n_cols, double* vf) {
+  const long long total = (long long)n_cols * nm * nt;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(e % nt);
+    const int i = (int)((e / nt) % nm);
+    const int cl = (int)(e / ((long long)nt * nm));
+    const int col = c0 + cl;
+    const int js = col / nt, tp = col - js * nt;
+    const double* row = spatial + (size_t)i * nm;
+    double acc = 0.0;  // apply_masked_prior (lti.hpp:205-238)
+    for (int j = 0; j < nm; ++j) {
+      double f = t <= tp ? h[((size_t)js * nm + j) * nt + (tp - t)] : 0.0;
+      if (mask) f = __dmul_rn(f, mask[(size_t)j * nt + t]);
+      acc = __dadd_rn(acc, __dmul_rn(row[j], f));
+    }
+    if (mask) acc = __dmul_rn(acc, mask[(size_t)i * nt + t]);
+    vf[e] = acc;
+  }
+}
+
+// forward responses (apply_forward, lti.hpp:178-197): out[c][s][t] for
+// columns [c0, c0 + n_cols) (fields vf, indexed from vc0) at sensors
+// [s0, s0 + n_s): d[s][t] = sum_j sum_{tau <= t, h != 0} h[s][j][tau] vf[c][j][t - tau]
+__global__ void lti_response_kernel(const double* h, const double* vf, int vc0, int nm, int nt, int c0,
+                                    int n_cols, int s0, int n_s, double* out) {
+  const long long total = (long long)n_cols * n_s * nt;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(e % nt);
+    const int sl = (int)((e / nt) % n_s);
+    const int cl = (int)(e / ((long long)nt * n_s));
+    const double* hs = h + (size_t)(s0 + sl) * nm * nt;
+    const double* v = vf + (size_t)(c0 + cl - vc0) * nm * nt;
+    double d = 0.0;
+    for (int j = 0; j < nm; ++j) {
+      const double* hj = hs + (size_t)j * nt;
+      const double* vj = v + (size_t)j * nt;
+      for (int tau = 0; tau <= t; ++tau) {
+        const double c = hj[tau];
+        if (c == 0.0) continue;
+        d = __dadd_rn(d, __dmul_rn(c, vj[t - tau]));
+      }
+    }
+    out[e] = d;
+  }
+}
+
+// own panel q (sensor js) from P1 = responses of columns (js, 0..nt) at all
+// sensors ([tp][i][t]) and P2 = responses of all columns at sensor js
+// ([col][t]): noise on the diagonal block, then the exact block
+// symmetrization of hessian.hpp:129-141: K(js,i)(r,c) = 0.5 (K(i,js)(c,r) + K(js,i)(r,c)).
+__global__ void lti_panel_kernel(const double* p1, const double* p2, int nd, int nt, int js, double noise,
+                                 const int* pos_sensor, int nc, double* panel, long long ldc) {
+  const long long total = (long long)nc * nt * nt;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e % nt);
+    const int p = (int)((e / nt) % nc);
+    const int r = (int)(e / ((long long)nt * nc));
+    const int i = pos_sensor[p];
+    double a, b;
+    if (i == js) {  // A = block(js, js) + noise I; K = 0.5 (A(r,c) + A(c,r))
+      a = p1[((size_t)c * nd + js) * nt + r];
+      b = p1[((size_t)r * nd + js) * nt + c];
+      if (r == c) {
+        a = __dadd_rn(a, noise);
+        b = a;
+      }
+    } else {
+      a = p1[((size_t)r * nd + i) * nt + c];            // block(i, js)(c, r): column (js, r), sensor i, time c
+      b = p2[((size_t)i * nt + c) * nt + r];            // block(js, i)(r, c): column (i, c), sensor js, time r
+    }
+    panel[((size_t)r) * ldc + (size_t)p * nt + c] = __dmul_rn(0.5, __dadd_rn(a, b));
+  }
+}
+
 struct GenArgs {
   const double* V;       // (nd*nt) x rank row-major, sensor-major rows
   int rank;

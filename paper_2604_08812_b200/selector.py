@@ -19,7 +19,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._abi import DSEL_OK, STATUS_NAMES, DselArgRec, DselConfig, DselStats, DselStepInfo, lib
+from ._abi import DSEL_OK, STATUS_NAMES, DselArgRec, DselConfig, DselLti, DselStats, DselStepInfo, lib
 
 
 # ---- errors (errors.hpp:10-86) -------------------------------------------- #
@@ -100,6 +100,44 @@ def synthetic_v(n_sensors: int, n_steps: int, rank: int, seed: int, threads: int
     out = np.empty(n_sensors * n_steps * rank, dtype=np.float64)
     _check(lib.dsel_synthetic_v(n_sensors, n_steps, rank, seed, _ptr(out), threads))
     return out.reshape(n_sensors * n_steps, rank)
+
+
+@dataclass
+class LtiProblem:
+    """Host tables of an LTI wave problem (lti.hpp:62-120): impulse[s][j][tau],
+    materialized spatial prior[i][j], optional mask[j][t] and cost weights."""
+    n_params: int
+    n_sensors: int
+    n_steps: int
+    noise_sigma: float
+    impulse: np.ndarray
+    spatial: np.ndarray
+    mask: np.ndarray | None = None
+    cost_weights: np.ndarray | None = None
+
+    @classmethod
+    def from_config(cls, path: str) -> "LtiProblem":
+        """Reference problem config (config.hpp) -> make_wave_problem tables."""
+        lt, owner = DselLti(), C.c_void_p()
+        _check(lib.dsel_lti_from_config(path.encode(), C.byref(lt), C.byref(owner)))
+        try:
+            nm, nd, nt = lt.n_params, lt.n_sensors, lt.n_steps
+
+            def arr(ptr, count):
+                return None if not ptr else np.ctypeslib.as_array(
+                    C.cast(ptr, C.POINTER(C.c_double)), shape=(count,)).copy()
+
+            return cls(nm, nd, nt, lt.noise_sigma, arr(lt.impulse, nd * nm * nt),
+                       arr(lt.spatial, nm * nm), arr(lt.mask, nm * nt), arr(lt.cost_weights, nd))
+        finally:
+            lib.dsel_lti_free(owner)
+
+    def _struct(self):
+        keep = [np.ascontiguousarray(x, dtype=np.float64) if x is not None else None
+                for x in (self.impulse, self.spatial, self.mask, self.cost_weights)]
+        lt = DselLti(self.n_params, self.n_sensors, self.n_steps, self.noise_sigma,
+                     *[x.ctypes.data if x is not None else None for x in keep])
+        return lt, keep
 
 
 class Engine:
@@ -197,6 +235,18 @@ class Engine:
         """K = sigma^2 I + V V^T with V from the device Philox stream (not the
         reference RNG; for C4/C5 scales where V cannot live on the host)."""
         _check(lib.dsel_gen_synthetic_device(self.h, rank, sigma, seed), self.h)
+
+    def assemble_lti(self, problem: "LtiProblem | str") -> np.ndarray:
+        """K = Gamma_noise + F W Gamma_prior W F^T formed on the GPU, bit-identical
+        to assemble_k (hessian.hpp:91-144); a config path or an LtiProblem.
+        Returns the per-sensor noise log-dets (noise_block_logdets)."""
+        if isinstance(problem, str):
+            problem = LtiProblem.from_config(problem)
+        lt, keep = problem._struct()
+        out = np.zeros(self.n_sensors)
+        _check(lib.dsel_assemble_lti(self.h, C.byref(lt), _ptr(out)), self.h)
+        del keep
+        return out
 
     def read_block_row(self, j: int) -> np.ndarray:
         out = np.empty(self.n_sensors * self.n_steps * self.n_steps)

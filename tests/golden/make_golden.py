@@ -2,7 +2,7 @@
 itself (oracle/_ref/libdoptsel_ref.so, compiled from /root/reference by
 oracle/Makefile). Run in the build container (needs /root/reference):
 
-    python tests/golden/make_golden.py [c1 wave random c2]
+    python tests/golden/make_golden.py [c1 wave random lti c2]
 
 c2 takes ~20 min on 8 cores (K materialization + 50 rounds).
 """
@@ -67,6 +67,31 @@ def wave():
                                         for row in ga.tolist()]})
 
 
+def lti_configs():
+    """Reference `doptsel build` on each tests/golden/configs/*.cfg: KBF sha256,
+    noise log-dets and the reference selection on the built store."""
+    import tempfile
+
+    out = {}
+    for name in sorted(os.listdir(os.path.join(HERE, "configs"))):
+        if not name.endswith(".cfg") or name.startswith("bad"):
+            continue
+        cfg = os.path.join(HERE, "configs", name)
+        with tempfile.TemporaryDirectory() as td:
+            path = os.path.join(td, "k.kbf")
+            nd = int([ln.split("=")[1] for ln in open(cfg) if ln.startswith("n_sensors")][0])
+            nl = O.ref_build_kbf(cfg, path, nd)
+            k, nd, nt = O.read_kbf(path)
+            budget = min(12, nd)
+            tr = O.ref_kbf_select(path, budget, workers=1)
+            out[name] = {"n_sensors": nd, "n_steps": nt, "budget": budget,
+                         "kbf_sha256": hashlib.sha256(open(path, "rb").read()).hexdigest(),
+                         "noise_logdets": nl.tolist(), **trace_dict(tr)}
+    dump("lti.json", {"source": "reference: load_problem_config -> problem_from_config -> "
+                                "weights_from_config -> assemble_k -> write_kbf (doptsel build), "
+                                "then KStoreReader -> run_parallel_greedy", "configs": out})
+
+
 def random_cases():
     cases = []
     # shapes follow proj/tests/test_selector.cpp / test_parallel.cpp generators
@@ -86,13 +111,15 @@ def random_cases():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["c1", "wave", "random"]
+    which = sys.argv[1:] or ["c1", "wave", "random", "lti"]
     if "c1" in which:
         synthetic_case("c1", 64, 32, 2048, 1.0, 2024, 16, replay=True)
     if "wave" in which:
         wave()
     if "random" in which:
         random_cases()
+    if "lti" in which:
+        lti_configs()
     if "c3mini" in which:  # Nt = 420 (the CSZ block size) at oracle-friendly scale
         synthetic_case("c3mini", 12, 420, 4096, 1.0, 2024, 6, workers=os.cpu_count(), replay=True)
     if "c2" in which:

@@ -91,3 +91,23 @@ def test_invalid_config_rejected_before_device_work():
         d.Engine(8, 2, 2, storage=2)               # streaming needs the left-looking algorithm
     with pytest.raises(d.InvalidConfig):
         d.Engine(8, 2, 2, algorithm="middle")
+
+
+def test_lti_config_host_tables(golden_dir=os.path.join(ROOT, "tests", "golden")):
+    """Config parsing + make_wave_problem on the host (no GPU): dimensions,
+    default noise (0.1 max|h|), mask/cost expansion, error mapping."""
+    import paper_2604_08812_b200 as d
+
+    p = d.LtiProblem.from_config(os.path.join(golden_dir, "configs", "wave_benchmark.cfg"))
+    assert (p.n_params, p.n_sensors, p.n_steps) == (48, 32, 16)
+    assert p.noise_sigma == 0.1 * np.abs(p.impulse).max()
+    assert abs(p.noise_sigma - 0.075696580131319649) < 1e-17
+    assert p.mask is None and p.cost_weights is None
+    assert p.spatial[0] == 1.0 and abs(p.spatial[1] - np.exp(-1 / 6.0)) < 1e-16
+    w = d.LtiProblem.from_config(os.path.join(golden_dir, "configs", "weighted.cfg"))
+    assert w.mask.shape == (48 * 16,) and w.mask[0] == 0.0 and w.mask[24 * 16 + 12] == 0.5
+    assert w.cost_weights[0] == 4.0
+    with pytest.raises(d.InvalidConfig):
+        d.LtiProblem.from_config(os.path.join(golden_dir, "configs", "bad_key.cfg"))
+    with pytest.raises(d.IoError):
+        d.LtiProblem.from_config(os.path.join(golden_dir, "configs", "missing.cfg"))
