@@ -11,12 +11,12 @@
 //                  [--seed S] [--pipeline on|off] [--precision f64]
 //                  [--config cfg | --noise-logdets file] [--kbf-rows] [--out DIR]
 //   doptsel select --synthetic nd,nt,rank,sigma,seed --budget B ...
+//   doptsel build <config> <out.kbf>     (doptsel_main.cpp:63-75; K on the GPU)
 //
 // --mode schur (the reference default) and gpu both run the GPU engine;
 // naive (refactorizing baseline) and --precision f32 are CPU-only paths of the
 // reference and are rejected. --workers is accepted (the reference's CPU
-// worker count) and ignored. Other subcommands (build, evaluate, bench) are
-// outside the selection hot path.
+// worker count) and ignored. evaluate and bench are outside the hot path.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -85,39 +85,76 @@ std::vector<double> parse_list(const std::string& s) {
   return out;
 }
 
-// Noise log-determinants from a problem config (config.hpp:25-128 syntax):
-// n_steps * log(w_c * noise_sigma^2) (doptsel_main.cpp:51-61). Only configs
-// with an explicit noise_sigma: the default noise level needs the LTI model.
+// noise_logdets_from_config (doptsel_main.cpp:47-59): the LTI problem of the
+// config (dsel_lti_from_config -- the full wave model, so the default noise
+// level 0.1 max|h| is honoured) gives gamma; n_steps * log(w_c gamma^2).
 std::vector<double> noise_from_config(const std::string& path) {
-  std::ifstream in(path);
-  if (!in) throw std::runtime_error("io:cannot open config file " + path);
-  int n_sensors = 8, n_steps = 8;
-  double sigma = -1.0;
-  std::vector<double> w;
-  std::string line;
-  while (std::getline(in, line)) {
-    const auto hash = line.find('#');
-    if (hash != std::string::npos) line = line.substr(0, hash);
-    const auto eq = line.find('=');
-    if (eq == std::string::npos) continue;
-    auto trim = [](std::string s) {
-      size_t a = s.find_first_not_of(" \t\r"), b = s.find_last_not_of(" \t\r");
-      return a == std::string::npos ? std::string() : s.substr(a, b - a + 1);
-    };
-    const std::string k = trim(line.substr(0, eq)), v = trim(line.substr(eq + 1));
-    if (k == "n_sensors") n_sensors = std::stoi(v);
-    else if (k == "n_steps") n_steps = std::stoi(v);
-    else if (k == "noise_sigma") sigma = std::stod(v);
-    else if (k == "cost_weights") w = parse_list(v);
-  }
-  if (!(sigma > 0.0))
-    throw std::runtime_error(
-        "usage:config has no explicit noise_sigma; its default needs the LTI model (K "
-        "formation, outside the selection path) -- pass --noise-logdets FILE instead");
-  std::vector<double> out(n_sensors);
-  for (int i = 0; i < n_sensors; ++i)
-    out[i] = n_steps * std::log((w.empty() ? 1.0 : w[i]) * sigma * sigma);
+  dsel_lti p{};
+  void* owner = nullptr;
+  const dsel_status st = dsel_lti_from_config(path.c_str(), &p, &owner);
+  if (st != DSEL_OK)
+    throw std::runtime_error(std::string(st == DSEL_E_IO ? "io:" : "usage:") + dsel_last_error(nullptr));
+  std::vector<double> out(p.n_sensors);
+  const double g2 = p.noise_sigma * p.noise_sigma;
+  for (int i = 0; i < p.n_sensors; ++i)
+    out[i] = p.n_steps * std::log((p.cost_weights ? p.cost_weights[i] : 1.0) * g2);
+  dsel_lti_free(owner);
   return out;
+}
+
+// `doptsel build <config> <out.kbf>` (doptsel_main.cpp:63-75): K assembled on
+// the GPU (dsel_assemble_lti, bit-identical to assemble_k), written as KBF.
+int cmd_build(const std::string& config, const std::string& out_path) {
+  dsel_lti p{};
+  void* owner = nullptr;
+  dsel_status st = dsel_lti_from_config(config.c_str(), &p, &owner);
+  if (st != DSEL_OK) {
+    std::cerr << "error: " << dsel_last_error(nullptr) << "\n";
+    return st == DSEL_E_IO ? kExitIo : kExitUsage;
+  }
+  const int nd = p.n_sensors, nt = p.n_steps;
+  dsel_config cfg{};
+  cfg.n_sensors = nd;
+  cfg.n_steps = nt;
+  cfg.budget = 1;
+  cfg.world_size = 1;
+  cfg.full_square = 1;  // whole panels: every block row is read back
+  cfg.algorithm = 1;
+  dsel_engine* e = nullptr;
+  st = dsel_create(&cfg, &e);
+  std::vector<double> row((size_t)nd * nt * nt);
+  std::FILE* f = nullptr;
+  if (st == DSEL_OK) st = dsel_assemble_lti(e, &p, nullptr);
+  dsel_lti_free(owner);
+  if (st != DSEL_OK) {
+    std::cerr << "error: " << dsel_last_error(e) << "\n";
+    dsel_destroy(e);
+    return kExitUsage;
+  }
+  f = std::fopen(out_path.c_str(), "wb");
+  if (!f) {
+    std::cerr << "error: cannot open " << out_path << " for writing\n";
+    dsel_destroy(e);
+    return kExitIo;
+  }
+  unsigned char h[32] = {'K', 'B', 'F', '1'};
+  const unsigned fields[5] = {1u, (unsigned)nd, (unsigned)nt, 1u, 1u};
+  for (int q = 0; q < 5; ++q)
+    for (int b = 0; b < 4; ++b) h[4 + 4 * q + b] = (unsigned char)(fields[q] >> (8 * b));
+  bool ok = std::fwrite(h, 1, 32, f) == 32;
+  for (int j = 0; j < nd && ok; ++j) {
+    st = dsel_read_block_row(e, j, row.data());
+    ok = st == DSEL_OK && std::fwrite(row.data(), sizeof(double), row.size(), f) == row.size();
+  }
+  ok = (std::fclose(f) == 0) && ok;
+  dsel_destroy(e);
+  if (!ok) {
+    std::cerr << "error: short write to " << out_path << "\n";
+    return kExitIo;
+  }
+  std::cout << "wrote " << out_path << ": n_sensors=" << nd << " n_steps=" << nt
+            << " bytes=" << 32ull + (unsigned long long)nd * nd * nt * nt * 8ull << "\n";
+  return kExitOk;
 }
 
 struct RankResult {
@@ -367,7 +404,8 @@ int usage() {
                "                      [--algorithm right|left] [--storage auto|hbm|stream]\n"
                "                      [--seed S] [--pipeline on|off] [--precision f64]\n"
                "                      [--config cfg | --noise-logdets file] [--kbf-rows] [--out DIR]\n"
-               "       doptsel select --synthetic nd,nt,rank,sigma,seed --budget B [...]\n";
+               "       doptsel select --synthetic nd,nt,rank,sigma,seed --budget B [...]\n"
+               "       doptsel build <config> <out.kbf>      (K assembled on the GPU)\n";
   return kExitUsage;
 }
 
@@ -376,7 +414,14 @@ int usage() {
 int main(int argc, char** argv) {
   if (argc < 2) return usage();
   const std::string cmd = argv[1];
-  if (cmd == "build" || cmd == "evaluate" || cmd == "bench") {
+  if (cmd == "build") {
+    if (argc != 4) {
+      std::cerr << "usage: doptsel build <config> <out.kbf>\n";
+      return kExitUsage;
+    }
+    return cmd_build(argv[2], argv[3]);
+  }
+  if (cmd == "evaluate" || cmd == "bench") {
     std::cerr << "error: `" << cmd << "` is outside the selection hot path served by this build "
                  "(use the reference tool)\n";
     return kExitUsage;

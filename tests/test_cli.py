@@ -26,7 +26,9 @@ def test_usage_and_argument_errors(tmp_path):
     assert run("select", wave, "--budget", "2", "--mode", "naive").returncode == 1
     assert run("select", wave, "--budget", "2", "--precision", "f32").returncode == 1
     assert run("select", wave, "--budget", "2", "--mode", "bogus").returncode == 1
-    assert run("build", "x.cfg", "y.kbf").returncode == 1
+    assert run("build", "only_one_arg.cfg").returncode == 1
+    assert run("build", os.path.join(GOLD, "configs", "bad_key.cfg"), str(tmp_path / "y.kbf")).returncode == 1
+    assert run("build", str(tmp_path / "missing.cfg"), str(tmp_path / "y.kbf")).returncode == 3
 
 
 def test_io_errors_exit_3(tmp_path):
@@ -98,3 +100,26 @@ def test_select_variants(tmp_path, extra):
             str(tmp_path / "o"))
     assert r.returncode == 0, r.stderr
     assert json.load(open(tmp_path / "o" / "selection.json"))["chosen"] == w["chosen"]
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not gpu_available(), reason="needs a CUDA GPU")
+def test_build_on_gpu_then_select(tmp_path):
+    """`doptsel build` assembles K on the GPU: the KBF file is byte-identical to the
+    reference's; `select --config` on it reports the reference normalized objective
+    (the config's default noise level needs the full wave model)."""
+    import hashlib
+
+    lti = json.load(open(os.path.join(GOLD, "lti.json")))["configs"]
+    for name in ("wave_benchmark.cfg", "weighted.cfg", "identity_prior.cfg"):
+        kbf = tmp_path / (name + ".kbf")
+        r = run("build", os.path.join(GOLD, "configs", name), str(kbf))
+        assert r.returncode == 0, r.stderr
+        assert hashlib.sha256(kbf.read_bytes()).hexdigest() == lti[name]["kbf_sha256"]
+    out = tmp_path / "out"
+    r = run("select", str(tmp_path / "wave_benchmark.cfg.kbf"), "--budget", "12", "--config",
+            os.path.join(GOLD, "configs", "wave_benchmark.cfg"), "--out", str(out))
+    assert r.returncode == 0, r.stderr
+    sel = json.load(open(out / "selection.json"))
+    assert sel["chosen"] == lti["wave_benchmark.cfg"]["chosen"]
+    assert abs(sel["objective_normalized_final"] - 1045.5268963527164) < 1e-6
