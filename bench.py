@@ -379,7 +379,7 @@ def our_arm(args, world, rank, local):
     if cpu is not None:
         line["cpu_baseline"] = cpu
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
 
 
 # ------------------------------------------------------------------------- #
@@ -424,8 +424,8 @@ def reference_arm(args, world, rank, local):
     from oracle import oracle as O
 
     if not O.ref_available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built "
-                          "(needs /root/reference at build time)"}))
+        emit({"impl": "reference", "unavailable": "oracle/_ref not built "
+                                                  "(needs /root/reference at build time)"})
         return
     w = workload(args.config, 1)
     nd, nt, vrank, budget = w["nd"], w["nt"], w["rank"], w["budget"]
@@ -461,7 +461,17 @@ def reference_arm(args, world, rank, local):
             "impl": "reference", "cpu_baseline": cpu,
             "e2e": {"value": round(value, 3), "unit": "s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+_STDOUT_FD = None
+
+
+def emit(line: dict) -> None:
+    """The one JSON line, on the real stdout (everything else -- NCCL's
+    version banner, library chatter -- was redirected to stderr)."""
+    fd = _STDOUT_FD if _STDOUT_FD is not None else 1
+    os.write(fd, (json.dumps(line) + "\n").encode())
 
 
 def main():
@@ -480,6 +490,10 @@ def main():
     ap.add_argument("--no-variants", action="store_true",
                     help="skip measuring the other algorithm beside the primary")
     args = ap.parse_args()
+    global _STDOUT_FD
+    sys.stdout.flush()
+    _STDOUT_FD = os.dup(1)
+    os.dup2(2, 1)  # C-level writes to stdout (NCCL init banner) go to stderr
     world, rank, local = dist_init()
     if args.impl == "reference":
         reference_arm(args, world, rank, local)
