@@ -58,6 +58,7 @@ struct Fail {
   } while (0)
 
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+constexpr int kWsGroupDefault = 16;  // column tiles per update rasterization group
 
 template <class T>
 T* dmalloc(size_t count, uint64_t& total) {
@@ -109,6 +110,9 @@ struct dsel_engine {
   int* d_sym = nullptr;  // [first_rt per column tile | group prefix]
   int* h_sym = nullptr;  // pinned
   int sym_tiles = 0;
+  int ws_br = 128;  // update-kernel tile height: 128 (ws::Big, 1 CTA/SM) or 64 (ws::Pair, 2 CTAs/SM)
+  int ws_cfg = -1;   // -1 auto (Big for short k, Big4 from 16 k-chunks), 0 ws::Big, 1 ws::Pair, 2 ws::Big4
+  int ws_group = kWsGroupDefault;  // column tiles per rasterization group
   double gen_flops = 0.0;  // last dsel_gen_synthetic_device (K formation on the update kernel)
   bool keep = false, export_factor = false;
   double tau = 1e-9;
@@ -349,25 +353,28 @@ void set_smem_limits(int dev) {
   allow_smem(schur_update_kernel<1>, optin);
   allow_smem(panel_w_kernel<2>, optin);
   allow_smem(panel_w_kernel<1>, optin);
-  allow_smem(schur_update_ws_kernel, optin);
+  allow_smem(schur_update_ws_kernel<ws::Big>, optin);
+  allow_smem(schur_update_ws_kernel<ws::Pair>, optin);
+  allow_smem(schur_update_ws_kernel<ws::Big4>, optin);
+  CU(cudaFuncSetAttribute(schur_update_ws_kernel<ws::Pair>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                          (int)cudaSharedmemCarveoutMaxShared));
   allow_smem(ll_gemm_kernel, optin);
   allow_smem(trinv_smem_kernel<4>, optin);
   allow_smem(trinv_smem_kernel<8>, optin);
   allow_smem(trinv_smem_kernel<14>, optin);
 }
 
-constexpr int ws_group = 16;
 
 // Wave balancing for a persistent launch over n_tiles equal tiles of n_k
 // k-chunks: the first n_full tiles run whole, the rest are split into s
 // k-ranges. Picks (n_full, s) minimising the modelled time: waves of whole
 // tiles + the split tail + the partial-plane round trip (write + reduce).
-void ws_balance(int n_tiles, int n_k, int sms, int max_s, int& n_full, int& split_s) {
+void ws_balance(int n_tiles, int n_k, int sms, int max_s, int br, int& n_full, int& split_s) {
   n_full = n_tiles;
   split_s = 1;
   if (max_s <= 1 || n_tiles <= 0 || n_k < 2) return;
-  const double t_chunk = 1.1e-6, t_tile0 = 2.0e-6;           // per k-chunk / per tile (s)
-  const double t_plane = (double)ws::BR * ws::BC * 8 * 2 / 6.0e12;  // partial write + read
+  const double t_chunk = 1.1e-6 * br / 128, t_tile0 = 2.0e-6;  // per k-chunk / per tile (s)
+  const double t_plane = (double)br * ws::BC * 8 * 2 / 6.0e12;    // partial write + read
   const double t_full = n_k * t_chunk + t_tile0;
   double best = ((n_tiles + sms - 1) / sms) * t_full;
   for (int f = 0; f * sms < n_tiles; ++f) {
@@ -385,23 +392,46 @@ void ws_balance(int n_tiles, int n_k, int sms, int max_s, int& n_full, int& spli
   }
 }
 
+// Launch the persistent update kernel in the engine's configuration (grid =
+// resident CTAs, capped by the number of work units).
+void launch_ws(dsel_engine* e, UpdateWSArgs& ua) {
+  ua.br = e->ws_br;
+  const long long units = (long long)ua.n_full + (long long)(ua.n_tiles - ua.n_full) * ua.split_s;
+  if (units <= 0) return;
+  // 3 chunks x 2 stages pays fewer stage hand-offs on long k loops (left-looking,
+  // Nt = 420); 2 x 3 keeps the producer further ahead on short ones (Nt = 128)
+  const int cfg = e->ws_cfg >= 0 ? e->ws_cfg : (ua.n_k >= 16 ? 2 : 0);
+  if (cfg == 1) {
+    const int grid = (int)std::min<long long>(2LL * e->n_sms, units);
+    schur_update_ws_kernel<ws::Pair><<<grid, ws::Pair::THREADS, ws::Pair::SMEM, e->s>>>(ua);
+  } else if (cfg == 2) {
+    const int grid = (int)std::min<long long>(e->n_sms, units);
+    schur_update_ws_kernel<ws::Big4><<<grid, ws::Big4::THREADS, ws::Big4::SMEM, e->s>>>(ua);
+  } else {
+    const int grid = (int)std::min<long long>(e->n_sms, units);
+    schur_update_ws_kernel<ws::Big><<<grid, ws::Big::THREADS, ws::Big::SMEM, e->s>>>(ua);
+  }
+  CU(cudaGetLastError());
+}
+
 // Block-lower tile schedule of the update (symmetric storage): first needed row
 // tile per column tile and the tile-id prefix per 16-column-tile group.
 void sym_tables(dsel_engine* e) {
   const int nt = e->nt, R = e->n_rows_tab, Rl = e->n_cols_tab;
   const int* cg = e->h_tab + e->nc + e->nloc;
   const int n_rows = R * nt, n_cols = Rl * nt;
-  const int nrt = (n_rows + ws::BR - 1) / ws::BR, nct = (n_cols + ws::BC - 1) / ws::BC;
-  const int ng = (nct + ws_group - 1) / ws_group;
+  const int br = e->ws_br;
+  const int nrt = (n_rows + br - 1) / br, nct = (n_cols + ws::BC - 1) / ws::BC;
+  const int ng = (nct + e->ws_group - 1) / e->ws_group;
   int* fr = e->h_sym;
   int* gp = e->h_sym + nct;
   for (int ct = 0; ct < nct; ++ct) {
     const int h = (ct * ws::BC) / nt;
-    fr[ct] = (cg[h] * nt) / ws::BR;
+    fr[ct] = (cg[h] * nt) / br;
   }
   gp[0] = 0;
   for (int g = 0; g < ng; ++g) {
-    const int ct0 = g * ws_group, gw = std::min(ws_group, nct - ct0);
+    const int ct0 = g * e->ws_group, gw = std::min(e->ws_group, nct - ct0);
     gp[g + 1] = gp[g] + (nrt - fr[ct0]) * gw;
   }
   e->sym_tiles = gp[ng];
@@ -555,24 +585,22 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
       ua.nt = nt;
       ua.n_rows = nt;
       ua.n_cols = n_rows;
-      ua.n_row_tiles = (nt + ws::BR - 1) / ws::BR;
+      ua.n_row_tiles = (nt + e->ws_br - 1) / e->ws_br;
       ua.n_col_tiles = (n_rows + ws::BC - 1) / ws::BC;
-      ua.group = ws_group;
+      ua.group = e->ws_group;
       ua.sym = 0;
       ua.n_tiles = ua.n_row_tiles * ua.n_col_tiles;
       ua.cout = e->cbuf;
       ua.ldo = e->ldo;
       ua.mpad_c = e->own_mpad;
       // wave balancing: the tiles past the last full wave are split along k
-      ws_balance(ua.n_tiles, ua.n_k, e->n_sms, e->cpart ? kLLMaxSplits : 1, ua.n_full, ua.split_s);
+      ws_balance(ua.n_tiles, ua.n_k, e->n_sms * (e->ws_br == 64 ? 2 : 1), e->cpart ? kLLMaxSplits : 1,
+                 e->ws_br, ua.n_full, ua.split_s);
       ua.part = e->cpart;
       ua.part_stride = (long long)e->ldo * nt;
-      const int n_units = ua.n_full + (ua.n_tiles - ua.n_full) * ua.split_s;
-      const int grid = std::min(e->n_sms, n_units);
-      schur_update_ws_kernel<<<grid, ws::THREADS, ws::SMEM, e->s>>>(ua);
-      CU(cudaGetLastError());
+      launch_ws(e, ua);
       if (ua.split_s > 1) {
-        const long long total = (long long)(ua.n_tiles - ua.n_full) * ws::BR * ws::BC;
+        const long long total = (long long)(ua.n_tiles - ua.n_full) * e->ws_br * ws::BC;
         ws_split_reduce_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 8), 256, 0,
                                  e->s>>>(ua);
         CU(cudaGetLastError());
@@ -880,18 +908,17 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       ua.nt = nt;
       ua.n_rows = n_rows;
       ua.n_cols = n_cols;
-      ua.n_row_tiles = (n_rows + ws::BR - 1) / ws::BR;
+      ua.n_row_tiles = (n_rows + e->ws_br - 1) / e->ws_br;
       ua.n_col_tiles = (n_cols + ws::BC - 1) / ws::BC;
-      ua.group = ws_group;
+      ua.group = e->ws_group;
       ua.sym = e->sym;
       ua.first_rt = e->d_sym;
       ua.gprefix = e->d_sym + ua.n_col_tiles;
-      ua.n_groups = (ua.n_col_tiles + ws_group - 1) / ws_group;
+      ua.n_groups = (ua.n_col_tiles + e->ws_group - 1) / e->ws_group;
       ua.n_tiles = e->sym ? e->sym_tiles : ua.n_row_tiles * ua.n_col_tiles;
       ua.n_full = ua.n_tiles;
       ua.split_s = 1;
-      const int grid = (int)std::min<long long>(e->n_sms, ua.n_tiles);
-      schur_update_ws_kernel<<<grid, ws::THREADS, ws::SMEM, e->s>>>(ua);
+      launch_ws(e, ua);
     } else {
       UpdateArgs ua{};
       ua.C = e->C;
@@ -1073,6 +1100,9 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     e->stream = cfg->storage == DSEL_STORAGE_STREAM;
     if (cfg->algorithm < 0 || cfg->algorithm > 1) throw Fail{DSEL_E_INVALID, "unknown algorithm"};
     e->sym = cfg->full_square == 0 && e->nt % 2 == 0 && !e->ll;
+    if (const char* wc = getenv("DSEL_WS_CFG")) e->ws_cfg = std::max(-1, std::min(2, atoi(wc)));
+    e->ws_br = e->ws_cfg == 1 ? 64 : 128;
+    if (const char* wg = getenv("DSEL_WS_GROUP")) e->ws_group = std::max(1, atoi(wg));
     if ((e->G > 1 || e->sym) && !e->ll) e->Pbuf = dmalloc<double>((size_t)e->n * e->nt, tot);
     if (e->ll) {
       const int B = std::max(e->eff_budget, 1);
@@ -1100,7 +1130,7 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     }
     {
       const size_t nct = (size_t)(e->nloc * e->nt + ws::BC - 1) / ws::BC + 2;
-      const size_t nsym = nct + nct / ws_group + 4;
+      const size_t nsym = nct + nct / e->ws_group + 4;
       e->d_sym = dmalloc<int>(nsym, tot);
       CU(cudaMallocHost(&e->h_sym, sizeof(int) * nsym));
     }
@@ -1673,18 +1703,17 @@ dsel_status dsel_gen_synthetic_device(dsel_engine* e, int rank, double sigma, ui
       ua.nt = nt;
       ua.n_rows = n_rows;
       ua.n_cols = n_cols;
-      ua.n_row_tiles = (n_rows + ws::BR - 1) / ws::BR;
+      ua.n_row_tiles = (n_rows + e->ws_br - 1) / e->ws_br;
       ua.n_col_tiles = (n_cols + ws::BC - 1) / ws::BC;
-      ua.group = ws_group;
+      ua.group = e->ws_group;
       ua.sym = sym;
       ua.first_rt = e->d_sym;
       ua.gprefix = sym ? e->d_sym + ua.n_col_tiles : nullptr;
-      ua.n_groups = (ua.n_col_tiles + ws_group - 1) / ws_group;
+      ua.n_groups = (ua.n_col_tiles + e->ws_group - 1) / e->ws_group;
       ua.n_tiles = sym ? e->sym_tiles : ua.n_row_tiles * ua.n_col_tiles;
       ua.n_full = ua.n_tiles;
       ua.split_s = 1;
-      const int grid = (int)std::min<long long>(e->n_sms, ua.n_tiles);
-      schur_update_ws_kernel<<<grid, ws::THREADS, ws::SMEM, e->s>>>(ua);
+      launch_ws(e, ua);
       ce = cudaGetLastError();
       gen_flops += 2.0 * kch * (sym ? 0.5 * (double)n_rows * (n_cols + nt) : (double)n_rows * n_cols);
     }

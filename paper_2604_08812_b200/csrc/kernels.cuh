@@ -296,22 +296,37 @@ __global__ void __launch_bounds__(upd::THREADS, 1) schur_update_kernel(UpdateArg
 // mainloop, so the C traffic (AI = nt/8 flop/B) hides behind the math.     //
 // ------------------------------------------------------------------------ //
 namespace ws {
-constexpr int BR = 128, BC = 64, KC = 16;
-constexpr int SC = 2;      // k-chunks per pipeline stage (one mbarrier round per 32 k)
-constexpr int STAGES = 3;
-constexpr int CONSUMERS = 256, THREADS = CONSUMERS + 32;
-constexpr int CP = BR + 8;  // C tile column pitch (doubles): conflict-free LDS.128
-constexpr size_t OFF_R = 0;
-constexpr size_t OFF_C = OFF_R + (size_t)STAGES * SC * BR * KC * 8;
-constexpr size_t OFF_CT = OFF_C + (size_t)STAGES * SC * BC * KC * 8;
-constexpr size_t OFF_MAPS = OFF_CT + (size_t)BC * CP * 8;  // 2 x {colbase[BC], rowphys[BR], cshift[BC]}
-constexpr size_t MAPS_BYTES = (size_t)BC * 8 + BR * 4 + BC * 4;
-constexpr size_t OFF_RUNS = OFF_MAPS + 2 * MAPS_BYTES;                   // producer scratch
-constexpr size_t OFF_BAR = OFF_RUNS + (size_t)(2 * BC + BR + 8) * 8;
+constexpr int BR = 128, BC = 64, KC = 16;  // BR: the largest tile height (row padding unit)
 constexpr int MAX_SYM_CT = 1024;  // column tiles whose schedule fits in shared memory
-constexpr size_t OFF_SYM = OFF_BAR + 16 * 8;
-constexpr size_t SMEM = OFF_SYM + (size_t)(MAX_SYM_CT + MAX_SYM_CT / 16 + 4) * 4;
-static_assert(SMEM <= 232448 - 64, "ws kernel shared memory");
+// One kernel configuration: BRT-row x 64-column tiles, (BRT/32) x 2 consumer
+// warps of 32 x 32, SCT k-chunks per pipeline stage, STG stages, MINB CTAs/SM.
+// Big: 128-row tiles, 8 consumer warps, 1 CTA/SM. Pair: 64-row tiles, 4
+// consumer warps, 2 CTAs/SM -- the two CTAs drift apart, so one's tile
+// prologue/epilogue (C tile in, results out) overlaps the other's DMMA loop.
+template <int BRT, int SCT, int STG, int MINBT>
+struct Cfg {
+  static constexpr int BR = BRT, SC = SCT, STAGES = STG, MINB = MINBT;
+  static constexpr int RG = BRT / 32;  // warp rows
+  static constexpr int CONSUMERS = RG * 2 * 32, THREADS = CONSUMERS + 32;
+  static constexpr int CP = BRT + 8;  // C tile column pitch (doubles): conflict-free LDS.128
+  static constexpr size_t OFF_R = 0;
+  static constexpr size_t OFF_C = OFF_R + (size_t)STAGES * SC * BR * KC * 8;
+  static constexpr size_t OFF_CT = OFF_C + (size_t)STAGES * SC * BC * KC * 8;
+  static constexpr size_t OFF_MAPS = OFF_CT + (size_t)BC * CP * 8;  // 2 x {colbase, rowphys, cshift}
+  static constexpr size_t MAPS_BYTES = (size_t)BC * 8 + BR * 4 + BC * 4;
+  static constexpr size_t OFF_RUNS = OFF_MAPS + 2 * MAPS_BYTES;     // producer scratch
+  static constexpr size_t OFF_BAR = OFF_RUNS + (size_t)(2 * BC + BR + 8) * 8;
+  static constexpr size_t OFF_SYM = OFF_BAR + 16 * 8;
+  static constexpr size_t SMEM = OFF_SYM + (size_t)(MAX_SYM_CT + MAX_SYM_CT / 16 + 4) * 4;
+};
+using Big = Cfg<128, 2, 3, 1>;
+using Pair = Cfg<64, 2, 2, 2>;
+using Big4 = Cfg<128, 3, 2, 1>;
+static_assert(Big::SMEM <= 232448 - 2048, "ws kernel shared memory (1 CTA/SM)");
+static_assert(Big4::SMEM <= 232448 - 2048, "ws kernel shared memory (Big4)");
+static_assert(2 * (Pair::SMEM + 2048) <= 233472, "ws kernel shared memory (2 CTAs/SM)");
+constexpr int THREADS = Big::THREADS;
+constexpr size_t SMEM = Big::SMEM;
 }  // namespace ws
 
 __host__ __device__ __forceinline__ size_t wt_index(int row, int k, int mpad) {
@@ -354,6 +369,7 @@ struct UpdateWSArgs {
   int n_full, split_s;
   double* part;
   long long part_stride;
+  int br;  // tile height of the launched configuration (128 or 64)
 };
 
 // unit -> (tile, split z, k-chunk range)
@@ -383,7 +399,7 @@ __device__ __forceinline__ bool ws_tile(const UpdateWSArgs& a, const int* fr, co
     const int within = id - grp * gsz;
     const int ct0 = grp * a.group;
     const int gw = min(a.group, a.n_col_tiles - ct0);
-    r0 = (within / gw) * 128;
+    r0 = (within / gw) * a.br;
     c0 = (ct0 + within % gw) * 64;
     return true;
   }
@@ -398,7 +414,7 @@ __device__ __forceinline__ bool ws_tile(const UpdateWSArgs& a, const int* fr, co
   const int gw = min(a.group, a.n_col_tiles - ct0);
   const int rt = fr[ct0] + local / gw;
   const int ct = ct0 + local % gw;
-  r0 = rt * 128;
+  r0 = rt * a.br;
   c0 = ct * 64;
   return rt >= fr[ct];
 }
@@ -463,8 +479,15 @@ __device__ __forceinline__ void ws_chunk(double (&acc)[4][4][2], const double* t
   }
 }
 
-__global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateWSArgs a) {
-  using namespace ws;
+template <class Cf>
+__global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(UpdateWSArgs a) {
+  using ws::BC;
+  using ws::KC;
+  using ws::MAX_SYM_CT;
+  constexpr int BR = Cf::BR, SC = Cf::SC, STAGES = Cf::STAGES, CONSUMERS = Cf::CONSUMERS, CP = Cf::CP;
+  constexpr size_t OFF_R = Cf::OFF_R, OFF_C = Cf::OFF_C, OFF_CT = Cf::OFF_CT, OFF_MAPS = Cf::OFF_MAPS,
+                   MAPS_BYTES = Cf::MAPS_BYTES, OFF_RUNS = Cf::OFF_RUNS, OFF_BAR = Cf::OFF_BAR,
+                   OFF_SYM = Cf::OFF_SYM;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sR = reinterpret_cast<double*>(smem_raw + OFF_R);
   double* sCc = reinterpret_cast<double*>(smem_raw + OFF_C);
@@ -499,7 +522,7 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
   int* sgp = sfr + MAX_SYM_CT;
   const int* fr = a.first_rt;
   const int* gp = a.gprefix;
-  if (a.sym && a.n_col_tiles <= MAX_SYM_CT) {
+  if (a.sym && a.n_col_tiles <= MAX_SYM_CT && a.n_groups + 1 <= MAX_SYM_CT / 16 + 4) {
     for (int i = threadIdx.x; i < a.n_col_tiles; i += blockDim.x) sfr[i] = a.first_rt[i];
     for (int i = threadIdx.x; i <= a.n_groups; i += blockDim.x) sgp[i] = a.gprefix[i];
     fr = sfr;
@@ -678,8 +701,8 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
 
   // ================================ consumers ================================
   const int g = lane >> 2, t = lane & 3;
-  const int wr = (warp & 3) * 32;   // r-side offset of this warp
-  const int wc = (warp >> 2) * 32;  // c-side offset of this warp
+  const int wr = (warp % Cf::RG) * 32;  // r-side offset of this warp
+  const int wc = (warp / Cf::RG) * 32;  // c-side offset of this warp
   int stage = 0;
   unsigned fphase = 0;
   int it = 0;
@@ -770,9 +793,9 @@ __global__ void __launch_bounds__(ws::THREADS, 1) schur_update_ws_kernel(UpdateW
 // Split units of the balanced left-looking GEMM: cout = sum_z part_z over
 // the tiles >= n_full, z in order (deterministic for a given rank count).
 __global__ void ws_split_reduce_kernel(UpdateWSArgs a) {
-  using namespace ws;
+  using ws::BC;
   const int n_split_tiles = a.n_tiles - a.n_full;
-  const long long per = (long long)BR * BC;
+  const long long per = (long long)a.br * BC;
   const long long total = per * n_split_tiles;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
