@@ -456,3 +456,26 @@ def test_assemble_lti_bit_exact(dsel, golden_dir, name):
         assert hashlib.sha256(hdr + k.astype("<f8").tobytes()).hexdigest() == g["kbf_sha256"], kw
         assert np.array_equal(nl, np.array(g["noise_logdets"]))
         assert_trace_matches(rows, g["chosen"], g["gains"], g["objectives"])
+
+
+# ---- GPU refactorizing baseline + complexity sweep ----- #
+def test_naive_refactorizing_baseline_gpu(O, golden_dir):
+    """naive_select (selector.hpp:253-348) on the GPU picks the reference
+    sequence; the complexity sweep runs and its rows are well-formed."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(golden_dir), "..", "tools"))
+    import complexity_gpu as cg
+
+    w = json.load(open(os.path.join(golden_dir, "wave.json")))
+    k, nd, nt = O.read_kbf(os.path.join(golden_dir, "wave.kbf"))
+    chosen, gains, objs = cg.naive_select_gpu(k, nd, nt, 12)
+    assert chosen == w["chosen"]
+    for g, want in zip(gains, w["gains"]):
+        assert abs(g - want) <= 1e-8 * max(abs(want), 1.0)
+    c = json.load(open(os.path.join(golden_dir, "random.json")))["cases"][6]
+    kr = O.random_hessian(c["n_sensors"], c["n_steps"], c["gamma"], c["rank"], c["seed"])
+    chosen, _, _ = cg.naive_select_gpu(kr, c["n_sensors"], c["n_steps"], c["budget"], chunk=5)
+    assert chosen == c["chosen"]
+    rows, slopes = cg.sweep(nt=8, k_max=12, step=4, reps=2, batch=4)
+    assert [r["k"] for r in rows] == [4, 8, 12]
+    assert all(r["naive_ms"] > 0 and r["schur_ms"] > 0 and r["engine_round_ms"] > 0 for r in rows)
