@@ -20,6 +20,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cerrno>
 #include <thread>
 #include <cmath>
@@ -59,6 +60,40 @@ struct Fail {
 
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 constexpr int kWsGroupDefault = 16;  // column tiles per update rasterization group
+// DEBUG probes (DSEL_PROBE=1): GPU events + host times at named points of a round
+struct Probe {
+  bool on = getenv("DSEL_PROBE") != nullptr;
+  cudaEvent_t ev[16];
+  double host[16];
+  const char* name[16];
+  int n = 0;
+  bool init = false;
+  void mark(const char* nm, cudaStream_t st) {
+    if (!on || n >= 16) return;
+    if (!init) {
+      for (auto& x : ev) cudaEventCreate(&x);
+      init = true;
+    }
+    cudaEventRecord(ev[n], st);
+    host[n] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    name[n++] = nm;
+  }
+  void dump(int rank) {
+    if (!on || n < 2) { n = 0; return; }
+    cudaEventSynchronize(ev[n - 1]);
+    if (rank == 0) {
+      fprintf(stderr, "[probe]");
+      for (int i = 1; i < n; ++i) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+        fprintf(stderr, " %s:%.0f/%.0f", name[i], ms * 1e3, host[i] - host[i - 1]);
+      }
+      fprintf(stderr, "\n");
+    }
+    n = 0;
+  }
+};
+Probe g_probe;
 
 template <class T>
 T* dmalloc(size_t count, uint64_t& total) {
@@ -110,6 +145,26 @@ struct dsel_engine {
   int* d_sym = nullptr;  // [first_rt per column tile | group prefix]
   int* h_sym = nullptr;  // pinned
   int sym_tiles = 0;
+  // symmetric storage on G > 1: W rows solved by the rank holding each block of
+  // C[:,k] (hb = holder-ordered compact blocks, hb_off = per-rank segments),
+  // exchanged by grouped broadcasts (all-gather-v) and scattered into Wt/Wnt
+  double *Wsend = nullptr, *Wrecv = nullptr;
+  int *d_hb = nullptr, *d_hbpos = nullptr, *h_hb = nullptr;
+  std::vector<int> hb_off;
+  int* d_hboff = nullptr;  // device copy of hb_off (G + 1)
+  // NVLink peer memory (symmetric storage, G > 1): peers' Wsend / gain
+  // scratch (L_k) / round flags mapped into this process (CUDA IPC across
+  // processes, peer access within one), so the W exchange is one kernel that
+  // reads the holders' rows over NVLink and scatters them (no NCCL call), and
+  // L_k^-1 reads the owner's factor in place
+  bool p2p = false;
+  unsigned long long* flag = nullptr;  // this rank's published round sequence
+  unsigned long long seq = 0;
+  std::vector<double*> peer_wsend, peer_lscr;
+  std::vector<unsigned long long*> peer_flag;
+  std::vector<void*> ipc_opened;
+  const double** d_peer_wsend = nullptr;
+  unsigned long long** d_peer_flag = nullptr;
   int ws_br = 128;  // update-kernel tile height: 128 (ws::Big, 1 CTA/SM) or 64 (ws::Pair, 2 CTAs/SM)
   int ws_cfg = -1;   // -1 auto (Big for short k, Big4 from 16 k-chunks), 0 ws::Big, 1 ws::Pair, 2 ws::Big4
   int ws_group = kWsGroupDefault;  // column tiles per rasterization group
@@ -126,6 +181,9 @@ struct dsel_engine {
          *stage = nullptr, *xbuf = nullptr;
   int *status = nullptr, *kstatus = nullptr;
   int *d_pos_sensor = nullptr, *d_slot_sensor = nullptr;
+  int* d_round = nullptr;  // per-round tables (one block, one upload): d_tab | d_sym | d_hb
+  int* h_round = nullptr;  // pinned staging of the same layout
+  size_t round_ints = 0;
   int* d_tab = nullptr;  // [row_pos nc | col_slot nloc | col_g nloc]
   ArgRec *d_rec = nullptr, *d_recs = nullptr;
   ArgRec* h_recs = nullptr;  // pinned
@@ -158,7 +216,7 @@ struct dsel_engine {
 
 namespace {
 
-void build_tables(dsel_engine* e) {
+void build_tables(dsel_engine* e, bool upload = true) {
   // compact global live list (ascending position) and local live list
   int* rp = e->h_tab;
   int* cs = e->h_tab + e->nc;
@@ -175,8 +233,14 @@ void build_tables(dsel_engine* e) {
   }
   e->n_rows_tab = R;
   e->n_cols_tab = Rl;
-  CU(cudaMemcpyAsync(e->d_tab, e->h_tab, sizeof(int) * (size_t)(e->nc + 2 * e->nloc),
-                     cudaMemcpyHostToDevice, e->s));
+  if (upload)
+    CU(cudaMemcpyAsync(e->d_tab, e->h_tab, sizeof(int) * (size_t)(e->nc + 2 * e->nloc),
+                       cudaMemcpyHostToDevice, e->s));
+}
+
+// every per-round table (row/col, tile schedule, holder lists) in one copy
+void upload_round(dsel_engine* e) {
+  CU(cudaMemcpyAsync(e->d_round, e->h_round, sizeof(int) * e->round_ints, cudaMemcpyHostToDevice, e->s));
 }
 
 }  // namespace
@@ -392,6 +456,106 @@ void ws_balance(int n_tiles, int n_k, int sms, int max_s, int br, int& n_full, i
   }
 }
 
+// Map the peers' Wsend, gain scratch and round flag (NVLink peer memory). All
+// ranks take the same decision (min-reduced), since the per-round collective
+// sequence depends on it. DSEL_P2P=0 keeps the NCCL exchange.
+struct PeerInfo {
+  cudaIpcMemHandle_t h_wsend, h_lscr, h_flag;
+  long long pid;
+  int dev;
+  int ok;
+  void *p_wsend, *p_lscr, *p_flag;
+};
+
+void setup_p2p(dsel_engine* e) {
+  const int G = e->G;
+  CU(cudaMalloc(&e->flag, 256));
+  CU(cudaMemset(e->flag, 0, 256));
+  PeerInfo mine{};
+  mine.pid = (long long)getpid();
+  mine.dev = e->dev;
+  mine.p_wsend = e->Wsend;
+  mine.p_lscr = e->Lscr;
+  mine.p_flag = e->flag;
+  const char* env = getenv("DSEL_P2P");
+  mine.ok = !(env && atoi(env) == 0);
+  if (mine.ok) {
+    mine.ok = cudaIpcGetMemHandle(&mine.h_wsend, e->Wsend) == cudaSuccess &&
+              cudaIpcGetMemHandle(&mine.h_lscr, e->Lscr) == cudaSuccess &&
+              cudaIpcGetMemHandle(&mine.h_flag, e->flag) == cudaSuccess;
+    cudaGetLastError();
+  }
+  PeerInfo* d_info = nullptr;
+  CU(cudaMalloc(&d_info, sizeof(PeerInfo) * (G + 1)));
+  CU(cudaMemcpy(d_info + G, &mine, sizeof(PeerInfo), cudaMemcpyHostToDevice));
+  NC(ncclAllGather(d_info + G, d_info, sizeof(PeerInfo), ncclUint8, e->comm, e->s));
+  std::vector<PeerInfo> all(G);
+  CU(cudaMemcpyAsync(all.data(), d_info, sizeof(PeerInfo) * G, cudaMemcpyDeviceToHost, e->s));
+  CU(cudaStreamSynchronize(e->s));
+  cudaFree(d_info);
+  int ok = 1;
+  for (const auto& x : all) ok &= x.ok;
+  e->peer_wsend.assign(G, nullptr);
+  e->peer_lscr.assign(G, nullptr);
+  e->peer_flag.assign(G, nullptr);
+  for (int r = 0; r < G && ok; ++r) {
+    if (r == e->rank) {
+      e->peer_wsend[r] = e->Wsend;
+      e->peer_lscr[r] = e->Lscr;
+      e->peer_flag[r] = e->flag;
+      continue;
+    }
+    if (all[r].pid == mine.pid) {  // same process (thread per GPU): peer access
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, e->dev, all[r].dev);
+      const cudaError_t pe = can ? cudaDeviceEnablePeerAccess(all[r].dev, 0) : cudaErrorPeerAccessUnsupported;
+      cudaGetLastError();
+      if (!can || (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled)) {
+        ok = 0;
+        break;
+      }
+      e->peer_wsend[r] = static_cast<double*>(all[r].p_wsend);
+      e->peer_lscr[r] = static_cast<double*>(all[r].p_lscr);
+      e->peer_flag[r] = static_cast<unsigned long long*>(all[r].p_flag);
+    } else {  // another process: CUDA IPC
+      void *a = nullptr, *b = nullptr, *c = nullptr;
+      if (cudaIpcOpenMemHandle(&a, all[r].h_wsend, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess)
+        e->ipc_opened.push_back(a);
+      if (cudaIpcOpenMemHandle(&b, all[r].h_lscr, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess)
+        e->ipc_opened.push_back(b);
+      if (cudaIpcOpenMemHandle(&c, all[r].h_flag, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess)
+        e->ipc_opened.push_back(c);
+      cudaGetLastError();
+      if (!a || !b || !c) {
+        ok = 0;
+        break;
+      }
+      e->peer_wsend[r] = static_cast<double*>(a);
+      e->peer_lscr[r] = static_cast<double*>(b);
+      e->peer_flag[r] = static_cast<unsigned long long*>(c);
+    }
+  }
+  // every rank must agree
+  int* d_ok = nullptr;
+  CU(cudaMalloc(&d_ok, sizeof(int)));
+  CU(cudaMemcpy(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice));
+  NC(ncclAllReduce(d_ok, d_ok, 1, ncclInt, ncclMin, e->comm, e->s));
+  CU(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, e->s));
+  CU(cudaStreamSynchronize(e->s));
+  cudaFree(d_ok);
+  e->p2p = ok != 0;
+  if (!e->p2p) {
+    for (void* ptr : e->ipc_opened) cudaIpcCloseMemHandle(ptr);
+    e->ipc_opened.clear();
+    return;
+  }
+  CU(cudaMalloc(&e->d_peer_wsend, sizeof(double*) * G));
+  CU(cudaMalloc(&e->d_peer_flag, sizeof(unsigned long long*) * G));
+  CU(cudaMemcpy(e->d_peer_wsend, e->peer_wsend.data(), sizeof(double*) * G, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(e->d_peer_flag, e->peer_flag.data(), sizeof(unsigned long long*) * G,
+                cudaMemcpyHostToDevice));
+}
+
 // Launch the persistent update kernel in the engine's configuration (grid =
 // resident CTAs, capped by the number of work units).
 void launch_ws(dsel_engine* e, UpdateWSArgs& ua) {
@@ -416,7 +580,7 @@ void launch_ws(dsel_engine* e, UpdateWSArgs& ua) {
 
 // Block-lower tile schedule of the update (symmetric storage): first needed row
 // tile per column tile and the tile-id prefix per 16-column-tile group.
-void sym_tables(dsel_engine* e) {
+void sym_tables(dsel_engine* e, bool upload = true) {
   const int nt = e->nt, R = e->n_rows_tab, Rl = e->n_cols_tab;
   const int* cg = e->h_tab + e->nc + e->nloc;
   const int n_rows = R * nt, n_cols = Rl * nt;
@@ -435,8 +599,9 @@ void sym_tables(dsel_engine* e) {
     gp[g + 1] = gp[g] + (nrt - fr[ct0]) * gw;
   }
   e->sym_tiles = gp[ng];
-  CU(cudaMemcpyAsync(e->d_sym, e->h_sym, sizeof(int) * (size_t)(nct + ng + 1),
-                     cudaMemcpyHostToDevice, e->s));
+  if (upload)
+    CU(cudaMemcpyAsync(e->d_sym, e->h_sym, sizeof(int) * (size_t)(nct + ng + 1),
+                       cudaMemcpyHostToDevice, e->s));
 }
 
 // left-looking split-K: one split per 64 k-chunks (1024 k), at most 8 splits;
@@ -805,29 +970,67 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   }
   e->alive[p] = 0;
   e->n_alive -= 1;
-  build_tables(e);
+  g_probe.mark("pre", e->s);
+  build_tables(e, !(e->sym && !last));  // symmetric rounds upload all tables at once below
   const int R = e->n_rows_tab, Rl = e->n_cols_tab;
+  g_probe.mark("tables", e->s);
   if (!last && e->sym) {
     // symmetric storage: column k of C assembled from the block-lower panels
     // (own blocks from panel k, the rest transposed from panels i < k), summed
     // across ranks (each block has exactly one nonzero contributor)
     P = e->Pbuf;
-    if (e->G > 1) CU(cudaMemsetAsync(e->Pbuf, 0, sizeof(double) * (size_t)e->n * nt, e->s));
-    if (R > 0) {
-      const long long total = (long long)R * nt * nt;
+    const int* gpos = e->row_pos();
+    int n_gather = R;
+    if (e->G > 1) {
+      // only L_k crosses ranks here; each rank solves W for the blocks of C[:,k]
+      // it holds (rows p_i > p_k in panel k at its owner, the rest transposed
+      // from panel i at i's owner) and the rows are exchanged after the solve
+      if (e->p2p) {
+        // L_k^-1 reads the owner's factor in place (its gain kernel finished
+        // before its argmax all-gather, which this rank has seen complete)
+        if (owner != e->rank) {
+          int bidx = 0;
+          for (int qq = 0; qq < q; ++qq) bidx += e->alive[(size_t)qq * e->G + owner] ? 1 : 0;
+          Lk = e->peer_lscr[owner] + (size_t)bidx * nt * nt;
+        }
+      } else {
+        NC(ncclBroadcast(e->Lk, e->Lk, (size_t)nt * nt, ncclDouble, owner, e->comm, e->s));
+        bytes += (uint64_t)nt * nt * sizeof(double) * (uint64_t)(e->G - 1);
+        Lk = e->Lk;
+      }
+      g_probe.mark("lkbc", e->s);
+      const int* rp = e->h_tab;
+      int* hb = e->h_hb;
+      int* hbpos = e->h_hb + e->nc;
+      e->hb_off.assign(e->G + 1, 0);
+      int m = 0;
+      for (int r = 0; r < e->G; ++r) {
+        e->hb_off[r] = m;
+        for (int h = 0; h < R; ++h) {
+          const int pos = rp[h];
+          if ((pos > p ? owner : pos % e->G) == r) {
+            hb[m] = h;
+            hbpos[m] = pos;
+            ++m;
+          }
+        }
+      }
+      e->hb_off[e->G] = m;
+      std::copy(e->hb_off.begin(), e->hb_off.end(), e->h_hb + 2 * (size_t)e->nc);
+      gpos = e->d_hbpos + e->hb_off[e->rank];
+      n_gather = e->hb_off[e->rank + 1] - e->hb_off[e->rank];
+      g_probe.mark("holders", e->s);
+    }
+    sym_tables(e, false);
+    upload_round(e);
+    if (n_gather > 0) {
+      const long long total = (long long)n_gather * nt * nt;
       gather_panel_sym_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 32), 256, 0,
-                                e->s>>>(e->C, e->n, nt, e->row_pos(), R, p, e->G, e->rank, e->Pbuf);
+                                e->s>>>(e->C, e->n, nt, gpos, n_gather, p, e->G, e->rank, e->Pbuf);
       CU(cudaGetLastError());
       e->launches += 1;
     }
-    if (e->G > 1) {
-      NC(ncclGroupStart());
-      NC(ncclAllReduce(e->Pbuf, e->Pbuf, (size_t)e->n * nt, ncclDouble, ncclSum, e->comm, e->s));
-      NC(ncclBroadcast(e->Lk, e->Lk, (size_t)nt * nt, ncclDouble, owner, e->comm, e->s));
-      NC(ncclGroupEnd());
-      bytes += (uint64_t)(2 * e->n + nt) * nt * sizeof(double) * (uint64_t)(e->G - 1) / e->G;
-    }
-    sym_tables(e);
+    g_probe.mark("gather", e->s);
   }
   double flops = 0.0;
   if (!last) {
@@ -852,7 +1055,70 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
     }
     CU(cudaGetLastError());
     e->launches += 1;
-    if (R > 0) {
+    g_probe.mark("trinv", e->s);
+    const bool dist_w = e->sym && e->G > 1;
+    const int n_own_rows = dist_w ? (e->hb_off[e->rank + 1] - e->hb_off[e->rank]) * nt : R * nt;
+    if (dist_w && n_own_rows > 0) {
+      // W rows of the blocks this rank holds, packed (row-major, ld = ldw)
+      PanelArgs pa{};
+      pa.P = P;
+      pa.ldp = e->n;
+      pa.Linv = e->Linv;
+      pa.ldl = e->ldw;
+      pa.W = e->Wsend;
+      pa.ldw = e->ldw;
+      pa.row_pos = e->d_hbpos + e->hb_off[e->rank];
+      pa.nt = nt;
+      pa.n_rows = n_own_rows;
+      pa.G = e->G;
+      pa.rank = e->rank;
+      dim3 grid((pa.n_rows + pw::BR - 1) / pw::BR, (nt + pw::BN - 1) / pw::BN);
+      panel_w_kernel<2><<<grid, pw::THREADS, pw::SMEM, e->s>>>(pa);
+      CU(cudaGetLastError());
+      e->launches += 1;
+    }
+    g_probe.mark("panelw", e->s);
+    if (dist_w && e->p2p) {
+      // publish this round's rows, then one kernel reads every holder's rows
+      // over NVLink (after its flag) and scatters them into Wt/Wnt (+history).
+      // Every rank signals and waits for every peer each round: a peer's next
+      // gain kernel (which overwrites the L_k read above) and next W rows come
+      // after its wait on this rank's signal.
+      ++e->seq;
+      p2p_signal_kernel<<<1, 32, 0, e->s>>>(e->flag, e->seq);
+      const long long total = (long long)std::max(R, 0) * nt * nt;
+      w_peer_scatter_kernel<<<(unsigned)std::max<long long>(1, std::min<long long>((total / 2 + 255) / 256, 148 * 8)),
+                              256, 0, e->s>>>(
+          e->d_peer_wsend, e->d_peer_flag, e->seq, e->G, e->d_hboff, e->ldw, e->d_hb, e->row_pos(), R, nt,
+          e->Wt, e->Wnt, e->mpad, e->export_factor ? e->hist : nullptr, (long long)e->eff_budget * nt * nt,
+          (long long)round * nt * nt, e->rank);
+      CU(cudaGetLastError());
+      e->launches += 2;
+      for (int r = 0; r < e->G; ++r)
+        if (r != e->rank) bytes += (uint64_t)(e->hb_off[r + 1] - e->hb_off[r]) * nt * nt * sizeof(double);
+      g_probe.mark("p2p-scatter", e->s);
+    } else if (dist_w && R > 0) {
+      // all-gather-v of the W rows (one broadcast per holder), then scatter into
+      // the tiled update operands (+ the factor history of own candidates)
+      const size_t rowel = (size_t)nt * e->ldw;
+      NC(ncclGroupStart());
+      for (int r = 0; r < e->G; ++r) {
+        const size_t cnt = (size_t)(e->hb_off[r + 1] - e->hb_off[r]) * rowel;
+        if (cnt == 0) continue;
+        double* dst = e->Wrecv + (size_t)e->hb_off[r] * rowel;
+        NC(ncclBroadcast(r == e->rank ? e->Wsend : dst, dst, cnt, ncclDouble, r, e->comm, e->s));
+        if (r != e->rank) bytes += cnt * sizeof(double);
+      }
+      NC(ncclGroupEnd());
+      const long long total = (long long)R * nt * nt;
+      w_scatter_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 32), 256, 0, e->s>>>(
+          e->Wrecv, e->ldw, e->d_hb, e->row_pos(), R, nt, e->Wt, e->Wnt, e->mpad,
+          e->export_factor ? e->hist : nullptr, (long long)e->eff_budget * nt * nt, (long long)round * nt * nt,
+          e->G, e->rank);
+      CU(cudaGetLastError());
+      e->launches += 1;
+      g_probe.mark("bcast+scatter", e->s);
+    } else if (R > 0) {
       PanelArgs pa{};
       pa.P = P;
       pa.ldp = e->n;
@@ -891,7 +1157,9 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       e->launches += 1;
     }
   }
+  g_probe.mark("hist", e->s);
   CU(cudaEventRecord(ev[3], e->s));
+  g_probe.dump(e->rank);
   if (!last && R > 0 && Rl > 0) {
     const int n_rows = R * nt, n_cols = Rl * nt;
     if (nt % 2 == 0) {
@@ -997,16 +1265,23 @@ void destroy_impl(dsel_engine* e) {
                     e->kgain, e->stage, e->xbuf};
   for (double* d : dptr)
     if (d) cudaFree(d);
-  int* iptr[] = {e->status, e->kstatus, e->d_pos_sensor, e->d_slot_sensor, e->d_tab, e->d_sym, e->d_iota};
+  int* iptr[] = {e->status, e->kstatus, e->d_pos_sensor, e->d_slot_sensor, e->d_round, e->d_iota};
   for (int* d : iptr)
     if (d) cudaFree(d);
   if (e->d_rec) cudaFree(e->d_rec);
   if (e->d_recs) cudaFree(e->d_recs);
   if (e->h_recs) cudaFreeHost(e->h_recs);
-  if (e->h_tab) cudaFreeHost(e->h_tab);
-  if (e->h_sym) cudaFreeHost(e->h_sym);
+  if (e->h_round) cudaFreeHost(e->h_round);
   if (e->hstore) cudaFreeHost(e->hstore);
   if (e->hk_registered) cudaHostUnregister(e->hk_registered);
+  for (void* ptr : e->ipc_opened) cudaIpcCloseMemHandle(ptr);
+  if (e->flag) cudaFree(e->flag);
+  if (e->d_peer_wsend) cudaFree(e->d_peer_wsend);
+  if (e->d_peer_flag) cudaFree(e->d_peer_flag);
+  if (e->Wsend) cudaFree(e->Wsend);
+  if (e->Wrecv) cudaFree(e->Wrecv);
+  if (e->d_hbpos) cudaFree(e->d_hbpos);
+
   if (e->Kk) cudaFree(e->Kk);
   if (e->ev_tab) cudaEventDestroy(e->ev_tab);
   if (e->h_stage) cudaFreeHost(e->h_stage);
@@ -1128,11 +1403,33 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
       CU(cudaMemsetAsync(e->Wown, 0, sizeof(double) * (size_t)e->own_mpad * B * e->ldw, e->s));
       CU(cudaMemsetAsync(e->Wkn, 0, sizeof(double) * (size_t)e->k_mpad * B * e->ldw, e->s));
     }
-    {
+    // per-round host tables, one pinned staging block and one device block so a
+    // round uploads them with a single copy: [row/col tables | block-lower tile
+    // schedule | W holder lists (symmetric, G > 1)]
+    size_t n_tab = ((size_t)e->nc + 2 * e->nloc + 1 + 3) / 4 * 4, n_sym = 0, n_hb = 0;
+    if (e->sym) {
       const size_t nct = (size_t)(e->nloc * e->nt + ws::BC - 1) / ws::BC + 2;
-      const size_t nsym = nct + nct / e->ws_group + 4;
-      e->d_sym = dmalloc<int>(nsym, tot);
-      CU(cudaMallocHost(&e->h_sym, sizeof(int) * nsym));
+      n_sym = (nct + nct / e->ws_group + 4 + 3) / 4 * 4;
+      if (e->G > 1) {
+        e->Wsend = dmalloc<double>((size_t)e->n * e->ldw, tot);
+        e->Wrecv = dmalloc<double>((size_t)e->n * e->ldw, tot);
+        n_hb = 2 * (size_t)e->nc + e->G + 1;
+      }
+    }
+    e->round_ints = n_tab + n_sym + n_hb;
+    e->d_round = dmalloc<int>(e->round_ints, tot);
+    CU(cudaMallocHost(&e->h_round, sizeof(int) * e->round_ints));
+    e->d_tab = e->d_round;
+    e->h_tab = e->h_round;
+    if (n_sym) {
+      e->d_sym = e->d_round + n_tab;
+      e->h_sym = e->h_round + n_tab;
+    }
+    if (n_hb) {
+      e->d_hb = e->d_round + n_tab + n_sym;
+      e->h_hb = e->h_round + n_tab + n_sym;
+      e->d_hbpos = e->d_hb + e->nc;
+      e->d_hboff = e->d_hb + 2 * (size_t)e->nc;
     }
     e->Lk = dmalloc<double>((size_t)e->nt * e->nt, tot);
     e->Linv = dmalloc<double>((size_t)e->ldw * e->ldw, tot);
@@ -1147,11 +1444,9 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
                                     e->nt * e->nt, tot);
     e->d_pos_sensor = dmalloc<int>(e->nc, tot);
     e->d_slot_sensor = dmalloc<int>(e->nloc + 1, tot);
-    e->d_tab = dmalloc<int>((size_t)e->nc + 2 * e->nloc, tot);
     e->d_rec = dmalloc<ArgRec>(1, tot);
     e->d_recs = dmalloc<ArgRec>(e->G, tot);
     CU(cudaMallocHost(&e->h_recs, sizeof(ArgRec) * e->G));
-    CU(cudaMallocHost(&e->h_tab, sizeof(int) * ((size_t)e->nc + 2 * e->nloc + 1)));
     if (e->W) CU(cudaMemsetAsync(e->W, 0, sizeof(double) * (size_t)e->n * e->ldw, e->s));
     if (e->Wn) CU(cudaMemsetAsync(e->Wn, 0, sizeof(double) * (size_t)e->n * e->ldw, e->s));
     if (e->Wt) {
@@ -1185,6 +1480,7 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
       NC(ncclAllReduce(wb, wb, wn, ncclDouble, ncclSum, e->comm, e->s));
       NC(ncclBroadcast(wb, wb, wn, ncclDouble, 0, e->comm, e->s));
       CU(cudaMemsetAsync(wb, 0, sizeof(double) * wn, e->s));
+      if (e->Wsend) setup_p2p(e);
     }
     build_tables(e);
     CU(cudaStreamSynchronize(e->s));

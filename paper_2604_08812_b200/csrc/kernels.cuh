@@ -1806,6 +1806,89 @@ __global__ void gather_panel_sym_kernel(const double* C, long long ldc, int nt, 
   }
 }
 
+// Distributed W (symmetric storage, G > 1): packed rows [j][r][c] (ld = ldw)
+// of holder-ordered compact blocks hb[j] -> the tiled update operands, and the
+// factor history of this rank's candidates.
+__global__ void w_scatter_kernel(const double* Wrecv, int ldw, const int* hb, const int* row_pos,
+                                 int n_blocks, int nt, double* Wt, double* Wnt, int mpad, double* hist,
+                                 long long slot_stride, long long step_off, int G, int rank) {
+  const long long n2 = (long long)nt * nt;
+  const long long total = n2 * n_blocks;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(e / n2);
+    const long long w = e - (long long)j * n2;
+    const int r = (int)(w / nt), c = (int)(w - (long long)r * nt);
+    const double v = Wrecv[((size_t)j * nt + r) * ldw + c];
+    const int blk = hb[j];
+    const int row = blk * nt + r;
+    Wt[wt_index(row, c, mpad)] = v;
+    Wnt[wt_index(row, c, mpad)] = -v;
+    if (hist) {
+      const int pos = row_pos[blk];
+      if (pos % G == rank) hist[(long long)(pos / G) * slot_stride + step_off + (size_t)r * nt + c] = v;
+    }
+  }
+}
+
+// NVLink peer-memory exchange (symmetric storage, G > 1): publish / wait on a
+// per-rank monotonically increasing round sequence.
+__global__ void p2p_signal_kernel(unsigned long long* flag, unsigned long long v) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();  // this rank's W rows (previous kernel) before the flag
+    asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(flag), "l"(v) : "memory");
+  }
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// All-gather-v fused with the scatter: element pairs (j, r, c..c+1) of the
+// holder-ordered W rows are read straight from the holder's Wsend over NVLink
+// and written to the tiled operands (+ the history of own candidates).
+__global__ void w_peer_scatter_kernel(const double* const* peer_w, unsigned long long* const* peer_flag,
+                                      unsigned long long seq, int G, const int* hb_off, int ldw,
+                                      const int* hb, const int* row_pos, int n_blocks, int nt, double* Wt,
+                                      double* Wnt, int mpad, double* hist, long long slot_stride,
+                                      long long step_off, int rank) {
+  if (threadIdx.x < G) {
+    const unsigned long long* f = peer_flag[threadIdx.x];
+    while (ld_acquire_sys(f) < seq) {
+    }
+  }
+  __syncthreads();
+  const int half = nt / 2;
+  const long long per = (long long)nt * half;
+  const long long total = per * n_blocks;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(e / per);
+    const long long w = e - (long long)j * per;
+    const int r = (int)(w / half), c = 2 * (int)(w - (long long)r * half);
+    int src = 0;
+    while (src + 1 < G && hb_off[src + 1] <= j) ++src;
+    const double2 v =
+        *reinterpret_cast<const double2*>(peer_w[src] + ((size_t)(j - hb_off[src]) * nt + r) * ldw + c);
+    const int blk = hb[j];
+    const int row = blk * nt + r;
+    Wt[wt_index(row, c, mpad)] = v.x;
+    Wt[wt_index(row, c + 1, mpad)] = v.y;
+    Wnt[wt_index(row, c, mpad)] = -v.x;
+    Wnt[wt_index(row, c + 1, mpad)] = -v.y;
+    if (hist) {
+      const int pos = row_pos[blk];
+      if (pos % G == rank) {
+        double* h = hist + (long long)(pos / G) * slot_stride + step_off + (size_t)r * nt + c;
+        h[0] = v.x;
+        h[1] = v.y;
+      }
+    }
+  }
+}
+
 // Block row j of the current C in symmetric storage (single rank): block
 // (j,i) = panel j's block (i,j)^T when p_i >= p_j, else panel i's block (j,i).
 __global__ void gather_block_row_sym_kernel(const double* C, long long ldc, int nt, int pj,
