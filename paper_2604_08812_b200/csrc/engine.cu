@@ -160,7 +160,7 @@ struct dsel_engine {
   bool p2p = false;
   unsigned long long* flag = nullptr;  // this rank's published round sequence
   unsigned long long seq = 0;
-  std::vector<double*> peer_wsend, peer_lscr;
+  std::vector<double*> peer_wsend, peer_lscr, peer_lk;  // peer_wsend: Wsend (right) / Wkn (left)
   std::vector<unsigned long long*> peer_flag;
   std::vector<void*> ipc_opened;
   const double** d_peer_wsend = nullptr;
@@ -456,35 +456,34 @@ void ws_balance(int n_tiles, int n_k, int sms, int max_s, int br, int& n_full, i
   }
 }
 
-// Map the peers' Wsend, gain scratch and round flag (NVLink peer memory). All
-// ranks take the same decision (min-reduced), since the per-round collective
+// Map the peers' exchange buffer (Wsend: symmetric right-looking; Wkn:
+// left-looking), gain scratch, round flag and L_k buffer (NVLink peer memory).
+// All ranks take the same decision (min-reduced): the per-round collective
 // sequence depends on it. DSEL_P2P=0 keeps the NCCL exchange.
+constexpr int kPeerBufs = 4;  // 0 exchange, 1 Lscr, 2 flag, 3 Lk
 struct PeerInfo {
-  cudaIpcMemHandle_t h_wsend, h_lscr, h_flag;
+  cudaIpcMemHandle_t h[kPeerBufs];
+  void* p[kPeerBufs];
   long long pid;
   int dev;
   int ok;
-  void *p_wsend, *p_lscr, *p_flag;
 };
 
 void setup_p2p(dsel_engine* e) {
   const int G = e->G;
   CU(cudaMalloc(&e->flag, 256));
   CU(cudaMemset(e->flag, 0, 256));
+  void* bufs[kPeerBufs] = {e->Wsend ? (void*)e->Wsend : (void*)e->Wkn, e->Lscr, e->flag, e->Lk};
   PeerInfo mine{};
   mine.pid = (long long)getpid();
   mine.dev = e->dev;
-  mine.p_wsend = e->Wsend;
-  mine.p_lscr = e->Lscr;
-  mine.p_flag = e->flag;
   const char* env = getenv("DSEL_P2P");
-  mine.ok = !(env && atoi(env) == 0);
-  if (mine.ok) {
-    mine.ok = cudaIpcGetMemHandle(&mine.h_wsend, e->Wsend) == cudaSuccess &&
-              cudaIpcGetMemHandle(&mine.h_lscr, e->Lscr) == cudaSuccess &&
-              cudaIpcGetMemHandle(&mine.h_flag, e->flag) == cudaSuccess;
-    cudaGetLastError();
+  mine.ok = !(env && atoi(env) == 0) && bufs[0] != nullptr;
+  for (int b = 0; b < kPeerBufs && mine.ok; ++b) {
+    mine.p[b] = bufs[b];
+    mine.ok = cudaIpcGetMemHandle(&mine.h[b], bufs[b]) == cudaSuccess;
   }
+  cudaGetLastError();
   PeerInfo* d_info = nullptr;
   CU(cudaMalloc(&d_info, sizeof(PeerInfo) * (G + 1)));
   CU(cudaMemcpy(d_info + G, &mine, sizeof(PeerInfo), cudaMemcpyHostToDevice));
@@ -495,14 +494,10 @@ void setup_p2p(dsel_engine* e) {
   cudaFree(d_info);
   int ok = 1;
   for (const auto& x : all) ok &= x.ok;
-  e->peer_wsend.assign(G, nullptr);
-  e->peer_lscr.assign(G, nullptr);
-  e->peer_flag.assign(G, nullptr);
+  std::vector<std::vector<void*>> peer(kPeerBufs, std::vector<void*>(G, nullptr));
   for (int r = 0; r < G && ok; ++r) {
     if (r == e->rank) {
-      e->peer_wsend[r] = e->Wsend;
-      e->peer_lscr[r] = e->Lscr;
-      e->peer_flag[r] = e->flag;
+      for (int b = 0; b < kPeerBufs; ++b) peer[b][r] = bufs[b];
       continue;
     }
     if (all[r].pid == mine.pid) {  // same process (thread per GPU): peer access
@@ -514,29 +509,21 @@ void setup_p2p(dsel_engine* e) {
         ok = 0;
         break;
       }
-      e->peer_wsend[r] = static_cast<double*>(all[r].p_wsend);
-      e->peer_lscr[r] = static_cast<double*>(all[r].p_lscr);
-      e->peer_flag[r] = static_cast<unsigned long long*>(all[r].p_flag);
+      for (int b = 0; b < kPeerBufs; ++b) peer[b][r] = all[r].p[b];
     } else {  // another process: CUDA IPC
-      void *a = nullptr, *b = nullptr, *c = nullptr;
-      if (cudaIpcOpenMemHandle(&a, all[r].h_wsend, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess)
-        e->ipc_opened.push_back(a);
-      if (cudaIpcOpenMemHandle(&b, all[r].h_lscr, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess)
-        e->ipc_opened.push_back(b);
-      if (cudaIpcOpenMemHandle(&c, all[r].h_flag, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess)
-        e->ipc_opened.push_back(c);
-      cudaGetLastError();
-      if (!a || !b || !c) {
-        ok = 0;
-        break;
+      for (int b = 0; b < kPeerBufs && ok; ++b) {
+        void* m = nullptr;
+        if (cudaIpcOpenMemHandle(&m, all[r].h[b], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
+          e->ipc_opened.push_back(m);
+          peer[b][r] = m;
+        } else {
+          ok = 0;
+        }
       }
-      e->peer_wsend[r] = static_cast<double*>(a);
-      e->peer_lscr[r] = static_cast<double*>(b);
-      e->peer_flag[r] = static_cast<unsigned long long*>(c);
+      cudaGetLastError();
     }
   }
-  // every rank must agree
-  int* d_ok = nullptr;
+  int* d_ok = nullptr;  // every rank must agree
   CU(cudaMalloc(&d_ok, sizeof(int)));
   CU(cudaMemcpy(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice));
   NC(ncclAllReduce(d_ok, d_ok, 1, ncclInt, ncclMin, e->comm, e->s));
@@ -548,6 +535,16 @@ void setup_p2p(dsel_engine* e) {
     for (void* ptr : e->ipc_opened) cudaIpcCloseMemHandle(ptr);
     e->ipc_opened.clear();
     return;
+  }
+  e->peer_wsend.assign(G, nullptr);
+  e->peer_lscr.assign(G, nullptr);
+  e->peer_flag.assign(G, nullptr);
+  e->peer_lk.assign(G, nullptr);
+  for (int r = 0; r < G; ++r) {
+    e->peer_wsend[r] = static_cast<double*>(peer[0][r]);
+    e->peer_lscr[r] = static_cast<double*>(peer[1][r]);
+    e->peer_flag[r] = static_cast<unsigned long long*>(peer[2][r]);
+    e->peer_lk[r] = static_cast<double*>(peer[3][r]);
   }
   CU(cudaMalloc(&e->d_peer_wsend, sizeof(double*) * G));
   CU(cudaMalloc(&e->d_peer_flag, sizeof(unsigned long long*) * G));
@@ -694,7 +691,27 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
       e->launches += 1;
     }
   }
-  if (!last && e->G > 1) {
+  if (!last && e->G > 1 && e->p2p) {
+    // the owner publishes -W_k and L_k (its Wkn / Lk, rewritten only when it
+    // owns a later round -- after every peer has passed the next argmax
+    // all-gather, i.e. finished these copies); peers wait on its flag and pull
+    // them over NVLink with the copy engines
+    ++e->seq;
+    if (owner == e->rank) {
+      p2p_signal_kernel<<<1, 32, 0, e->s>>>(e->flag, e->seq);
+      CU(cudaGetLastError());
+    } else {
+      p2p_wait_kernel<<<1, 32, 0, e->s>>>(e->peer_flag[owner], e->seq);
+      CU(cudaGetLastError());
+      if (kcols > 0)
+        CU(cudaMemcpyAsync(e->Wkn, e->peer_wsend[owner], sizeof(double) * (size_t)kcols * e->k_mpad,
+                           cudaMemcpyDefault, e->s));
+      CU(cudaMemcpyAsync(e->Lk, e->peer_lk[owner], sizeof(double) * (size_t)n2, cudaMemcpyDefault, e->s));
+      bytes += (uint64_t)((size_t)kcols * e->k_mpad + n2) * sizeof(double);
+    }
+    e->launches += 1;
+    Lk = e->Lk;
+  } else if (!last && e->G > 1) {
     NC(ncclGroupStart());
     if (kcols > 0)
       NC(ncclBroadcast(e->Wkn, e->Wkn, (size_t)kcols * e->k_mpad, ncclDouble, owner, e->comm, e->s));
@@ -1480,7 +1497,7 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
       NC(ncclAllReduce(wb, wb, wn, ncclDouble, ncclSum, e->comm, e->s));
       NC(ncclBroadcast(wb, wb, wn, ncclDouble, 0, e->comm, e->s));
       CU(cudaMemsetAsync(wb, 0, sizeof(double) * wn, e->s));
-      if (e->Wsend) setup_p2p(e);
+      setup_p2p(e);
     }
     build_tables(e);
     CU(cudaStreamSynchronize(e->s));

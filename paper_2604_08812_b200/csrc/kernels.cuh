@@ -1846,6 +1846,12 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   return v;
 }
 
+__global__ void p2p_wait_kernel(const unsigned long long* flag, unsigned long long v) {
+  if (threadIdx.x == 0)
+    while (ld_acquire_sys(flag) < v) {
+    }
+}
+
 // All-gather-v fused with the scatter: element pairs (j, r, c..c+1) of the
 // holder-ordered W rows are read straight from the holder's Wsend over NVLink
 // and written to the tiled operands (+ the history of own candidates).
