@@ -133,7 +133,9 @@ struct dsel_engine {
   const double* hk_user = nullptr;
   bool hk_rows = false;  // hk_user holds only this rank's block rows (slot order)
   void* hk_registered = nullptr;  // cudaHostRegister'ed by the engine (pageable input)
-  cudaEvent_t ev_tab = nullptr;  // this round's table upload done (orders the column copy after it)
+  cudaEvent_t ev_tab = nullptr;
+  cudaStream_t ts = nullptr;  // side stream: L_k^-1 concurrent with the panel gather
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // this round's table upload done (orders the column copy after it)
   std::vector<int> streamed_round;  // rounds whose ev[5..7] are valid
   double *Wown = nullptr, *Wkn = nullptr, *D = nullptr, *cbuf = nullptr, *ldiag = nullptr,
          *cpart = nullptr;
@@ -622,26 +624,36 @@ void finish_row(dsel_engine* e, dsel_step_info& row, int s1, int s2, double g1, 
   if (info) *info = row;
 }
 
-void launch_trinv(dsel_engine* e, const double* Lk) {
+void launch_trinv(dsel_engine* e, const double* Lk, cudaStream_t st = nullptr) {
+  if (!st) st = e->s;
   const int nt = e->nt, tb = 256 / 32;
   const unsigned g = (unsigned)((e->ldw + tb - 1) / tb);
   if (nt <= TRINV_SMEM_MAX_NT) {
     const size_t sm = ((size_t)2 * 32 * nt + nt) * sizeof(double);
     if (e->ldw <= 128)
-      trinv_smem_kernel<4><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+      trinv_smem_kernel<4><<<g, 256, sm, st>>>(Lk, nt, e->Linv, e->ldw);
     else if (e->ldw <= 256)
-      trinv_smem_kernel<8><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+      trinv_smem_kernel<8><<<g, 256, sm, st>>>(Lk, nt, e->Linv, e->ldw);
     else
-      trinv_smem_kernel<14><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+      trinv_smem_kernel<14><<<g, 256, sm, st>>>(Lk, nt, e->Linv, e->ldw);
   } else {
     const size_t sm = (size_t)nt * sizeof(double);
     if (e->ldw <= 512)
-      trinv_kernel<16><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+      trinv_kernel<16><<<g, 256, sm, st>>>(Lk, nt, e->Linv, e->ldw);
     else
-      trinv_kernel<32><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
+      trinv_kernel<32><<<g, 256, sm, st>>>(Lk, nt, e->Linv, e->ldw);
   }
   CU(cudaGetLastError());
   e->launches += 1;
+}
+
+// L_k^-1 on the side stream, overlapping the panel gather / table upload; the
+// compute stream joins before the W solve.
+void launch_trinv_async(dsel_engine* e, const double* Lk) {
+  CU(cudaEventRecord(e->ev_fork, e->s));
+  CU(cudaStreamWaitEvent(e->ts, e->ev_fork, 0));
+  launch_trinv(e, Lk, e->ts);
+  CU(cudaEventRecord(e->ev_join, e->ts));
 }
 
 // Block (own slot qq, sensor col) of the caller-attached host K.
@@ -1016,6 +1028,7 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
         Lk = e->Lk;
       }
       g_probe.mark("lkbc", e->s);
+      launch_trinv_async(e, Lk);
       const int* rp = e->h_tab;
       int* hb = e->h_hb;
       int* hbpos = e->h_hb + e->nc;
@@ -1037,6 +1050,8 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       gpos = e->d_hbpos + e->hb_off[e->rank];
       n_gather = e->hb_off[e->rank + 1] - e->hb_off[e->rank];
       g_probe.mark("holders", e->s);
+    } else {
+      launch_trinv_async(e, Lk);
     }
     sym_tables(e, false);
     upload_round(e);
@@ -1051,27 +1066,10 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   }
   double flops = 0.0;
   if (!last) {
-    const int tb = 256 / 32;
-    {
-      const unsigned g = (unsigned)((e->ldw + tb - 1) / tb);
-      if (nt <= TRINV_SMEM_MAX_NT) {
-        const size_t sm = ((size_t)2 * 32 * nt + nt) * sizeof(double);
-        if (e->ldw <= 128)
-          trinv_smem_kernel<4><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
-        else if (e->ldw <= 256)
-          trinv_smem_kernel<8><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
-        else
-          trinv_smem_kernel<14><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
-      } else {
-        const size_t sm = (size_t)nt * sizeof(double);
-        if (e->ldw <= 512)
-          trinv_kernel<16><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
-        else
-          trinv_kernel<32><<<g, 256, sm, e->s>>>(Lk, nt, e->Linv, e->ldw);
-      }
-    }
-    CU(cudaGetLastError());
-    e->launches += 1;
+    if (e->sym)
+      CU(cudaStreamWaitEvent(e->s, e->ev_join, 0));  // L_k^-1 from the side stream
+    else
+      launch_trinv(e, Lk);
     g_probe.mark("trinv", e->s);
     const bool dist_w = e->sym && e->G > 1;
     const int n_own_rows = dist_w ? (e->hb_off[e->rank + 1] - e->hb_off[e->rank]) * nt : R * nt;
@@ -1307,6 +1305,12 @@ void destroy_impl(dsel_engine* e) {
     if (e->ev_copy[b]) cudaEventDestroy(e->ev_copy[b]);
     if (e->ev_scat[b]) cudaEventDestroy(e->ev_scat[b]);
   }
+  if (e->ts) {
+    cudaStreamSynchronize(e->ts);
+    cudaStreamDestroy(e->ts);
+  }
+  if (e->ev_fork) cudaEventDestroy(e->ev_fork);
+  if (e->ev_join) cudaEventDestroy(e->ev_join);
   if (e->cs) cudaStreamDestroy(e->cs);
   if (e->s) cudaStreamDestroy(e->s);
   delete e;
@@ -1370,6 +1374,9 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     CU(cudaDeviceGetAttribute(&e->n_sms, cudaDevAttrMultiProcessorCount, e->dev));
     CU(cudaStreamCreateWithFlags(&e->s, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&e->cs, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&e->ts, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
     for (int b = 0; b < 2; ++b) {
       CU(cudaEventCreateWithFlags(&e->ev_copy[b], cudaEventDisableTiming));
       CU(cudaEventCreateWithFlags(&e->ev_scat[b], cudaEventDisableTiming));

@@ -9,6 +9,9 @@ __device__ long long g_stamps[64];
 __device__ unsigned long long g_tstart[4096], g_tend[4096];
 #include "../paper_2604_08812_b200/csrc/kernels.cuh"
 using namespace dsel;
+#ifndef PROBE_NB
+#define PROBE_NB 32
+#endif
 #ifndef PROBE_MINB
 #define PROBE_MINB 1
 #endif
@@ -29,12 +32,12 @@ int main(int argc, char** argv) {
   cudaMemcpy(sr, rows.data(), batch * 4, cudaMemcpyHostToDevice);
   CholArgs a; a.src = src; a.lds = nt; a.src_col = sc; a.src_row = sr; a.L = L; a.l_stride = n2;
   a.gain = gain; a.status = st; a.nt = nt; a.n = batch; a.mp = mp;
-  size_t smem = ((size_t)2 * 32 * mp + nt) * 8;
-  cudaFuncSetAttribute(chol_logdet_kernel<32, PROBE_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  size_t smem = ((size_t)2 * PROBE_NB * mp + nt) * 8;
+  cudaFuncSetAttribute(chol_logdet_kernel<PROBE_NB, PROBE_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  for (int r = 0; r < 3; ++r) chol_logdet_kernel<32, PROBE_MINB><<<batch, 256, smem>>>(a);
+  for (int r = 0; r < 3; ++r) chol_logdet_kernel<PROBE_NB, PROBE_MINB><<<batch, 256, smem>>>(a);
   cudaEventRecord(e0);
-  chol_logdet_kernel<32, PROBE_MINB><<<batch, 256, smem>>>(a);
+  chol_logdet_kernel<PROBE_NB, PROBE_MINB><<<batch, 256, smem>>>(a);
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   long long stamps[64]; cudaMemcpyFromSymbol(stamps, g_stamps, sizeof(stamps));
