@@ -1473,12 +1473,25 @@ __global__ void __launch_bounds__(256, MINB) chol_logdet_kernel(CholArgs a) {
     //     x L_dd^T = s, one row per thread, row in registers
 #pragma unroll 1
     for (int i = NB + tid; i < m; i += 256) {
-      double s[NB];
+      // right-looking in groups of 8 columns: an 8-long chain per group in
+      // registers, the later columns updated in shared memory (no spills)
 #pragma unroll
-      for (int c = 0; c < NB; ++c) s[c] = S[c * mp + i];
-      trsm_step<0, NB>(s, S, mp, rdiag);
+      for (int jb = 0; jb < NB; jb += 8) {
+        double s8[8];
 #pragma unroll
-      for (int c = 0; c < NB; ++c) S[c * mp + i] = s[c];
+        for (int c = 0; c < 8; ++c) s8[c] = S[(jb + c) * mp + i];
+        trsm_step<0, 8>(s8, S + jb * mp + jb, mp, rdiag + jb);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) S[(jb + c) * mp + i] = s8[c];
+#pragma unroll 4
+        for (int c = jb + 8; c < NB; ++c) {
+          const double* lc = S + c;  // L_dd[c][jb + j] at S[(jb + j) * mp + c]
+          double v = S[c * mp + i];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v -= s8[j] * lc[(jb + j) * mp];
+          S[c * mp + i] = v;
+        }
+      }
     }
     __syncthreads();
     STAMP();
