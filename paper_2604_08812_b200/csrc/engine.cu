@@ -557,13 +557,25 @@ void setup_p2p(dsel_engine* e) {
 
 // Launch the persistent update kernel in the engine's configuration (grid =
 // resident CTAs, capped by the number of work units).
-void launch_ws(dsel_engine* e, UpdateWSArgs& ua) {
-  ua.br = e->ws_br;
+// Configuration for a launch: 3 chunks x 2 stages (Big4) pays fewer stage
+// hand-offs on long k loops, 2 x 3 (Big) keeps the producer further ahead on
+// short ones (Nt = 128 right-looking); 64-row tiles (Pair) when the r-side row
+// count pads badly to 128 (left-looking r-side = Nt rows: 420 -> 82 % of 4 x
+// 128 tiles, 94 % of 7 x 64). -1 = auto.
+int ws_pick(const dsel_engine* e, int r_rows, int n_k, bool fixed_rows) {
+  if (e->ws_cfg >= 0) return e->ws_cfg;
+  if (fixed_rows) {
+    const double u128 = (double)r_rows / (((r_rows + 127) / 128) * 128);
+    const double u64 = (double)r_rows / (((r_rows + 63) / 64) * 64);
+    if (u64 > u128 + 0.05) return 1;
+  }
+  return n_k >= 16 ? 2 : 0;
+}
+
+void launch_ws(dsel_engine* e, UpdateWSArgs& ua, int cfg) {
+  ua.br = cfg == 1 ? 64 : 128;
   const long long units = (long long)ua.n_full + (long long)(ua.n_tiles - ua.n_full) * ua.split_s;
   if (units <= 0) return;
-  // 3 chunks x 2 stages pays fewer stage hand-offs on long k loops (left-looking,
-  // Nt = 420); 2 x 3 keeps the producer further ahead on short ones (Nt = 128)
-  const int cfg = e->ws_cfg >= 0 ? e->ws_cfg : (ua.n_k >= 16 ? 2 : 0);
   if (cfg == 1) {
     const int grid = (int)std::min<long long>(2LL * e->n_sms, units);
     schur_update_ws_kernel<ws::Pair><<<grid, ws::Pair::THREADS, ws::Pair::SMEM, e->s>>>(ua);
@@ -779,7 +791,9 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
       ua.nt = nt;
       ua.n_rows = nt;
       ua.n_cols = n_rows;
-      ua.n_row_tiles = (nt + e->ws_br - 1) / e->ws_br;
+      const int cfg = ws_pick(e, nt, ua.n_k, true);
+      const int br = cfg == 1 ? 64 : 128;
+      ua.n_row_tiles = (nt + br - 1) / br;
       ua.n_col_tiles = (n_rows + ws::BC - 1) / ws::BC;
       ua.group = e->ws_group;
       ua.sym = 0;
@@ -788,13 +802,13 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
       ua.ldo = e->ldo;
       ua.mpad_c = e->own_mpad;
       // wave balancing: the tiles past the last full wave are split along k
-      ws_balance(ua.n_tiles, ua.n_k, e->n_sms * (e->ws_br == 64 ? 2 : 1), e->cpart ? kLLMaxSplits : 1,
-                 e->ws_br, ua.n_full, ua.split_s);
+      ws_balance(ua.n_tiles, ua.n_k, e->n_sms * (br == 64 ? 2 : 1), e->cpart ? kLLMaxSplits : 1, br,
+                 ua.n_full, ua.split_s);
       ua.part = e->cpart;
       ua.part_stride = (long long)e->ldo * nt;
-      launch_ws(e, ua);
+      launch_ws(e, ua, cfg);
       if (ua.split_s > 1) {
-        const long long total = (long long)(ua.n_tiles - ua.n_full) * e->ws_br * ws::BC;
+        const long long total = (long long)(ua.n_tiles - ua.n_full) * br * ws::BC;
         ws_split_reduce_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 8), 256, 0,
                                  e->s>>>(ua);
         CU(cudaGetLastError());
@@ -1201,7 +1215,7 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       ua.n_tiles = e->sym ? e->sym_tiles : ua.n_row_tiles * ua.n_col_tiles;
       ua.n_full = ua.n_tiles;
       ua.split_s = 1;
-      launch_ws(e, ua);
+      launch_ws(e, ua, ws_pick(e, 0, ua.n_k, false));
     } else {
       UpdateArgs ua{};
       ua.C = e->C;
@@ -2033,7 +2047,7 @@ dsel_status dsel_gen_synthetic_device(dsel_engine* e, int rank, double sigma, ui
       ua.n_tiles = sym ? e->sym_tiles : ua.n_row_tiles * ua.n_col_tiles;
       ua.n_full = ua.n_tiles;
       ua.split_s = 1;
-      launch_ws(e, ua);
+      launch_ws(e, ua, ws_pick(e, 0, ua.n_k, false));
       ce = cudaGetLastError();
       gen_flops += 2.0 * kch * (sym ? 0.5 * (double)n_rows * (n_cols + nt) : (double)n_rows * n_cols);
     }
