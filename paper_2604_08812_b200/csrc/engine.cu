@@ -360,7 +360,13 @@ void launch_chol(const CholArgs& a, int n_batch, cudaStream_t s, int n_sms) {
   // more candidates than SMs: squeeze two CTAs per SM (capped registers) so the
   // batch runs in one wave; otherwise one uncapped CTA per candidate
   const bool two = n_batch > n_sms;
-  if (nb == 32) {
+  if (a.nt >= 32 && a.nt <= 128 && !getenv("DSEL_CHOL_PANELS")) {  // triangle-resident variant
+    const size_t ts = tri_smem_bytes(a.nt);
+    if (two)
+      chol_logdet_tri_kernel<2><<<n_batch, 256, ts, s>>>(a);
+    else
+      chol_logdet_tri_kernel<1><<<n_batch, 256, ts, s>>>(a);
+  } else if (nb == 32) {
     if (two)
       chol_logdet_kernel<32, 2><<<n_batch, 256, smem, s>>>(a);
     else
@@ -415,6 +421,8 @@ void set_smem_limits(int dev) {
   allow_smem(chol_logdet_kernel<32, 1>, optin);
   allow_smem(chol_logdet_kernel<32, 2>, optin);
   allow_smem(chol_logdet_kernel<8, 1>, optin);
+  allow_smem(chol_logdet_tri_kernel<1>, optin);
+  allow_smem(chol_logdet_tri_kernel<2>, optin);
   allow_smem(schur_update_kernel<2>, optin);
   allow_smem(schur_update_kernel<1>, optin);
   allow_smem(panel_w_kernel<2>, optin);

@@ -1530,6 +1530,153 @@ __global__ void __launch_bounds__(256, MINB) chol_logdet_kernel(CholArgs a) {
 }
 
 // ------------------------------------------------------------------------ //
+// Gain kernel, Nt <= 128: the whole lower triangle stays in shared memory    //
+// (32-column panels, each holding its rows from the panel's diagonal down),  //
+// loaded once; the left-looking panel update reads earlier panels from       //
+// shared memory (no global round trips between panels) and sums all earlier  //
+// columns in one DMMA accumulation. Diagonal block and row solve as above.   //
+// ------------------------------------------------------------------------ //
+__host__ __device__ __forceinline__ int tri_pitch(int nt, int q) { return ((nt - 32 * q + 7) / 8) * 8 + 4; }
+__host__ __device__ __forceinline__ int tri_offset(int nt, int q) {
+  int off = 0;
+  for (int r = 0; r < q; ++r) off += 32 * tri_pitch(nt, r);
+  return off;
+}
+__host__ __device__ __forceinline__ size_t tri_smem_bytes(int nt) {
+  const int np = (nt + 31) / 32;
+  return ((size_t)tri_offset(nt, np) + nt) * sizeof(double);
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) chol_logdet_tri_kernel(CholArgs a) {
+  constexpr int NB = 32;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int b = blockIdx.x;
+  if (b >= a.n) return;
+  const int nt = a.nt;
+  const int np = (nt + NB - 1) / NB;
+  double* T = reinterpret_cast<double*>(smem_raw);
+  double* diagv = T + tri_offset(nt, np);
+  __shared__ double rdiag[NB];
+  __shared__ __align__(16) double s_colbuf[64];
+  __shared__ int s_fail;
+  __shared__ double s_red[8];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const double* src = a.src + (size_t)a.src_col[b] * a.lds + a.src_row[b];
+  double* L = a.L + (size_t)b * a.l_stride;  // column-major nt x nt
+  if (tid == 0) s_fail = -1;
+  // the lower triangle (by panels, rows from each panel's diagonal down), one async load
+  for (int q = 0; q < np; ++q) {
+    const int J0 = q * NB, nb = min(NB, nt - J0), m = nt - J0, P = tri_pitch(nt, q);
+    double* Sq = T + tri_offset(nt, q);
+    for (int e = tid; e < nb * m; e += 256) {
+      const int j = e / m, i = e - j * m;
+      cp_async8(Sq + j * P + i, src + (size_t)(J0 + j) * a.lds + J0 + i, true);
+    }
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  for (int p = 0; p < np; ++p) {
+    const int J0 = p * NB, nb = min(NB, nt - J0), m = nt - J0, mp = tri_pitch(nt, p);
+    double* S = T + tri_offset(nt, p);
+    if (p > 0) {
+      // S -= L[J0:, 0:J0] L[J0:J0+nb, 0:J0]^T, all earlier panels at once
+      const int mt_n = (m + 7) >> 3;
+      for (int mt = warp; mt < mt_n; mt += 8) {
+        double acc[4][2];
+#pragma unroll
+        for (int n8 = 0; n8 < 4; ++n8) acc[n8][0] = acc[n8][1] = 0.0;
+        for (int kk = 0; kk < p; ++kk) {
+          const int Pk = tri_pitch(nt, kk);
+          const double* Lk = T + tri_offset(nt, kk) + (J0 - kk * NB);
+#pragma unroll
+          for (int k4 = 0; k4 < NB / 4; ++k4) {
+            const double* col = Lk + (k4 * 4 + t) * Pk;
+            const double av = col[mt * 8 + g];
+#pragma unroll
+            for (int n8 = 0; n8 < 4; ++n8) dmma884(acc[n8], av, col[n8 * 8 + g]);
+          }
+        }
+        const int i = mt * 8 + g;
+        if (i < m) {
+#pragma unroll
+          for (int n8 = 0; n8 < 4; ++n8) {
+            const int j0 = n8 * 8 + 2 * t;
+            if (j0 < nb) S[j0 * mp + i] -= acc[n8][0];
+            if (j0 + 1 < nb) S[(j0 + 1) * mp + i] -= acc[n8][1];
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (warp == 0) {  // diagonal block: one warp, lane l owns row l
+      double r[NB];
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        r[c] = (lane < nb && c < nb) ? (c <= lane ? S[c * mp + lane] : 0.0) : (c == lane ? 1.0 : 0.0);
+      int fail = -1;
+      diag_step<0, NB>(r, lane, nb, diagv + J0, rdiag, fail, s_colbuf);
+      if (lane < nb) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+          if (c <= lane) S[c * mp + lane] = r[c];
+      }
+      if (lane == 0 && fail >= 0) s_fail = J0 + fail;
+    }
+    __syncthreads();
+    if (s_fail >= 0) break;
+#pragma unroll 1
+    for (int i = NB + tid; i < m; i += 256) {  // rows below: x L_dd^T = s
+#pragma unroll
+      for (int jb = 0; jb < NB; jb += 8) {
+        double s8[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) s8[c] = S[(jb + c) * mp + i];
+        trsm_step<0, 8>(s8, S + jb * mp + jb, mp, rdiag + jb);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) S[(jb + c) * mp + i] = s8[c];
+#pragma unroll 4
+        for (int c = jb + 8; c < NB; ++c) {
+          const double* lc = S + c;
+          double v = S[c * mp + i];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v -= s8[j] * lc[(jb + j) * mp];
+          S[c * mp + i] = v;
+        }
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < nb * m; e += 256) {  // the factor panel out (not waited on)
+      const int j = e / m, i = e - j * m;
+      L[(size_t)(J0 + j) * nt + J0 + i] = S[j * mp + i];
+    }
+  }
+  __syncthreads();
+  if (s_fail >= 0) {
+    if (tid == 0) {
+      a.status[b] = s_fail;
+      a.gain[b] = -INFINITY;
+    }
+    return;
+  }
+  double part = 0.0;  // log det = 2 sum log(d_j), fixed-order reduction
+  for (int j = tid; j < nt; j += 256) part += log(diagv[j]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
+  if (lane == 0) s_red[warp] = part;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += s_red[w];
+    a.status[b] = -1;
+    a.gain[b] = 2.0 * s;
+  }
+}
+
+// ------------------------------------------------------------------------ //
 // Triangular inverse of the chosen factor: Linv = L_k^{-1}, row-major [c][m] //
 // with zeros above the diagonal and in the pad (ld = ldl). Warp per column. //
 // ------------------------------------------------------------------------ //
