@@ -11,7 +11,7 @@ run() {  # run <n> <outfile> <args...>
     timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$n --master-addr $P \
       --master-port $((29600 + n)) bench.py --gpus $n "$@" > gpurun_out/$out 2> gpurun_out/$out.err
   fi
-  echo "$out rc=$? $(tail -c 300 gpurun_out/$out)"
+  echo "$out rc=$? $(tail -c 200 gpurun_out/$out)"
 }
 run 1 bench_c2_n1.json
 run 2 bench_c2_n2.json
@@ -19,3 +19,10 @@ run 4 bench_c2_n4.json
 run 1 bench_c3_n1.json --config c3 --no-cpu
 run 2 bench_c3_n2.json --config c3
 run 4 bench_c3_n4.json --config c3
+timeout 600 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/bench_ref_c2.json 2> gpurun_out/bench_ref_c2.err
+echo "ref rc=$? $(tail -c 300 gpurun_out/bench_ref_c2.json)"
+for a in right left; do
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=4 --master-addr $P \
+    --master-port 29650 tools/c4_run.py --algorithm $a > gpurun_out/c4_g4_$a.log 2>&1
+  echo "c4 $a rc=$? $(tail -c 300 gpurun_out/c4_g4_$a.log)"
+done
