@@ -42,6 +42,21 @@ def test_multi_gpu_matches_reference(which):
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not gpu_available() or ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("which", ["c1", "random"])
+def test_multi_gpu_nccl_exchange_fallback(which):
+    """DSEL_P2P=0: the W / W_k exchange over NCCL broadcasts instead of NVLink
+    peer memory gives the same results."""
+    n = min(ngpu(), 8)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(ROOT, "tests", "mp_engine_check.py"), which]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900,
+                       env=dict(os.environ, DSEL_P2P="0"))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not gpu_available() or ngpu() < 2, reason="needs >= 2 GPUs")
 def test_cli_multi_gpu(tmp_path):
     import json
 
