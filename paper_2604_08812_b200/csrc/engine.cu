@@ -1077,10 +1077,10 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
     }
     sym_tables(e, false);
     upload_round(e);
-    if (n_gather > 0) {
-      const long long total = (long long)n_gather * nt * nt;
-      gather_panel_sym_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 32), 256, 0,
-                                e->s>>>(e->C, e->n, nt, gpos, n_gather, p, e->G, e->rank, e->Pbuf);
+    if (n_gather > 0) {  // every listed block is held by this rank
+      const int tpb = (nt + 31) / 32;
+      gather_panel_sym_tiled_kernel<<<(unsigned)((long long)n_gather * tpb * tpb), 256, 0, e->s>>>(
+          e->C, e->n, nt, gpos, p, e->G, e->Pbuf);
       CU(cudaGetLastError());
       e->launches += 1;
     }

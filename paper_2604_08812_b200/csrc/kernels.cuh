@@ -1966,6 +1966,39 @@ __global__ void gather_panel_sym_kernel(const double* C, long long ldc, int nt, 
   }
 }
 
+// Same gather, tiled: one CTA per 32 x 32 sub-tile of a block, both the direct
+// (p_i > p_k) and the transposed (p_i < p_k) sources read along their
+// contiguous dimension, the transpose through shared memory.
+__global__ void __launch_bounds__(256) gather_panel_sym_tiled_kernel(const double* C, long long ldc, int nt,
+                                                                     const int* row_pos, int pk, int G,
+                                                                     double* P) {
+  __shared__ double tile[32][33];
+  const int tpb = (nt + 31) / 32;
+  const int blk = blockIdx.x / (tpb * tpb);
+  const int rem = blockIdx.x - blk * tpb * tpb;
+  const int r0 = (rem / tpb) * 32, c0 = (rem % tpb) * 32;  // sub-tile: rows r0.., columns c0.. of P's block
+  const int pi = row_pos[blk];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  if (pi > pk) {  // P[(pi*nt + r), c] = panel k (column c), row pi*nt + r: rows contiguous
+    const double* srcb = C + (size_t)((pk / G) * nt) * ldc + (size_t)pi * nt;
+    for (int cc = ty; cc < 32; cc += 8) {
+      const int c = c0 + cc, r = r0 + tx;
+      if (c < nt && r < nt) P[(size_t)c * ldc + (size_t)pi * nt + r] = srcb[(size_t)c * ldc + r];
+    }
+  } else {  // P[(pi*nt + r), c] = panel i (column r), row pk*nt + c: contiguous in c
+    const double* srcb = C + (size_t)((pi / G) * nt) * ldc + (size_t)pk * nt;
+    for (int rr = ty; rr < 32; rr += 8) {
+      const int r = r0 + rr, c = c0 + tx;
+      tile[rr][tx] = (r < nt && c < nt) ? srcb[(size_t)r * ldc + c] : 0.0;
+    }
+    __syncthreads();
+    for (int cc = ty; cc < 32; cc += 8) {
+      const int c = c0 + cc, r = r0 + tx;
+      if (c < nt && r < nt) P[(size_t)c * ldc + (size_t)pi * nt + r] = tile[tx][cc];
+    }
+  }
+}
+
 // Distributed W (symmetric storage, G > 1): packed rows [j][r][c] (ld = ldw)
 // of holder-ordered compact blocks hb[j] -> the tiled update operands, and the
 // factor history of this rank's candidates.
