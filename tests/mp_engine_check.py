@@ -78,6 +78,37 @@ if which == "device":
     print(f"rank {rank}/{world} device: {'OK' if not bad else 'MISMATCH'}", flush=True)
     dist.destroy_process_group()
     sys.exit(1 if bad else 0)
+if which in ("lti", "attach"):
+    # lti: K assembled on every rank from the wave config (bit-exact); attach:
+    # the streaming store over each rank's own pinned block rows of the wave K
+    lti = json.load(open(os.path.join(ROOT, "tests", "golden", "lti.json")))["configs"]
+    g = lti["wave_benchmark.cfg"]
+    nd, nt, B = g["n_sensors"], g["n_steps"], g["budget"]
+    variants = ((dict(), dict(algorithm="left"), dict(full_square=True)) if which == "lti"
+                else (dict(algorithm="left", storage=2),))
+    bad = 0
+    for kw in variants:
+        cid = [d.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(cid, src=0)
+        with d.Engine(nd, nt, B, device=local, world_size=world, rank=rank, nccl_id=cid[0], **kw) as eng:
+            if which == "lti":
+                eng.assemble_lti(os.path.join(ROOT, "tests", "golden", "configs", "wave_benchmark.cfg"))
+            else:
+                from oracle import oracle as O  # checker only: parses the KBF fixture
+                k, _, _ = O.read_kbf(os.path.join(ROOT, "tests", "golden", "wave.kbf"))
+                kb = k.reshape(nd, nd * nt * nt)
+                mine = [j for j in range(nd) if j % world == rank]
+                rows_pinned = torch.from_numpy(np.ascontiguousarray(kb[mine])).pin_memory()
+                eng.attach_host_rows(rows_pinned)
+            eng.run()
+            rows = eng.trace()
+        ok = [r["chosen_index"] for r in rows] == list(g["chosen"])
+        for r, gg in zip(rows, g["gains"]):
+            ok = ok and abs(r["gain"] - gg) <= 1e-9 * max(abs(gg), 1.0)
+        bad += not ok
+    print(f"rank {rank}/{world} {which}: {'OK' if not bad else 'MISMATCH'}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(1 if bad else 0)
 gold = json.load(open(os.path.join(ROOT, "tests", "golden", f"{which}.json")))
 if which == "wave":
     from oracle import oracle as O  # checker only: parses the KBF fixture

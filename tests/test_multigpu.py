@@ -29,7 +29,7 @@ def free_port():
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not gpu_available() or ngpu() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("which", ["c1", "wave", "c2", "random", "device"])
+@pytest.mark.parametrize("which", ["c1", "wave", "c2", "random", "device", "lti", "attach"])
 def test_multi_gpu_matches_reference(which):
     n = min(ngpu(), 8)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
