@@ -60,6 +60,24 @@ struct Fail {
 
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 constexpr int kWsGroupDefault = 16;  // column tiles per update rasterization group
+
+// scratch device allocation released on every exit path (including throws)
+template <class T>
+struct DevScratch {
+  T* p = nullptr;
+  explicit DevScratch(size_t count) {
+    if (cudaMalloc(&p, sizeof(T) * (count ? count : 1)) != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      throw Fail{DSEL_E_OOM, "cudaMalloc of scratch (" + std::to_string(count * sizeof(T)) + " bytes) failed"};
+    }
+  }
+  ~DevScratch() {
+    if (p) cudaFree(p);
+  }
+  DevScratch(const DevScratch&) = delete;
+  DevScratch& operator=(const DevScratch&) = delete;
+};
 // DEBUG probes (DSEL_PROBE=1): GPU events + host times at named points of a round
 struct Probe {
   bool on = getenv("DSEL_PROBE") != nullptr;
@@ -494,14 +512,13 @@ void setup_p2p(dsel_engine* e) {
     mine.ok = cudaIpcGetMemHandle(&mine.h[b], bufs[b]) == cudaSuccess;
   }
   cudaGetLastError();
-  PeerInfo* d_info = nullptr;
-  CU(cudaMalloc(&d_info, sizeof(PeerInfo) * (G + 1)));
+  DevScratch<PeerInfo> info_buf(G + 1);
+  PeerInfo* d_info = info_buf.p;
   CU(cudaMemcpy(d_info + G, &mine, sizeof(PeerInfo), cudaMemcpyHostToDevice));
   NC(ncclAllGather(d_info + G, d_info, sizeof(PeerInfo), ncclUint8, e->comm, e->s));
   std::vector<PeerInfo> all(G);
   CU(cudaMemcpyAsync(all.data(), d_info, sizeof(PeerInfo) * G, cudaMemcpyDeviceToHost, e->s));
   CU(cudaStreamSynchronize(e->s));
-  cudaFree(d_info);
   int ok = 1;
   for (const auto& x : all) ok &= x.ok;
   std::vector<std::vector<void*>> peer(kPeerBufs, std::vector<void*>(G, nullptr));
@@ -533,13 +550,12 @@ void setup_p2p(dsel_engine* e) {
       cudaGetLastError();
     }
   }
-  int* d_ok = nullptr;  // every rank must agree
-  CU(cudaMalloc(&d_ok, sizeof(int)));
+  DevScratch<int> ok_buf(1);  // every rank must agree
+  int* d_ok = ok_buf.p;
   CU(cudaMemcpy(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice));
   NC(ncclAllReduce(d_ok, d_ok, 1, ncclInt, ncclMin, e->comm, e->s));
   CU(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, e->s));
   CU(cudaStreamSynchronize(e->s));
-  cudaFree(d_ok);
   e->p2p = ok != 0;
   if (!e->p2p) {
     for (void* ptr : e->ipc_opened) cudaIpcCloseMemHandle(ptr);
@@ -2023,8 +2039,8 @@ dsel_status dsel_gen_synthetic_device(dsel_engine* e, int rank, double sigma, ui
     }
     constexpr int kch = 512;  // rank columns per update launch
     const int mpad = round_up(std::max(n_rows, 1), ws::BR);
-    double* Vt = nullptr;
-    CU(cudaMalloc(&Vt, sizeof(double) * (size_t)mpad * kch));
+    DevScratch<double> vt_buf((size_t)mpad * kch);
+    double* Vt = vt_buf.p;
     cudaError_t ce = cudaSuccess;
     double gen_flops = 0.0;
     for (int k0 = 0; k0 < rank && ce == cudaSuccess && Rl > 0; k0 += kch) {
@@ -2060,7 +2076,6 @@ dsel_status dsel_gen_synthetic_device(dsel_engine* e, int rank, double sigma, ui
       gen_flops += 2.0 * kch * (sym ? 0.5 * (double)n_rows * (n_cols + nt) : (double)n_rows * n_cols);
     }
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(e->s);
-    cudaFree(Vt);
     if (ce != cudaSuccess) throw Fail{DSEL_E_CUDA, std::string("device synthetic K: ") + cudaGetErrorString(ce)};
     e->gen_flops = gen_flops;
     e->full_panels = !sym;
@@ -2117,8 +2132,8 @@ dsel_status dsel_assemble_lti(dsel_engine* e, const dsel_lti* lp, double* noise_
     reset_state(e);
     const size_t nh = (size_t)nd * nm * nt, ns = (size_t)nm * nm, nmask = lp->mask ? (size_t)nm * nt : 0;
     const size_t nvf = n * nm * nt, np1 = (size_t)nt * nd * nt, np2 = n * nt;
-    double* buf = nullptr;
-    CU(cudaMalloc(&buf, sizeof(double) * (nh + ns + nmask + nvf + np1 + np2)));
+    DevScratch<double> scratch(nh + ns + nmask + nvf + np1 + np2);
+    double* buf = scratch.p;
     double *h = buf, *sp = h + nh, *mk = lp->mask ? sp + ns : nullptr, *vf = sp + ns + nmask,
            *p1 = vf + nvf, *p2 = p1 + np1;
     cudaError_t ce = cudaMemcpyAsync(h, lp->impulse, sizeof(double) * nh, cudaMemcpyHostToDevice, e->s);
@@ -2141,7 +2156,6 @@ dsel_status dsel_assemble_lti(dsel_engine* e, const dsel_lti* lp, double* noise_
       ce = cudaGetLastError();
     }
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(e->s);
-    cudaFree(buf);
     if (ce != cudaSuccess) throw Fail{DSEL_E_CUDA, std::string("assemble_lti: ") + cudaGetErrorString(ce)};
     e->full_panels = true;
     if (e->keep && e->C)
