@@ -1162,7 +1162,7 @@ struct LLDArgs {
 
 __global__ void __launch_bounds__(256) ll_dupdate_kernel(LLDArgs a) {
   constexpr int T = 64, KC = 16, LDK = KC + 4;
-  __shared__ __align__(16) double sA[T][LDK], sB[T][LDK];
+  __shared__ __align__(16) double sA[2][T][LDK], sB[2][T][LDK];  // double-buffered k-chunks
   const int h = blockIdx.y;
   const int tt = blockIdx.x;
   const int nti = a.n_tiles_1d;
@@ -1172,32 +1172,41 @@ __global__ void __launch_bounds__(256) ll_dupdate_kernel(LLDArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp & 3) * 16, wn = (warp >> 2) * 32;  // 8 warps: 4 x 2, warp tile 16 x 32
+  const bool diag = ti == tj;  // A == B: one load
   double acc[2][4][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  for (int k0 = 0; k0 < a.ldw; k0 += KC) {
-    for (int idx = tid; idx < 2 * T * (KC / 2); idx += 256) {
+  auto load = [&](int buf, int k0) {
+    const int n_sides = diag ? 1 : 2;
+    for (int idx = tid; idx < n_sides * T * (KC / 2); idx += 256) {
       const int which = idx / (T * (KC / 2));
       const int rem = idx - which * T * (KC / 2);
       const int row = rem / (KC / 2), ch = rem - row * (KC / 2);
       const int rr = (which ? tj : ti) * T + row;
       const bool ok = rr < nt;
       const double* src = a.Wown + wt_index(q * nt + (ok ? rr : 0), a.koff + k0 + 2 * ch, a.own_mpad);
-      double2 v = ok ? *reinterpret_cast<const double2*>(src) : make_double2(0.0, 0.0);
-      double* dst = which ? &sB[row][2 * ch] : &sA[row][2 * ch];
-      dst[0] = v.x;
-      dst[1] = v.y;
+      cp_async16(which ? &sB[buf][row][2 * ch] : &sA[buf][row][2 * ch], src, ok);
     }
+  };
+  const int nk = a.ldw / KC;
+  load(0, 0);
+  cp_async_commit();
+  for (int kc = 0; kc < nk; ++kc) {
+    if (kc + 1 < nk) load((kc + 1) & 1, (kc + 1) * KC);
+    cp_async_commit();
+    cp_async_wait<1>();
     __syncthreads();
+    const int b = kc & 1;
+    const double(*tB)[LDK] = diag ? sA[b] : sB[b];
 #pragma unroll
     for (int k4 = 0; k4 < KC / 4; ++k4) {
       double fa[2], fb[4];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) fa[i] = sA[wm + i * 8 + g][k4 * 4 + t];
+      for (int i = 0; i < 2; ++i) fa[i] = sA[b][wm + i * 8 + g][k4 * 4 + t];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) fb[j] = sB[wn + j * 8 + g][k4 * 4 + t];
+      for (int j = 0; j < 4; ++j) fb[j] = tB[wn + j * 8 + g][k4 * 4 + t];
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
