@@ -862,7 +862,10 @@ __global__ void __launch_bounds__(pw::THREADS, 2) panel_w_kernel(PanelArgs a) {
   double* sB = sA + STAGES * KC * LDA;                // [STAGES][BN][LDB]
   int* rowphys = reinterpret_cast<int*>(sB + STAGES * BN * LDB);
   const int tid = threadIdx.x;
-  const int r0 = blockIdx.x * BR, c0 = blockIdx.y * BN;
+  // column tiles in reverse launch order: the right-most tiles need the whole
+  // k range of the lower-triangular L_k^-1, the left-most only part of it, so
+  // the heavy tiles fill the first wave and the light ones the tail
+  const int r0 = blockIdx.x * BR, c0 = (gridDim.y - 1 - blockIdx.y) * BN;
   const int nt = a.nt;
   for (int i = tid; i < BR; i += THREADS) {
     const int r = r0 + i;
