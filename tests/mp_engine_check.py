@@ -51,6 +51,26 @@ if which == "random":
             if not ok:
                 bad += 1
                 print(f"rank {rank} MISMATCH nd={nd} nt={nt} {kw}", flush=True)
+    # candidate subsets (uneven ownership of the remaining positions)
+    nd, nt = 30, 6
+    k = O.random_hessian(nd, nt, 1.0, 100, 21)
+    cands = [0, 1, 2, 4, 7, 8, 11, 13, 17, 18, 22, 25, 29]
+    want = O.greedy_select(k, nd, nt, 7, candidates=cands)
+    for kw in (dict(), dict(algorithm="left"), dict(full_square=True)):
+        cid = [d.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(cid, src=0)
+        eng = d.Engine(nd, nt, 7, candidates=cands, device=local, world_size=world, rank=rank,
+                       nccl_id=cid[0], **kw)
+        eng.load_k(k)
+        eng.run()
+        rows = eng.trace()
+        eng.close()
+        ok = [r["chosen_index"] for r in rows] == list(want.chosen)
+        for r, g in zip(rows, want.gains):
+            ok = ok and abs(r["gain"] - g) <= 1e-9 * max(abs(g), 1.0)
+        if not ok:
+            bad += 1
+            print(f"rank {rank} MISMATCH subset {kw}", flush=True)
     print(f"rank {rank}/{world} random: {'OK' if not bad else 'MISMATCH'}", flush=True)
     dist.destroy_process_group()
     sys.exit(1 if bad else 0)
