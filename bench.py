@@ -339,8 +339,9 @@ def our_arm(args, world, rank, local):
                                f"(n={nd * nt}) select {budget}, rank {vrank}, sigma {SIGMA}, "
                                f"seed {SEED}, K resident in HBM",
                    "n_sensors": nd, "n_steps": nt, "budget": budget, "rank": vrank,
-                   "parallelism": f"candidate-sharded x{world} (cyclic block columns), "
-                                  "NCCL allgather(argmax) + all-reduce/broadcast(panel)",
+                   "parallelism": f"candidate-sharded x{world} (cyclic block columns); per round "
+                                  "NCCL allgather of the 32-B argmax records, W rows exchanged over "
+                                  "NVLink peer memory (one fused read+scatter kernel) when x>1",
                    "l2": f"inputs {nd * nt * nd * nt * 8 / 1e9:.2f} GB >> 126 MB L2 (no flush needed)",
                    "chosen_first": chosen[:8]},
         "algorithm": ALGO_DESC[args.algorithm],
