@@ -201,6 +201,7 @@ struct dsel_engine {
          *stage = nullptr, *xbuf = nullptr;
   int *status = nullptr, *kstatus = nullptr;
   int *d_pos_sensor = nullptr, *d_slot_sensor = nullptr;
+  unsigned* d_counter = nullptr;  // gain-launch ticket for the fused argmax (zero between launches)
   int* d_round = nullptr;  // per-round tables (one block, one upload): d_tab | d_sym | d_hb
   int* h_round = nullptr;  // pinned staging of the same layout
   size_t round_ints = 0;
@@ -399,7 +400,7 @@ GainTabs gain_tabs(dsel_engine* e) {
   return {base, base + e->nloc + 1, base + 2 * (e->nloc + 1)};
 }
 
-void run_gain(dsel_engine* e, const int* slots, int n_batch) {
+void run_gain(dsel_engine* e, const int* slots, int n_batch, ArgRec* rec = nullptr) {
   if (n_batch <= 0) return;
   GainTabs t = gain_tabs(e);
   gain_tables_kernel<<<(n_batch + 127) / 128, 128, 0, e->s>>>(
@@ -418,6 +419,9 @@ void run_gain(dsel_engine* e, const int* slots, int n_batch) {
   a.nt = e->nt;
   a.n = n_batch;
   a.mp = chol_mp(e->nt);
+  a.sensor = t.sensor;
+  a.rec = rec;  // fused local argmax (the last block of the launch)
+  a.counter = e->d_counter;
   launch_chol(a, n_batch, e->s, e->n_sms);
   CU(cudaGetLastError());
   e->launches += 2;
@@ -958,14 +962,17 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
     e->launches += 1;
   }
   const int n_batch = e->n_cols_tab;
-  run_gain(e, e->col_slot(), n_batch);
+  // the local top-2 is folded by the gain launch itself (last block); forced
+  // steps and empty batches use the separate pick / argmax kernels
+  const bool fused = forced < 0 && n_batch > 0;
+  run_gain(e, e->col_slot(), n_batch, fused ? e->d_rec : nullptr);
   GainTabs t = gain_tabs(e);
   if (forced >= 0)
     pick_kernel<<<1, 32, 0, e->s>>>(e->gains, e->status, t.sensor, n_batch, forced, e->d_rec);
-  else
+  else if (!fused)
     argmax_kernel<<<1, 256, 0, e->s>>>(e->gains, e->status, t.sensor, n_batch, e->d_rec);
   CU(cudaGetLastError());
-  e->launches += 1;
+  if (!fused) e->launches += 1;
   CU(cudaEventRecord(ev[1], e->s));
 
   // ---- cross-rank argmax: 32 B per rank ----
@@ -1322,6 +1329,7 @@ void destroy_impl(dsel_engine* e) {
   for (int* d : iptr)
     if (d) cudaFree(d);
   if (e->d_rec) cudaFree(e->d_rec);
+  if (e->d_counter) cudaFree(e->d_counter);
   if (e->d_recs) cudaFree(e->d_recs);
   if (e->h_recs) cudaFreeHost(e->h_recs);
   if (e->h_round) cudaFreeHost(e->h_round);
@@ -1507,6 +1515,8 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     e->d_pos_sensor = dmalloc<int>(e->nc, tot);
     e->d_slot_sensor = dmalloc<int>(e->nloc + 1, tot);
     e->d_rec = dmalloc<ArgRec>(1, tot);
+    e->d_counter = reinterpret_cast<unsigned*>(dmalloc<int>(1, tot));
+    CU(cudaMemsetAsync(e->d_counter, 0, sizeof(unsigned), e->s));
     e->d_recs = dmalloc<ArgRec>(e->G, tot);
     CU(cudaMallocHost(&e->h_recs, sizeof(ArgRec) * e->G));
     if (e->W) CU(cudaMemsetAsync(e->W, 0, sizeof(double) * (size_t)e->n * e->ldw, e->s));

@@ -1287,6 +1287,80 @@ __global__ void ll_extract_wk_kernel(const double* Wown, int own_mpad, int row0,
 // with lds = nt (column-major nt x nt per slot, slots side by side).
 
 // ------------------------------------------------------------------------ //
+// Local top-2 argmax with the reference tie rule (selector.hpp:132-134):   //
+// larger gain wins, exact ties go to the lower sensor index.              //
+// ------------------------------------------------------------------------ //
+using ArgRec = dsel_argrec;  // include/dsel.h
+
+__device__ __forceinline__ bool better(double d, int s, double bd, int bs) {
+  return d > bd || (d == bd && (bs < 0 || s < bs));
+}
+
+__device__ __forceinline__ void top2_insert(double d, int s, double& g1, int& s1, double& g2, int& s2) {
+  if (s < 0) return;
+  if (s1 < 0 || better(d, s, g1, s1)) {
+    g2 = g1;
+    s2 = s1;
+    g1 = d;
+    s1 = s;
+  } else if (s2 < 0 || better(d, s, g2, s2)) {
+    g2 = d;
+    s2 = s;
+  }
+}
+
+// Block-wide (256 threads) top-2 over n records; gain/status read through L2
+// (they may have been written by other blocks of the same launch).
+__device__ __forceinline__ void block_argmax(const double* gain, const int* status, const int* sensor, int n,
+                                             ArgRec* out) {
+  __shared__ double sg1[256], sg2[256];
+  __shared__ int ss1[256], ss2[256], sinf[256];
+  const int tid = threadIdx.x;
+  double g1 = -INFINITY, g2 = -INFINITY;
+  int s1 = -1, s2 = -1, ninf = 0;
+  for (int i = tid; i < n; i += 256) {
+    if (__ldcg(status + i) >= 0) {
+      ++ninf;
+      continue;
+    }
+    top2_insert(__ldcg(gain + i), sensor[i], g1, s1, g2, s2);
+  }
+  sg1[tid] = g1;
+  sg2[tid] = g2;
+  ss1[tid] = s1;
+  ss2[tid] = s2;
+  sinf[tid] = ninf;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (tid < w) {
+      double a1 = sg1[tid], a2 = sg2[tid];
+      int b1 = ss1[tid], b2 = ss2[tid];
+      top2_insert(sg1[tid + w], ss1[tid + w], a1, b1, a2, b2);
+      top2_insert(sg2[tid + w], ss2[tid + w], a1, b1, a2, b2);
+      sg1[tid] = a1;
+      sg2[tid] = a2;
+      ss1[tid] = b1;
+      ss2[tid] = b2;
+      sinf[tid] += sinf[tid + w];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    out->g1 = sg1[0];
+    out->g2 = sg2[0];
+    out->s1 = ss1[0];
+    out->s2 = ss2[0];
+    out->n_eval = n;
+    out->n_inf = sinf[0];
+  }
+}
+
+__global__ void __launch_bounds__(256) argmax_kernel(const double* gain, const int* status,
+                                                     const int* sensor, int n, ArgRec* out) {
+  block_argmax(gain, status, sensor, n, out);
+}
+
+// ------------------------------------------------------------------------ //
 // Gain kernel: batched nt x nt Cholesky + log-determinant (north-star (3)). //
 // One CTA per candidate; left-looking by NB-wide column panels held in     //
 // shared memory, previous factor columns staged from an L2-resident       //
@@ -1305,7 +1379,30 @@ struct CholArgs {
   int nt;
   int n;                    // batch size
   int mp;                   // smem pitch (>= nt)
+  // fused local argmax: the last block to finish (atomic ticket) reduces all
+  // gains into rec (null: no argmax, e.g. gain peeks and forced steps)
+  const int* sensor;
+  ArgRec* rec;
+  unsigned* counter;        // zero between launches (reset by the last block)
 };
+
+// common tail of the gain kernels: this block's gain is written; the last
+// block of the launch folds every gain into the local top-2 record
+__device__ __forceinline__ void gain_epilogue(const CholArgs& a) {
+  if (!a.rec) return;
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(a.counter, 1u) == (unsigned)a.n - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    block_argmax(a.gain, a.status, a.sensor, a.n, a.rec);
+    if (threadIdx.x == 0) *a.counter = 0u;
+  }
+}
 
 // 1/sqrt(p) for the pivot chain: hardware fp32 seed + 3 Newton steps in fp64
 // (relative error ~1e-16; shorter dependency chain than the library rsqrt,
@@ -1519,26 +1616,27 @@ __global__ void __launch_bounds__(256, MINB) chol_logdet_kernel(CholArgs a) {
       a.status[b] = s_fail;
       a.gain[b] = -INFINITY;
     }
-    return;
-  }
-  // log det = 2 sum log(d_j): fixed-order (deterministic) reduction
-  double part = 0.0;
-  for (int j = tid; j < nt; j += 256) part += log(diagv[j]);
+  } else {
+    // log det = 2 sum log(d_j): fixed-order (deterministic) reduction
+    double part = 0.0;
+    for (int j = tid; j < nt; j += 256) part += log(diagv[j]);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
-  if (lane == 0) s_red[warp] = part;
-  __syncthreads();
-  if (tid == 0) {
-    double s = 0.0;
-    for (int w = 0; w < 8; ++w) s += s_red[w];
-    a.status[b] = -1;
-    a.gain[b] = 2.0 * s;
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
+    if (lane == 0) s_red[warp] = part;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < 8; ++w) s += s_red[w];
+      a.status[b] = -1;
+      a.gain[b] = 2.0 * s;
 #ifdef DSEL_PROBE
-    unsigned long long t1;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-    g_tend[b] = t1;
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      g_tend[b] = t1;
 #endif
+    }
   }
+  gain_epilogue(a);
 }
 
 // ------------------------------------------------------------------------ //
@@ -1672,20 +1770,21 @@ __global__ void __launch_bounds__(256, MINB) chol_logdet_tri_kernel(CholArgs a) 
       a.status[b] = s_fail;
       a.gain[b] = -INFINITY;
     }
-    return;
-  }
-  double part = 0.0;  // log det = 2 sum log(d_j), fixed-order reduction
-  for (int j = tid; j < nt; j += 256) part += log(diagv[j]);
+  } else {
+    double part = 0.0;  // log det = 2 sum log(d_j), fixed-order reduction
+    for (int j = tid; j < nt; j += 256) part += log(diagv[j]);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
-  if (lane == 0) s_red[warp] = part;
-  __syncthreads();
-  if (tid == 0) {
-    double s = 0.0;
-    for (int w = 0; w < 8; ++w) s += s_red[w];
-    a.status[b] = -1;
-    a.gain[b] = 2.0 * s;
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
+    if (lane == 0) s_red[warp] = part;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < 8; ++w) s += s_red[w];
+      a.status[b] = -1;
+      a.gain[b] = 2.0 * s;
+    }
   }
+  gain_epilogue(a);
 }
 
 // ------------------------------------------------------------------------ //
@@ -1809,73 +1908,6 @@ __global__ void __launch_bounds__(256) trinv_smem_kernel(const double* L, int nt
   for (int s = 0; s < S; ++s) {
     const int i = lane + 32 * s;
     if (i < ldl) Linv[(size_t)i * ldl + j] = (j < nt && i < nt && i >= j) ? x[s] : 0.0;
-  }
-}
-
-// ------------------------------------------------------------------------ //
-// Local top-2 argmax with the reference tie rule (selector.hpp:132-134):   //
-// larger gain wins, exact ties go to the lower sensor index.              //
-// ------------------------------------------------------------------------ //
-using ArgRec = dsel_argrec;  // include/dsel.h
-
-__device__ __forceinline__ bool better(double d, int s, double bd, int bs) {
-  return d > bd || (d == bd && (bs < 0 || s < bs));
-}
-
-__device__ __forceinline__ void top2_insert(double d, int s, double& g1, int& s1, double& g2, int& s2) {
-  if (s < 0) return;
-  if (s1 < 0 || better(d, s, g1, s1)) {
-    g2 = g1;
-    s2 = s1;
-    g1 = d;
-    s1 = s;
-  } else if (s2 < 0 || better(d, s, g2, s2)) {
-    g2 = d;
-    s2 = s;
-  }
-}
-
-__global__ void __launch_bounds__(256) argmax_kernel(const double* gain, const int* status,
-                                                     const int* sensor, int n, ArgRec* out) {
-  __shared__ double sg1[256], sg2[256];
-  __shared__ int ss1[256], ss2[256], sinf[256];
-  const int tid = threadIdx.x;
-  double g1 = -INFINITY, g2 = -INFINITY;
-  int s1 = -1, s2 = -1, ninf = 0;
-  for (int i = tid; i < n; i += 256) {
-    if (status[i] >= 0) {
-      ++ninf;
-      continue;
-    }
-    top2_insert(gain[i], sensor[i], g1, s1, g2, s2);
-  }
-  sg1[tid] = g1;
-  sg2[tid] = g2;
-  ss1[tid] = s1;
-  ss2[tid] = s2;
-  sinf[tid] = ninf;
-  __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
-    if (tid < w) {
-      double a1 = sg1[tid], a2 = sg2[tid];
-      int b1 = ss1[tid], b2 = ss2[tid];
-      top2_insert(sg1[tid + w], ss1[tid + w], a1, b1, a2, b2);
-      top2_insert(sg2[tid + w], ss2[tid + w], a1, b1, a2, b2);
-      sg1[tid] = a1;
-      sg2[tid] = a2;
-      ss1[tid] = b1;
-      ss2[tid] = b2;
-      sinf[tid] += sinf[tid + w];
-    }
-    __syncthreads();
-  }
-  if (tid == 0) {
-    out->g1 = sg1[0];
-    out->g2 = sg2[0];
-    out->s1 = ss1[0];
-    out->s2 = ss2[0];
-    out->n_eval = n;
-    out->n_inf = sinf[0];
   }
 }
 

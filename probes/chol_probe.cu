@@ -30,7 +30,7 @@ int main(int argc, char** argv) {
   for (int b = 0; b < batch; ++b) cols[b] = b * nt;  // block b = columns b*nt.., rows 0..nt (ld = nt)
   cudaMemcpy(sc, cols.data(), batch * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(sr, rows.data(), batch * 4, cudaMemcpyHostToDevice);
-  CholArgs a; a.src = src; a.lds = nt; a.src_col = sc; a.src_row = sr; a.L = L; a.l_stride = n2;
+  CholArgs a{}; a.src = src; a.lds = nt; a.src_col = sc; a.src_row = sr; a.L = L; a.l_stride = n2;
   a.gain = gain; a.status = st; a.nt = nt; a.n = batch; a.mp = mp;
   size_t smem = ((size_t)2 * PROBE_NB * mp + nt) * 8;
   cudaFuncSetAttribute(chol_logdet_kernel<PROBE_NB, PROBE_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
