@@ -479,3 +479,15 @@ def test_naive_refactorizing_baseline_gpu(O, golden_dir):
     rows, slopes = cg.sweep(nt=8, k_max=12, step=4, reps=2, batch=4)
     assert [r["k"] for r in rows] == [4, 8, 12]
     assert all(r["naive_ms"] > 0 and r["schur_ms"] > 0 and r["engine_round_ms"] > 0 for r in rows)
+
+
+def test_out_of_memory_is_a_clean_error(dsel):
+    """A store that cannot fit in HBM fails at create with DSEL_E_OOM (WorkerFailure),
+    frees what it allocated, and the device stays usable."""
+    with pytest.raises(dsel.WorkerFailure) as ei:
+        dsel.Engine(4000, 420, 10)          # n = 1.68M: a 22 TB panel store
+    assert "OOM" in str(ei.value) or "cudaMalloc" in str(ei.value)
+    with dsel.Engine(8, 2, 2) as eng:       # the device is still usable
+        eng.load_k(np.eye(16).reshape(8, 2, 8, 2).transpose(0, 2, 1, 3).copy().reshape(-1) * 2.0)
+        eng.run()
+        assert len(eng.trace()) == 2
