@@ -375,7 +375,7 @@ int chol_mp(int nt) {
 
 void launch_chol(const CholArgs& a, int n_batch, cudaStream_t s, int n_sms) {
   const int nb = chol_nb(a.nt);
-  const size_t smem = ((size_t)2 * nb * a.mp + a.nt) * sizeof(double);
+  const size_t smem = ((size_t)nb * a.mp + a.nt) * sizeof(double);
   // more candidates than SMs: squeeze two CTAs per SM (capped registers) so the
   // batch runs in one wave; otherwise one uncapped CTA per candidate
   const bool two = n_batch > n_sms;

@@ -1487,8 +1487,7 @@ __global__ void __launch_bounds__(256, MINB) chol_logdet_kernel(CholArgs a) {
   if (b >= a.n) return;
   const int nt = a.nt, mp = a.mp;
   double* S = reinterpret_cast<double*>(smem_raw);  // [NB][mp] panel, column-major
-  double* Lc = S + NB * mp;                         // [NB][mp] staged factor columns
-  double* diagv = Lc + NB * mp;                     // [nt] pivots sqrt
+  double* diagv = S + NB * mp;                      // [nt] pivots sqrt
   __shared__ double rdiag[NB];                      // 1/d of the current panel
   __shared__ __align__(16) double s_colbuf[64];     // diag factorization column broadcast
   __shared__ int s_fail;
@@ -1521,36 +1520,40 @@ __global__ void __launch_bounds__(256, MINB) chol_logdet_kernel(CholArgs a) {
       cp_async8(S + j * mp + i, src + (size_t)(J0 + j) * a.lds + J0 + i, true);
     }
     cp_async_commit();
-    // left-looking: S -= L[J0:, kk:kk+NB] * L[J0:J0+nb, kk:kk+NB]^T on DMMA
-    for (int kk = 0; kk < J0; kk += NB) {
-      __syncthreads();
-      for (int e = tid; e < NB * m; e += 256) {
-        const int c = e / m, i = e - c * m;
-        cp_async8(Lc + c * mp + i, L + (size_t)(kk + c) * nt + J0 + i, true);
-      }
-      cp_async_commit();
+    // left-looking: S -= L[J0:, 0:J0] * L[J0:J0+nb, 0:J0]^T on DMMA, the factor
+    // fragments read straight from the L2-resident scratch (written by this
+    // block's earlier panels): no staging round trip per earlier panel, the
+    // loads of the two warps of an SM sub-partition overlap each other's math
+    if (J0 > 0) {
       cp_async_wait<0>();
       __syncthreads();
       const int mt_n = (m + 7) >> 3;
       constexpr int NT8 = NB / 8;
-      // each warp owns an m8 row and all NB/8 n-tiles: independent DMMA chains
       for (int mt = warp; mt < mt_n; mt += 8) {
         double acc[NT8][2];
 #pragma unroll
         for (int n8 = 0; n8 < NT8; ++n8) acc[n8][0] = acc[n8][1] = 0.0;
+        const int ia = mt * 8 + g;
+        for (int kk = 0; kk < J0; kk += NB) {
+          double av[NB / 4], bv[NB / 4][NT8];
 #pragma unroll
-        for (int k4 = 0; k4 < NB / 4; ++k4) {
-          const double av = Lc[(k4 * 4 + t) * mp + mt * 8 + g];
+          for (int k4 = 0; k4 < NB / 4; ++k4) {
+            const double* col = L + (size_t)(kk + k4 * 4 + t) * nt + J0;
+            av[k4] = ia < m ? __ldcg(col + ia) : 0.0;
 #pragma unroll
-          for (int n8 = 0; n8 < NT8; ++n8) dmma884(acc[n8], av, Lc[(k4 * 4 + t) * mp + n8 * 8 + g]);
+            for (int n8 = 0; n8 < NT8; ++n8) bv[k4][n8] = n8 * 8 + g < nb ? __ldcg(col + n8 * 8 + g) : 0.0;
+          }
+#pragma unroll
+          for (int k4 = 0; k4 < NB / 4; ++k4)
+#pragma unroll
+            for (int n8 = 0; n8 < NT8; ++n8) dmma884(acc[n8], av[k4], bv[k4][n8]);
         }
-        const int i = mt * 8 + g;
-        if (i < m) {
+        if (ia < m) {
 #pragma unroll
           for (int n8 = 0; n8 < NT8; ++n8) {
             const int j0 = n8 * 8 + 2 * t;
-            if (j0 < nb) S[j0 * mp + i] -= acc[n8][0];
-            if (j0 + 1 < nb) S[(j0 + 1) * mp + i] -= acc[n8][1];
+            if (j0 < nb) S[j0 * mp + ia] -= acc[n8][0];
+            if (j0 + 1 < nb) S[(j0 + 1) * mp + ia] -= acc[n8][1];
           }
         }
       }

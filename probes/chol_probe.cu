@@ -32,7 +32,7 @@ int main(int argc, char** argv) {
   cudaMemcpy(sr, rows.data(), batch * 4, cudaMemcpyHostToDevice);
   CholArgs a{}; a.src = src; a.lds = nt; a.src_col = sc; a.src_row = sr; a.L = L; a.l_stride = n2;
   a.gain = gain; a.status = st; a.nt = nt; a.n = batch; a.mp = mp;
-  size_t smem = ((size_t)2 * PROBE_NB * mp + nt) * 8;
+  size_t smem = ((size_t)PROBE_NB * mp + nt) * 8;
   cudaFuncSetAttribute(chol_logdet_kernel<PROBE_NB, PROBE_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   for (int r = 0; r < 3; ++r) chol_logdet_kernel<PROBE_NB, PROBE_MINB><<<batch, 256, smem>>>(a);
