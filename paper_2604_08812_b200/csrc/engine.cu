@@ -1100,6 +1100,15 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
     }
     sym_tables(e, false);
     upload_round(e);
+    {
+      // blocks below the chosen one (position > p, in panel k at its owner)
+      // are read in place by the W solve: only the transposed ones above it
+      // are gathered -- a prefix of the position-ordered list
+      const int* lp = e->G > 1 ? e->h_hb + e->nc + e->hb_off[e->rank] : e->h_tab;
+      int n_lt = 0;
+      while (n_lt < n_gather && lp[n_lt] < p) ++n_lt;
+      n_gather = n_lt;
+    }
     if (n_gather > 0) {  // every listed block is held by this rank
       const int tpb = (nt + 31) / 32;
       gather_panel_sym_tiled_kernel<<<(unsigned)((long long)n_gather * tpb * tpb), 256, 0, e->s>>>(
@@ -1123,6 +1132,8 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       PanelArgs pa{};
       pa.P = P;
       pa.ldp = e->n;
+      pa.P2 = owner == e->rank ? e->C + (size_t)q * nt * e->n : nullptr;
+      pa.pk = p;
       pa.Linv = e->Linv;
       pa.ldl = e->ldw;
       pa.W = e->Wsend;
@@ -1182,6 +1193,10 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       PanelArgs pa{};
       pa.P = P;
       pa.ldp = e->n;
+      if (e->sym) {  // G == 1: this rank owns panel k
+        pa.P2 = e->C + (size_t)q * nt * e->n;
+        pa.pk = p;
+      }
       pa.Linv = e->Linv;
       pa.ldl = e->ldw;
       pa.W = e->Wt ? nullptr : e->W;

@@ -825,12 +825,17 @@ constexpr int LDA = BR + 4;  // sA is [KC][LDA] (k-major, r contiguous)
 constexpr int LDB = KC + 4;  // sB is [BN][LDB]
 constexpr int STAGES = 3;
 constexpr int THREADS = 256;
-constexpr size_t SMEM = (size_t)STAGES * (KC * LDA + BN * LDB) * sizeof(double) + BR * sizeof(int);
+constexpr size_t SMEM = (size_t)STAGES * (KC * LDA + BN * LDB) * sizeof(double) + 2 * BR * sizeof(int);
 }  // namespace pw
 
 struct PanelArgs {
   const double* P;      // panel, column-major, element (row, m) at P[m*ldp + row]
   long long ldp;
+  // symmetric storage: rows of blocks below the chosen one (position > pk)
+  // are read in place from the chosen candidate's own panel P2 (same ldp);
+  // only the transposed blocks above it were gathered into P (null: all P)
+  const double* P2;
+  int pk;
   const double* Linv;   // row-major [c][m], ld = ldl, zero above the diagonal and in pads
   int ldl;
   double* W;            // out, row-major, ld = ldw; may be null
@@ -861,6 +866,7 @@ __global__ void __launch_bounds__(pw::THREADS, 2) panel_w_kernel(PanelArgs a) {
   double* sA = reinterpret_cast<double*>(smem_raw);  // [STAGES][KC][LDA]
   double* sB = sA + STAGES * KC * LDA;                // [STAGES][BN][LDB]
   int* rowphys = reinterpret_cast<int*>(sB + STAGES * BN * LDB);
+  int* rowsrc = rowphys + BR;  // 1: row read from P2
   const int tid = threadIdx.x;
   // column tiles in reverse launch order: the right-most tiles need the whole
   // k range of the lower-triangular L_k^-1, the left-most only part of it, so
@@ -871,9 +877,12 @@ __global__ void __launch_bounds__(pw::THREADS, 2) panel_w_kernel(PanelArgs a) {
     const int r = r0 + i;
     if (r < a.n_rows) {
       const int blk = r / nt;
-      rowphys[i] = a.row_pos[blk] * nt + (r - blk * nt);
+      const int pos = a.row_pos[blk];
+      rowphys[i] = pos * nt + (r - blk * nt);
+      rowsrc[i] = a.P2 != nullptr && pos > a.pk;
     } else {
       rowphys[i] = -1;
+      rowsrc[i] = 0;
     }
   }
   __syncthreads();
@@ -890,7 +899,7 @@ __global__ void __launch_bounds__(pw::THREADS, 2) panel_w_kernel(PanelArgs a) {
         const int rr = (idx - k * (BR / 2)) * 2;
         const int pr = rowphys[rr];
         const bool ok = pr >= 0 && kc + k < nt;
-        const double* src = a.P + (ok ? (size_t)(kc + k) * a.ldp + pr : 0);
+        const double* src = (rowsrc[rr] ? a.P2 : a.P) + (ok ? (size_t)(kc + k) * a.ldp + pr : 0);
         cp_async16(dA + k * LDA + rr, src, ok);
       }
     } else {
@@ -899,7 +908,7 @@ __global__ void __launch_bounds__(pw::THREADS, 2) panel_w_kernel(PanelArgs a) {
         const int rr = idx - k * BR;
         const int pr = rowphys[rr];
         const bool ok = pr >= 0 && kc + k < nt;
-        const double* src = a.P + (ok ? (size_t)(kc + k) * a.ldp + pr : 0);
+        const double* src = (rowsrc[rr] ? a.P2 : a.P) + (ok ? (size_t)(kc + k) * a.ldp + pr : 0);
         cp_async8(dA + k * LDA + rr, src, ok);
       }
     }
