@@ -181,6 +181,8 @@ struct dsel_engine {
   unsigned long long* flag = nullptr;  // this rank's published round sequence
   unsigned long long seq = 0;
   std::vector<double*> peer_wsend, peer_lscr, peer_lk;  // peer_wsend: Wsend (right) / Wkn (left)
+  std::vector<double*> peer_c;  // the peers' panel shards (symmetric right-looking W solve)
+  std::vector<int> h_holder;     // per-round W-row holder of each live block (host scratch)
   std::vector<unsigned long long*> peer_flag;
   std::vector<void*> ipc_opened;
   const double** d_peer_wsend = nullptr;
@@ -492,7 +494,7 @@ void ws_balance(int n_tiles, int n_k, int sms, int max_s, int br, int& n_full, i
 // left-looking), gain scratch, round flag and L_k buffer (NVLink peer memory).
 // All ranks take the same decision (min-reduced): the per-round collective
 // sequence depends on it. DSEL_P2P=0 keeps the NCCL exchange.
-constexpr int kPeerBufs = 4;  // 0 exchange, 1 Lscr, 2 flag, 3 Lk
+constexpr int kPeerBufs = 5;  // 0 exchange, 1 Lscr, 2 flag, 3 Lk, 4 C (panels)
 struct PeerInfo {
   cudaIpcMemHandle_t h[kPeerBufs];
   void* p[kPeerBufs];
@@ -505,7 +507,8 @@ void setup_p2p(dsel_engine* e) {
   const int G = e->G;
   CU(cudaMalloc(&e->flag, 256));
   CU(cudaMemset(e->flag, 0, 256));
-  void* bufs[kPeerBufs] = {e->Wsend ? (void*)e->Wsend : (void*)e->Wkn, e->Lscr, e->flag, e->Lk};
+  void* bufs[kPeerBufs] = {e->Wsend ? (void*)e->Wsend : (void*)e->Wkn, e->Lscr, e->flag, e->Lk,
+                           e->C ? (void*)e->C : (void*)e->Lk};
   PeerInfo mine{};
   mine.pid = (long long)getpid();
   mine.dev = e->dev;
@@ -570,11 +573,13 @@ void setup_p2p(dsel_engine* e) {
   e->peer_lscr.assign(G, nullptr);
   e->peer_flag.assign(G, nullptr);
   e->peer_lk.assign(G, nullptr);
+  e->peer_c.assign(G, nullptr);
   for (int r = 0; r < G; ++r) {
     e->peer_wsend[r] = static_cast<double*>(peer[0][r]);
     e->peer_lscr[r] = static_cast<double*>(peer[1][r]);
     e->peer_flag[r] = static_cast<unsigned long long*>(peer[2][r]);
     e->peer_lk[r] = static_cast<double*>(peer[3][r]);
+    e->peer_c[r] = static_cast<double*>(peer[4][r]);
   }
   CU(cudaMalloc(&e->d_peer_wsend, sizeof(double*) * G));
   CU(cudaMalloc(&e->d_peer_flag, sizeof(unsigned long long*) * G));
@@ -1077,15 +1082,25 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       const int* rp = e->h_tab;
       int* hb = e->h_hb;
       int* hbpos = e->h_hb + e->nc;
+      // W-row holders: a block above the chosen one is held (transposed) by
+      // its own panel's rank; the blocks below it sit in panel k at the owner.
+      // With peer memory they are dealt round-robin to every rank, each
+      // reading its share of panel k over NVLink inside the W solve, so the
+      // solve and the serving of W rows are balanced (not ~half on the owner)
       e->hb_off.assign(e->G + 1, 0);
+      std::vector<int>& hrank = e->h_holder;
+      hrank.resize(R);
+      for (int h = 0, j = 0; h < R; ++h) {
+        const int pos = rp[h];
+        hrank[h] = pos < p ? pos % e->G : (e->p2p ? (j++ % e->G) : owner);
+      }
       int m = 0;
       for (int r = 0; r < e->G; ++r) {
         e->hb_off[r] = m;
         for (int h = 0; h < R; ++h) {
-          const int pos = rp[h];
-          if ((pos > p ? owner : pos % e->G) == r) {
+          if (hrank[h] == r) {
             hb[m] = h;
-            hbpos[m] = pos;
+            hbpos[m] = rp[h];
             ++m;
           }
         }
@@ -1132,7 +1147,8 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       PanelArgs pa{};
       pa.P = P;
       pa.ldp = e->n;
-      pa.P2 = owner == e->rank ? e->C + (size_t)q * nt * e->n : nullptr;
+      pa.P2 = (owner == e->rank ? e->C : e->p2p ? e->peer_c[owner] : nullptr);
+      if (pa.P2) pa.P2 += (size_t)q * nt * e->n;
       pa.pk = p;
       pa.Linv = e->Linv;
       pa.ldl = e->ldw;
