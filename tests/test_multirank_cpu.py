@@ -125,3 +125,93 @@ def test_fold_records_tie_rule_and_associativity():
         cut = int(rng.integers(1, len(perm)))
         left, right = fold_records(perm[:cut]), fold_records(perm[cut:])
         assert fold_records([left, right])[:4] == full[:4]
+
+
+def _sym_rank_main(rank, world, port, nd, nt, budget, k_flat, out_q):
+    """The symmetric (block-lower) multi-rank round of engine.cu step_impl:
+    panel j keeps blocks (i, j) with position i >= j; C[:,k] is assembled from
+    the blocks below k (owner's panel k) and the transposed blocks above k
+    (panel i at i's rank); W-row holders: above k -> i % world, below k ->
+    dealt round-robin (each holder reads its share of the owner's panel k,
+    here a broadcast of that panel standing in for the NVLink read)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2604_08812_b200 import fold_records
+    from oracle import oracle as O
+
+    K = O.blocks_to_dense(np.asarray(k_flat), nd, nt)
+    blk = lambda i, j: K[i * nt:(i + 1) * nt, j * nt:(j + 1) * nt].copy()  # noqa: E731
+    mine = [p for p in range(nd) if p % world == rank]
+    C = {j: {i: blk(i, j) for i in range(j, nd)} for j in mine}      # block-lower panels
+    alive = [True] * nd
+    seq, gains_out = [], []
+    for _ in range(budget):
+        live_local = [j for j in mine if alive[j]]
+        g = [2.0 * np.log(np.diag(np.linalg.cholesky(C[j][j]))).sum() for j in live_local]
+        allr = [torch.zeros(6, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(allr, torch.tensor(_record(g, live_local), dtype=torch.float64))
+        g1, k, *_ = fold_records([(float(r[0]), int(r[1]), float(r[2]), int(r[3]), int(r[4]), int(r[5]))
+                                  for r in allr])
+        owner = k % world
+        below = torch.zeros(nd, nt, nt, dtype=torch.float64)   # owner's panel k, rows below k
+        if owner == rank:
+            for i in range(k + 1, nd):
+                below[i] = torch.from_numpy(C[k][i])
+        dist.broadcast(below, src=owner)
+        Lk = np.linalg.cholesky(C[k][k]) if owner == rank else np.zeros((nt, nt))
+        Lt = torch.from_numpy(Lk)
+        dist.broadcast(Lt, src=owner)
+        Lk = Lt.numpy()
+        alive[k] = False
+        live = [i for i in range(nd) if alive[i]]
+        holder, j = {}, 0
+        for i in live:
+            if i < k:
+                holder[i] = i % world
+            else:
+                holder[i] = j % world
+                j += 1
+        assert sorted(holder) == live                              # every block exactly once
+        Wmine = torch.zeros(nd, nt, nt, dtype=torch.float64)
+        for i in live:
+            if holder[i] != rank:
+                continue
+            P = C[i][k].T if i < k else below[i].numpy()            # block (i, k) of C[:,k]
+            Wmine[i] = torch.from_numpy(np.linalg.solve(Lk, P.T).T)
+        dist.all_reduce(Wmine)                                      # one contributor per block
+        W = Wmine.numpy()
+        for jj in mine:
+            if alive[jj]:
+                for i in range(jj, nd):
+                    if alive[i]:
+                        C[jj][i] -= W[i] @ W[jj].T
+        seq.append(k)
+        gains_out.append(g1)
+    out_q.put((rank, seq, gains_out))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_symmetric_protocol_balanced_holders():
+    from oracle import oracle as O
+
+    nd, nt, budget = 13, 4, 8
+    k = O.random_hessian(nd, nt, 0.9, 48, 4321)
+    want = O.greedy_select(k, nd, nt, budget)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sym_rank_main, args=(r, 2, port, nd, nt, budget, k.tolist(), q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, seq, gains in res:
+        assert seq == want.chosen, (rank, seq, want.chosen)
+        for a, b in zip(gains, want.gains):
+            assert abs(a - b) <= 1e-9 * max(abs(b), 1.0)
