@@ -507,8 +507,8 @@ void setup_p2p(dsel_engine* e) {
   const int G = e->G;
   CU(cudaMalloc(&e->flag, 256));
   CU(cudaMemset(e->flag, 0, 256));
-  void* bufs[kPeerBufs] = {e->Wsend ? (void*)e->Wsend : (void*)e->Wkn, e->Lscr, e->flag, e->Lk,
-                           e->C ? (void*)e->C : (void*)e->Lk};
+  // buffer 4 (the panel shard) is absent with a streaming store: not mapped
+  void* bufs[kPeerBufs] = {e->Wsend ? (void*)e->Wsend : (void*)e->Wkn, e->Lscr, e->flag, e->Lk, e->C};
   PeerInfo mine{};
   mine.pid = (long long)getpid();
   mine.dev = e->dev;
@@ -516,6 +516,7 @@ void setup_p2p(dsel_engine* e) {
   mine.ok = !(env && atoi(env) == 0) && bufs[0] != nullptr;
   for (int b = 0; b < kPeerBufs && mine.ok; ++b) {
     mine.p[b] = bufs[b];
+    if (b == 4 && !bufs[b]) continue;
     mine.ok = cudaIpcGetMemHandle(&mine.h[b], bufs[b]) == cudaSuccess;
   }
   cudaGetLastError();
@@ -547,6 +548,7 @@ void setup_p2p(dsel_engine* e) {
     } else {  // another process: CUDA IPC
       for (int b = 0; b < kPeerBufs && ok; ++b) {
         void* m = nullptr;
+        if (!all[r].p[b]) continue;  // not exported (streaming store)
         if (cudaIpcOpenMemHandle(&m, all[r].h[b], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
           e->ipc_opened.push_back(m);
           peer[b][r] = m;

@@ -1995,34 +1995,10 @@ __global__ void gather_block_row_kernel(const double* panel, long long ldc, int 
   }
 }
 
-// Symmetric (block-lower) storage: column k of C for the live blocks, into a
-// full-height panel P (column-major, physical rows). Block (i,k) is stored in
-// panel k when p_i >= p_k, else as block (k,i)^T in panel i. Each rank writes
-// the blocks whose source panel it owns (the others stay zero for the
-// all-reduce that assembles P across ranks).
-__global__ void gather_panel_sym_kernel(const double* C, long long ldc, int nt, const int* row_pos,
-                                        int n_blocks, int pk, int G, int rank, double* P) {
-  const long long n2 = (long long)nt * nt;
-  const long long total = n2 * n_blocks;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int blk = (int)(e / n2);
-    const long long w = e - (long long)blk * n2;
-    const int c = (int)(w / nt), r = (int)(w - (long long)c * nt);  // P[(pi*nt + r), c]
-    const int pi = row_pos[blk];
-    double v;
-    if (pi >= pk) {
-      if (pk % G != rank) continue;
-      v = C[(size_t)((pk / G) * nt + c) * ldc + (size_t)pi * nt + r];
-    } else {
-      if (pi % G != rank) continue;
-      v = C[(size_t)((pi / G) * nt + r) * ldc + (size_t)pk * nt + c];
-    }
-    P[(size_t)c * ldc + (size_t)pi * nt + r] = v;
-  }
-}
-
-// Same gather, tiled: one CTA per 32 x 32 sub-tile of a block, both the direct
+// Symmetric (block-lower) storage: the blocks of column k of C this rank
+// holds, into a full-height panel P (column-major, physical rows). Block (i,k)
+// is stored in panel k when p_i >= p_k, else as block (k,i)^T in panel i.
+// One CTA per 32 x 32 sub-tile of a block, both the direct
 // (p_i > p_k) and the transposed (p_i < p_k) sources read along their
 // contiguous dimension, the transpose through shared memory.
 __global__ void __launch_bounds__(256) gather_panel_sym_tiled_kernel(const double* C, long long ldc, int nt,
