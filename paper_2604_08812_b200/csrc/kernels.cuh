@@ -1438,26 +1438,31 @@ __device__ __forceinline__ void diag_upd_s(double (&r)[NB], const double* col) {
   if constexpr (C < NB) {
     if constexpr (C + 1 < NB && (C % 2) == 0) {
       const double2 v = *reinterpret_cast<const double2*>(col + C);
-      r[C] -= r[J] * v.x;
-      r[C + 1] -= r[J] * v.y;
+      r[C] = fma(-r[J], v.x, r[C]);
+      r[C + 1] = fma(-r[J], v.y, r[C + 1]);
       diag_upd_s<J, C + 2, NB>(r, col);
     } else {
-      r[C] -= r[J] * col[C];
+      r[C] = fma(-r[J], col[C], r[C]);
       diag_upd_s<J, C + 1, NB>(r, col);
     }
   }
 }
+// pv: this pivot's value on lane J, computed lane-locally by the previous step
+// (r[J] - r[J-1]^2 on lane J is exactly what the shared-memory update below
+// produces there), so the pivot chain skips the shared-memory round trip.
 template <int J, int NB>
 __device__ __forceinline__ void diag_step(double (&r)[NB], int lane, int nb, double* dv, double* rdv,
-                                          int& fail, double* colbuf) {
+                                          int& fail, double* colbuf, double pv) {
   if constexpr (J < NB) {
-    const double piv = __shfl_sync(0xffffffffu, r[J], J);
+    const double piv = __shfl_sync(0xffffffffu, pv, J);
     const bool bad = !(piv > 0.0) || !isfinite(piv);
     if (bad && fail < 0 && J < nb) fail = J;
     const double p2 = bad ? 1.0 : piv;
     const double rd = fast_rsqrt(p2);
     const double d = p2 * rd;
     r[J] = lane == J ? d : r[J] * rd;
+    double pn = 0.0;
+    if constexpr (J + 1 < NB) pn = fma(-r[J], r[J], r[J + 1]);
     if (lane == 0 && J < nb) {
       dv[J] = d;
       rdv[J] = rd;
@@ -1466,7 +1471,7 @@ __device__ __forceinline__ void diag_step(double (&r)[NB], int lane, int nb, dou
     col[lane] = r[J];
     __syncwarp();
     diag_upd_s<J, J + 1, NB>(r, col);
-    diag_step<J + 1, NB>(r, lane, nb, dv, rdv, fail, colbuf);
+    diag_step<J + 1, NB>(r, lane, nb, dv, rdv, fail, colbuf, pn);
   }
 }
 template <int J, int C, int NB>
@@ -1579,7 +1584,7 @@ __global__ void __launch_bounds__(256, MINB) chol_logdet_kernel(CholArgs a) {
         r[c] = (lane < nb && c < nb) ? (c <= lane ? S[c * mp + lane] : 0.0)
                                      : (c == lane ? 1.0 : 0.0);
       int fail = -1;
-      diag_step<0, NB>(r, lane, nb, diagv + J0, rdiag, fail, s_colbuf);
+      diag_step<0, NB>(r, lane, nb, diagv + J0, rdiag, fail, s_colbuf, r[0]);
       if (lane < nb) {
 #pragma unroll
         for (int c = 0; c < NB; ++c)
@@ -1740,7 +1745,7 @@ __global__ void __launch_bounds__(256, MINB) chol_logdet_tri_kernel(CholArgs a) 
       for (int c = 0; c < NB; ++c)
         r[c] = (lane < nb && c < nb) ? (c <= lane ? S[c * mp + lane] : 0.0) : (c == lane ? 1.0 : 0.0);
       int fail = -1;
-      diag_step<0, NB>(r, lane, nb, diagv + J0, rdiag, fail, s_colbuf);
+      diag_step<0, NB>(r, lane, nb, diagv + J0, rdiag, fail, s_colbuf, r[0]);
       if (lane < nb) {
 #pragma unroll
         for (int c = 0; c < NB; ++c)
