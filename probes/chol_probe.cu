@@ -5,7 +5,7 @@
 #include <vector>
 #include <cmath>
 #include <algorithm>
-__device__ long long g_stamps[64];
+__device__ long long g_stamps[128];
 __device__ unsigned long long g_tstart[4096], g_tend[4096];
 #include "../paper_2604_08812_b200/csrc/kernels.cuh"
 using namespace dsel;
@@ -40,10 +40,10 @@ int main(int argc, char** argv) {
   chol_logdet_kernel<PROBE_NB, PROBE_MINB><<<batch, 256, smem>>>(a);
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
-  long long stamps[64]; cudaMemcpyFromSymbol(stamps, g_stamps, sizeof(stamps));
+  long long stamps[128]; cudaMemcpyFromSymbol(stamps, g_stamps, sizeof(stamps));
   double g; cudaMemcpy(&g, gain, 8, cudaMemcpyDeviceToHost);
-  printf("nt %d batch %d: %.1f us  gain[0]=%.6f err=%s\n", nt, batch, ms * 1e3, g, cudaGetErrorString(cudaGetLastError()));
-  for (int i = 1; i < 64 && stamps[i]; ++i) printf("  stamp %2d: +%lld cycles\n", i, stamps[i] - stamps[i - 1]);
+  printf("nt %d batch %d: %.1f us  gain[0]=%.17g err=%s\n", nt, batch, ms * 1e3, g, cudaGetErrorString(cudaGetLastError()));
+  for (int i = 1; i < 128 && stamps[i]; ++i) printf("  stamp %2d: +%lld cycles\n", i, stamps[i] - stamps[i - 1]);
   std::vector<unsigned long long> ts(batch), te(batch);
   cudaMemcpyFromSymbol(ts.data(), g_tstart, batch * 8); cudaMemcpyFromSymbol(te.data(), g_tend, batch * 8);
   unsigned long long mn = ts[0], mx = te[0]; double avg = 0, mxd = 0;
