@@ -126,6 +126,37 @@ def test_random_cases(dsel, O, golden_dir):
         assert_trace_matches(rows, c["chosen"], c["gains"], c["objectives"])
 
 
+def test_selector_known_answers_on_gpu(dsel):
+    """The reference's analytic selector cases, through the CUDA engine.
+
+    diag(2,5,3), B=2 -> [1, 2] with gains log 5, log 3 (test_selector.cpp:94-101);
+    K = [[4,2],[2,5]]: first pick 1 (log 5), then the Schur gain of 0 given 1,
+    log(4 - 2*2/5) (the scalar Schur form of test_selector.cpp:48-62).
+    """
+    k = np.diag([2.0, 5.0, 3.0]).reshape(-1)
+    eng, rows, n = run_engine(dsel, k, 3, 1, 2)
+    eng.close()
+    assert_trace_matches(rows, [1, 2], [np.log(5.0), np.log(3.0)])
+    k = np.array([4.0, 2.0, 2.0, 5.0])
+    eng, rows, n = run_engine(dsel, k, 2, 1, 2)
+    eng.close()
+    assert_trace_matches(rows, [1, 0], [np.log(5.0), np.log(4.0 - 4.0 / 5.0)])
+
+
+def test_rescale_invariance_on_gpu(dsel, O):
+    """K -> 3.7 K: same sequence, gains + Nt*log 3.7 (test_selector.cpp:160-175)."""
+    nd, nt = 8, 3
+    k = O.random_hessian(nd, nt, 1.0, 24, 5)
+    ea, a, _ = run_engine(dsel, k, nd, nt, 5)
+    eb, b, _ = run_engine(dsel, k * 3.7, nd, nt, 5)
+    ea.close()
+    eb.close()
+    assert [r["chosen_index"] for r in a] == [r["chosen_index"] for r in b]
+    for ra, rb in zip(a, b):
+        want = ra["gain"] + nt * np.log(3.7)
+        assert abs(rb["gain"] - want) <= 1e-10 * max(abs(want), 1.0)
+
+
 def test_wave_benchmark_kbf(dsel, O, golden_dir):
     """The reference's standard wave benchmark K (assemble_k -> write_kbf);
     raw gains go negative here (step 8: -0.0994)."""
