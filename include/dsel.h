@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define DSEL_ABI_VERSION 1
+#define DSEL_ABI_VERSION 2
 
 typedef enum {
   DSEL_OK = 0,
@@ -62,7 +62,11 @@ typedef struct {
   int world_size;         /* ranks sharing the candidate set (1 = single GPU) */
   int rank;               /* 0..world_size-1 */
   const void* nccl_id;    /* 128-byte ncclUniqueId (dsel_nccl_unique_id) when world_size > 1 */
-  int storage;            /* dsel_storage; STREAM is reserved (returns E_INVALID) */
+  int storage;            /* dsel_storage: HBM = K resident on the devices; STREAM = K stays in
+                             host memory (pinned store, the caller's attached buffer or a KBF
+                             file) and each round copies the blocks it reads (left-looking,
+                             algorithm 1); AUTO = HBM when the plan fits hbm_budget, else
+                             STREAM (see dsel_get_plan) */
   int keep_pristine;      /* keep a device copy of K so dsel_reset can rerun */
   int export_factor;      /* keep per-step W rows so dsel_export_factor can rebuild L_S */
   double near_tie_tau;    /* near-tie flag threshold (default 1e-9 when 0) */
@@ -74,7 +78,30 @@ typedef struct {
                              1: left-looking W-resident variant:
                              K stays pristine, W_all = K[:,S] L_S^{-T} is kept, one
                              column c = K[:,k] - W_all W_all[k]^T per round. */
+  /* ---- ABI 2 ---- */
+  int panel_layout;       /* symmetric storage only: 0 (default) packed block-lower panels
+                             (each panel keeps the rows from its diagonal block down: half
+                             the HBM of the full square); 1 full-height panels */
+  uint64_t hbm_budget;    /* AUTO storage: device bytes the engine may use; 0 = the device's
+                             free memory at create minus 2 GiB */
+  int defer_connect;      /* world_size > 1: 1 = dsel_create only allocates; the caller
+                             checks that every rank created its engine, then calls
+                             dsel_connect (NCCL init + NVLink peer mappings). 0 = create
+                             connects (a rank that fails to create leaves its peers
+                             blocked in ncclCommInitRank). */
 } dsel_config;
+
+/* What dsel_create decided (AUTO resolved) and what it holds. */
+typedef struct {
+  int storage;            /* DSEL_STORAGE_HBM or DSEL_STORAGE_STREAM */
+  int algorithm;          /* 0 right-looking, 1 left-looking */
+  int symmetric;          /* block-lower (half-flop) update */
+  int packed;             /* packed block-lower panel store */
+  uint64_t device_bytes;  /* allocated on the device at create */
+  uint64_t planned_bytes; /* the create-time estimate AUTO compared with the budget */
+  uint64_t budget_bytes;  /* the budget it was compared with */
+  uint64_t host_store_bytes; /* pinned host store (STREAM) once K is loaded */
+} dsel_plan;
 
 /* One selection round; field names follow TraceRow (selector.hpp:40-49) and
  * RoundResult (parallel.hpp:30-35). Times are device milliseconds measured
@@ -97,6 +124,8 @@ typedef struct {
   double ms_update;       /* rank-nt Schur update (+ factor history) */
   double ms_round;        /* whole round on the device */
   double update_flops;    /* algorithmic flops of this rank's update: 2*nt*rows*cols */
+  double ms_io;           /* ABI 2: H2D of the round's streamed K blocks (copy stream;
+                             storage = STREAM, else 0) -- timing.csv io_ms */
 } dsel_step_info;
 
 /* Per-rank argmax record exchanged each round (32 bytes, allgathered): the
@@ -115,8 +144,22 @@ dsel_status dsel_create(const dsel_config* cfg, dsel_engine** out);
 void dsel_destroy(dsel_engine* e);
 const char* dsel_last_error(const dsel_engine* e); /* NULL engine -> last create error */
 dsel_status dsel_sync(dsel_engine* e);
+/* Collective half of create for defer_connect engines (no-op otherwise). */
+dsel_status dsel_connect(dsel_engine* e);
+/* Peer failure (WorkerFailure, parallel.hpp:469-475): callable from any
+ * thread while this engine's own thread is blocked in dsel_step. Aborts the
+ * NCCL communicator and releases the NVLink flag waits; the blocked call
+ * and every later step return DSEL_E_NCCL. The engine must still be
+ * destroyed. */
+dsel_status dsel_abort(dsel_engine* e);
 /* bytes of device memory the engine holds */
 uint64_t dsel_device_bytes(const dsel_engine* e);
+dsel_status dsel_get_plan(const dsel_engine* e, dsel_plan* out);
+/* Device/pinned allocations (cudaMalloc, cudaMallocHost, cudaHostRegister)
+ * made by the library since load, all engines: the zero-allocation contract
+ * of candidate evaluation (test_selector.cpp:281-298) is that
+ * dsel_step / dsel_run never move this counter. */
+uint64_t dsel_alloc_count(void);
 
 /* ---- panel store ingest (north-star (1)) -------------------------------- */
 /* Block row j of K: blocks (j, i), i = 0..n_sensors-1, each row-major Nt x Nt
@@ -125,7 +168,11 @@ uint64_t dsel_device_bytes(const dsel_engine* e);
  * candidate owned by this rank. Host memory may be pageable or pinned. */
 dsel_status dsel_load_block_row(dsel_engine* e, int j, const double* host_row);
 /* Block column j: blocks (i, j), i = 0..n_sensors-1, each row-major, stacked
- * (what read_test_column reads, kaccess.hpp:27-35). Exact for any K. */
+ * (what read_test_column reads, kaccess.hpp:27-35). Under symmetric storage
+ * (the default for even n_steps) only the blocks (i, j) with position(i) >=
+ * position(j) are kept and the rest of C is taken from them by symmetry, so
+ * K must be symmetric (as every reference KAccess is); full_square = 1 keeps
+ * every block and is exact for any K. */
 dsel_status dsel_load_block_col(dsel_engine* e, int j, const double* host_col);
 /* Whole K in DataSpaceHessian / KBF payload order (n_sensors^2 blocks,
  * block-row-major, hessian.hpp:17-84): loads every owned panel. */
@@ -241,6 +288,11 @@ dsel_status dsel_get_stats(dsel_engine* e, dsel_stats* st);
  * row stride `ld` (>= k*Nt), k = rounds done. Collective: every rank gets the
  * full factor. Requires export_factor. */
 dsel_status dsel_export_factor(dsel_engine* e, double* host, int64_t ld);
+/* Block row i (0-based) of L_S alone: n_steps x (i+1)*n_steps, row-major,
+ * row stride ld -- what append_block_column adds in round i+1
+ * (linalg.hpp:159-178). Collective like dsel_export_factor; lets a per-round
+ * hook rebuild the factor incrementally. */
+dsel_status dsel_export_factor_row(dsel_engine* e, int i, double* host, int64_t ld);
 
 #ifdef __cplusplus
 }

@@ -164,6 +164,49 @@ void orc_synthetic_materialize_rows(const double* v, int n_sensors, int n_steps,
                           n_steps);
 }
 
+/* The same K as orc_synthetic_materialize_rows, bit for bit, at golden-fixture
+ * scale (C3 75x420 rank 24576, C4s 600x64): every element is still the
+ * sequential sum over t of the rounded products a[t]*b[t] (kaccess.hpp:111,
+ * built with -ffp-contract=off so mul and add round separately), with sigma^2
+ * added last. Only the loop nest differs: the t loop is cut into chunks with
+ * the output block itself as the running accumulator, and the c loop is
+ * innermost over vt = V^T (rank x n), so the compiler vectorizes across
+ * independent elements. Blocks j <= i are computed; (j,i) is the exact
+ * transpose (a*b == b*a in IEEE, same summation order). Block row i of the
+ * output is written for j <= i and block column i above the diagonal, so
+ * threads owning distinct i never touch the same bytes. */
+void orc_synthetic_block_rows_fast(const double* v, const double* vt, int n_sensors,
+                                   int n_steps, int rank, double noise_sigma, int i,
+                                   double* k) {
+  const double noise2 = noise_sigma * noise_sigma;
+  const size_t n = (size_t)n_sensors * n_steps;
+  const size_t bsz = (size_t)n_steps * n_steps;
+  const int tc = 64;
+  for (int j = 0; j <= i; ++j) {
+    double* o = k + ((size_t)i * n_sensors + j) * bsz;
+    for (size_t e = 0; e < bsz; ++e) o[e] = 0.0;
+    for (int t0 = 0; t0 < rank; t0 += tc) {
+      const int t1 = t0 + tc < rank ? t0 + tc : rank;
+      for (int r = 0; r < n_steps; ++r) {
+        const double* a = v + ((size_t)i * n_steps + r) * rank;
+        double* orow = o + (size_t)r * n_steps;
+        for (int t = t0; t < t1; ++t) {
+          const double at = a[t];
+          const double* b = vt + (size_t)t * n + (size_t)j * n_steps;
+          for (int c = 0; c < n_steps; ++c) orow[c] += at * b[c];
+        }
+      }
+    }
+    if (i == j)
+      for (int r = 0; r < n_steps; ++r) o[(size_t)r * n_steps + r] += noise2;
+    if (j != i) {
+      double* m = k + ((size_t)j * n_sensors + i) * bsz;
+      for (int r = 0; r < n_steps; ++r)
+        for (int c = 0; c < n_steps; ++c) m[(size_t)c * n_steps + r] = o[(size_t)r * n_steps + c];
+    }
+  }
+}
+
 /* proj/tests/support/generators.hpp:19-40 random_hessian. */
 void orc_random_hessian(int n_sensors, int n_steps, double gamma, int rank, uint64_t seed,
                         double* k) {

@@ -52,6 +52,8 @@ def lib():
         L.orc_synthetic_v.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, _dp]
         L.orc_synthetic_materialize_rows.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_double,
                                                      C.c_int, C.c_int, _dp]
+        L.orc_synthetic_block_rows_fast.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_int,
+                                                    C.c_double, C.c_int, _dp]
         L.orc_random_hessian.argtypes = [C.c_int, C.c_int, C.c_double, C.c_int, C.c_uint64, _dp]
         L.orc_cholesky_in_place.argtypes = [_dp, C.c_int, C.c_int]
         L.orc_cholesky_in_place.restype = C.c_int
@@ -131,6 +133,26 @@ def synthetic_k(nd: int, nt: int, rank: int, sigma: float, seed: int,
     with cf.ThreadPoolExecutor(threads) as ex:
         list(ex.map(lambda i: L.orc_synthetic_materialize_rows(
             v, nd, nt, rank, sigma, int(bounds[i]), int(bounds[i + 1]), k), range(threads)))
+    return k
+
+
+def synthetic_k_fast(nd: int, nt: int, rank: int, sigma: float, seed: int,
+                     threads: int | None = None) -> np.ndarray:
+    """synthetic_k, bit for bit, by the blocked/vectorized loop nest
+    (orc_synthetic_block_rows_fast); for the large golden fixtures."""
+    import concurrent.futures as cf
+
+    v = synthetic_v(nd, nt, rank, seed)
+    vt = np.ascontiguousarray(v.T)
+    v = np.ascontiguousarray(v.reshape(-1))
+    vt = vt.reshape(-1)
+    k = np.empty(nd * nd * nt * nt, dtype=np.float64)
+    threads = threads or os.cpu_count() or 1
+    L = lib()
+    # heavy rows (large i) first so the pool drains evenly
+    with cf.ThreadPoolExecutor(threads) as ex:
+        list(ex.map(lambda i: L.orc_synthetic_block_rows_fast(v, vt, nd, nt, rank, sigma, i, k),
+                    range(nd - 1, -1, -1)))
     return k
 
 

@@ -8,8 +8,8 @@ from .selector import (CorruptFile, DselError, Engine, IoError, GpuOptions, Inde
                        LtiProblem,
                        InfeasibleRound, InvalidConfig, ParallelRunReport, SelectionState,
                        SelectionTrace, TraceRow, WorkerFailure, gpu_greedy_select,
-                       fold_records, nccl_unique_id, synthetic_v)
+                       alloc_count, fold_records, nccl_unique_id, synthetic_v)
 
-__all__ = ["Engine", "LtiProblem", "GpuOptions", "gpu_greedy_select", "synthetic_v", "nccl_unique_id", "fold_records",
+__all__ = ["Engine", "LtiProblem", "GpuOptions", "gpu_greedy_select", "synthetic_v", "nccl_unique_id", "fold_records", "alloc_count",
            "DselError", "IoError", "CorruptFile", "InvalidConfig", "IndexOutOfRange", "InfeasibleRound", "WorkerFailure",
            "SelectionState", "SelectionTrace", "ParallelRunReport", "TraceRow", "LIB_PATH"]

@@ -18,11 +18,12 @@ STATUS_NAMES = {0: "DSEL_OK", 1: "DSEL_E_INVALID", 2: "DSEL_E_RANGE", 3: "DSEL_E
 
 # every entry point declared in include/dsel.h (tests check the exports)
 EXPORTS = ["dsel_abi_version", "dsel_fold_records", "dsel_nccl_unique_id", "dsel_create", "dsel_destroy",
-           "dsel_last_error", "dsel_sync", "dsel_device_bytes", "dsel_load_block_row",
+           "dsel_last_error", "dsel_sync", "dsel_connect", "dsel_abort", "dsel_device_bytes", "dsel_get_plan", "dsel_alloc_count", "dsel_load_block_row",
            "dsel_load_block_col", "dsel_load_k", "dsel_attach_host_k", "dsel_attach_host_rows", "dsel_load_kbf", "dsel_read_block_row", "dsel_synthetic_v",
            "dsel_gen_synthetic", "dsel_gen_synthetic_device", "dsel_lti_from_config", "dsel_lti_free",
            "dsel_assemble_lti", "dsel_step", "dsel_step_forced", "dsel_run", "dsel_peek_gains",
-           "dsel_get_trace", "dsel_reset", "dsel_get_stats", "dsel_export_factor"]
+           "dsel_get_trace", "dsel_reset", "dsel_get_stats", "dsel_export_factor",
+           "dsel_export_factor_row"]
 
 
 class DselConfig(C.Structure):
@@ -31,7 +32,18 @@ class DselConfig(C.Structure):
                 ("device", C.c_int), ("world_size", C.c_int), ("rank", C.c_int),
                 ("nccl_id", C.c_void_p), ("storage", C.c_int), ("keep_pristine", C.c_int),
                 ("export_factor", C.c_int), ("near_tie_tau", C.c_double),
-                ("full_square", C.c_int), ("algorithm", C.c_int)]
+                ("full_square", C.c_int), ("algorithm", C.c_int),
+                ("panel_layout", C.c_int), ("hbm_budget", C.c_uint64),
+                ("defer_connect", C.c_int)]
+
+
+class DselPlan(C.Structure):
+    _fields_ = [("storage", C.c_int), ("algorithm", C.c_int), ("symmetric", C.c_int),
+                ("packed", C.c_int), ("device_bytes", C.c_uint64), ("planned_bytes", C.c_uint64),
+                ("budget_bytes", C.c_uint64), ("host_store_bytes", C.c_uint64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
 
 
 class DselStepInfo(C.Structure):
@@ -42,7 +54,7 @@ class DselStepInfo(C.Structure):
                 ("bytes_exchanged", C.c_uint64), ("ms_gain", C.c_double),
                 ("ms_exchange", C.c_double), ("ms_panel", C.c_double),
                 ("ms_update", C.c_double), ("ms_round", C.c_double),
-                ("update_flops", C.c_double)]
+                ("update_flops", C.c_double), ("ms_io", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -85,8 +97,13 @@ def _load():
     L.dsel_last_error.argtypes = [vp]
     L.dsel_last_error.restype = C.c_char_p
     L.dsel_sync.argtypes = [vp]
+    L.dsel_connect.argtypes = [vp]
+    L.dsel_abort.argtypes = [vp]
     L.dsel_device_bytes.argtypes = [vp]
     L.dsel_device_bytes.restype = C.c_uint64
+    L.dsel_get_plan.argtypes = [vp, C.POINTER(DselPlan)]
+    L.dsel_alloc_count.argtypes = []
+    L.dsel_alloc_count.restype = C.c_uint64
     L.dsel_load_block_row.argtypes = [vp, C.c_int, vp]
     L.dsel_load_block_col.argtypes = [vp, C.c_int, vp]
     L.dsel_load_k.argtypes = [vp, vp]
@@ -109,11 +126,13 @@ def _load():
     L.dsel_get_trace.restype = C.c_int
     L.dsel_reset.argtypes = [vp]
     L.dsel_export_factor.argtypes = [vp, vp, C.c_int64]
+    L.dsel_export_factor_row.argtypes = [vp, C.c_int, vp, C.c_int64]
     L.dsel_get_stats.argtypes = [vp, C.POINTER(DselStats)]
     L.dsel_fold_records.argtypes = [C.POINTER(DselArgRec), C.c_int, C.POINTER(DselArgRec)]
     L.dsel_fold_records.restype = None
     for name in EXPORTS:
         if name not in ("dsel_destroy", "dsel_last_error", "dsel_device_bytes", "dsel_fold_records",
+                        "dsel_alloc_count",
                         "dsel_lti_free",
                         "dsel_get_trace", "dsel_abi_version"):
             getattr(L, name).restype = C.c_int

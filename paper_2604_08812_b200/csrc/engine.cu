@@ -20,6 +20,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cerrno>
 #include <thread>
@@ -59,6 +60,30 @@ struct Fail {
   } while (0)
 
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// Every device / pinned allocation of the library goes through these three
+// (counted): the zero-allocation contract of candidate evaluation
+// (test_selector.cpp:281-298) is asserted on dsel_alloc_count().
+std::atomic<uint64_t> g_allocs{0};
+template <class T>
+cudaError_t ds_malloc(T** p, size_t bytes) {
+  g_allocs.fetch_add(1, std::memory_order_relaxed);
+  return cudaMalloc(reinterpret_cast<void**>(p), bytes);
+}
+template <class T>
+cudaError_t ds_malloc_host(T** p, size_t bytes) {
+  g_allocs.fetch_add(1, std::memory_order_relaxed);
+  return cudaMallocHost(reinterpret_cast<void**>(p), bytes);
+}
+template <class T>
+cudaError_t ds_host_alloc_mapped(T** p, size_t bytes) {
+  g_allocs.fetch_add(1, std::memory_order_relaxed);
+  return cudaHostAlloc(reinterpret_cast<void**>(p), bytes, cudaHostAllocMapped);
+}
+cudaError_t ds_host_register(void* p, size_t bytes, unsigned flags) {
+  g_allocs.fetch_add(1, std::memory_order_relaxed);
+  return cudaHostRegister(p, bytes, flags);
+}
 constexpr int kWsGroupDefault = 16;  // column tiles per update rasterization group
 
 // scratch device allocation released on every exit path (including throws)
@@ -66,7 +91,7 @@ template <class T>
 struct DevScratch {
   T* p = nullptr;
   explicit DevScratch(size_t count) {
-    if (cudaMalloc(&p, sizeof(T) * (count ? count : 1)) != cudaSuccess) {
+    if (ds_malloc(&p, sizeof(T) * (count ? count : 1)) != cudaSuccess) {
       cudaGetLastError();
       p = nullptr;
       throw Fail{DSEL_E_OOM, "cudaMalloc of scratch (" + std::to_string(count * sizeof(T)) + " bytes) failed"};
@@ -117,7 +142,7 @@ template <class T>
 T* dmalloc(size_t count, uint64_t& total) {
   void* p = nullptr;
   if (count == 0) count = 1;
-  cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+  cudaError_t e = ds_malloc(&p, count * sizeof(T));
   if (e != cudaSuccess) {
     cudaGetLastError();
     throw Fail{DSEL_E_OOM, "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed"};
@@ -161,6 +186,18 @@ struct dsel_engine {
   int own_mpad = 0, k_mpad = 0;
   long long ldo = 0;
   bool sym = true;  // block-lower-triangle (symmetric) update
+  // packed block-lower panel store (symmetric storage): each panel keeps only
+  // the rows from its own diagonal block down (PanelGeom), half the HBM of the
+  // full square; C = Craw + c_pad (the pad keeps masked reads of rows above a
+  // panel's first stored row inside the allocation)
+  bool packed = false;
+  uint64_t planned = 0, plan_budget = 0;  // create-time plan (dsel_get_plan)
+  unsigned char nccl_id[128] = {};
+  int* h_abort = nullptr;          // host-mapped peer-failure word (dsel_abort)
+  const volatile int* d_abort = nullptr;
+  std::atomic<bool> aborted{false};
+  double* Craw = nullptr;
+  size_t c_elems = 0, c_pad = 0;
   bool full_panels = true;  // both triangles of every panel hold K (gen_synthetic / full-square load)
   int* d_sym = nullptr;  // [first_rt per column tile | group prefix]
   int* h_sym = nullptr;  // pinned
@@ -232,6 +269,16 @@ struct dsel_engine {
   bool finished = false;
   std::string err;
 
+  PanelGeom geom() const {
+    PanelGeom g;
+    g.base = C;
+    g.n = n;
+    g.nt = nt;
+    g.G = G;
+    g.rank = rank;
+    g.packed = packed ? 1 : 0;
+    return g;
+  }
   int* row_pos() { return d_tab; }
   int* col_slot() { return d_tab + nc; }
   int* col_g() { return d_tab + nc + nloc; }
@@ -270,15 +317,21 @@ void upload_round(dsel_engine* e) {
 
 // Kernel-side helpers for the gain kernel batch description.
 namespace {
-__global__ void gain_tables_kernel(const int* col_slot, int n, int G, int rank, int nt,
-                                   const int* pos_sensor, int* src_col, int* src_row,
+__global__ void gain_tables_kernel(const int* col_slot, int n, PanelGeom geom,
+                                   const int* pos_sensor, long long* src_off, long long* src_ld,
                                    int* sensor, int diag_store) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= n) return;
   const int q = col_slot[b];
-  const int p = q * G + rank;
-  src_col[b] = q * nt;
-  src_row[b] = diag_store ? 0 : p * nt;  // left-looking: separate D blocks, ld = nt
+  const int nt = geom.nt;
+  const int p = q * geom.G + geom.rank;
+  if (diag_store) {  // left-looking: separate D blocks, ld = nt
+    src_off[b] = (long long)q * nt * nt;
+    src_ld[b] = nt;
+  } else {  // the diagonal block of panel q
+    src_off[b] = geom.idx(q, 0, (long long)p * nt);
+    src_ld[b] = geom.ld(q);
+  }
   sensor[b] = pos_sensor[p];
 }
 
@@ -357,10 +410,10 @@ __global__ void pack_factor_row_kernel(const double* hist_slot, int nt, int i_bl
 
 namespace {
 
-// scratch int tables for the gain kernel batch: [src_col | src_row | sensor]
+// scratch tables for the gain kernel batch: [src_off | src_ld | sensor]
 struct GainTabs {
-  int* src_col;
-  int* src_row;
+  long long* src_off;
+  long long* src_ld;
   int* sensor;
 };
 
@@ -398,22 +451,20 @@ void launch_chol(const CholArgs& a, int n_batch, cudaStream_t s, int n_sms) {
 }
 
 GainTabs gain_tabs(dsel_engine* e) {
-  int* base = reinterpret_cast<int*>(e->xbuf);
-  return {base, base + e->nloc + 1, base + 2 * (e->nloc + 1)};
+  long long* base = reinterpret_cast<long long*>(e->xbuf);  // 3*(nloc+1) doubles
+  return {base, base + e->nloc + 1, reinterpret_cast<int*>(base + 2 * (e->nloc + 1))};
 }
 
 void run_gain(dsel_engine* e, const int* slots, int n_batch, ArgRec* rec = nullptr) {
   if (n_batch <= 0) return;
   GainTabs t = gain_tabs(e);
   gain_tables_kernel<<<(n_batch + 127) / 128, 128, 0, e->s>>>(
-      slots, n_batch, e->G, e->rank, e->nt, e->d_pos_sensor, t.src_col, t.src_row, t.sensor,
-      e->ll ? 1 : 0);
+      slots, n_batch, e->geom(), e->d_pos_sensor, t.src_off, t.src_ld, t.sensor, e->ll ? 1 : 0);
   CU(cudaGetLastError());
   CholArgs a{};
   a.src = e->ll ? e->D : e->C;
-  a.lds = e->ll ? (long long)e->nt : e->n;
-  a.src_col = t.src_col;
-  a.src_row = t.src_row;
+  a.src_off = t.src_off;
+  a.src_ld = t.src_ld;
   a.L = e->Lscr;
   a.l_stride = (long long)e->nt * e->nt;
   a.gain = e->gains;
@@ -505,10 +556,10 @@ struct PeerInfo {
 
 void setup_p2p(dsel_engine* e) {
   const int G = e->G;
-  CU(cudaMalloc(&e->flag, 256));
+  CU(ds_malloc(&e->flag, 256));
   CU(cudaMemset(e->flag, 0, 256));
   // buffer 4 (the panel shard) is absent with a streaming store: not mapped
-  void* bufs[kPeerBufs] = {e->Wsend ? (void*)e->Wsend : (void*)e->Wkn, e->Lscr, e->flag, e->Lk, e->C};
+  void* bufs[kPeerBufs] = {e->Wsend ? (void*)e->Wsend : (void*)e->Wkn, e->Lscr, e->flag, e->Lk, e->Craw};
   PeerInfo mine{};
   mine.pid = (long long)getpid();
   mine.dev = e->dev;
@@ -581,10 +632,10 @@ void setup_p2p(dsel_engine* e) {
     e->peer_lscr[r] = static_cast<double*>(peer[1][r]);
     e->peer_flag[r] = static_cast<unsigned long long*>(peer[2][r]);
     e->peer_lk[r] = static_cast<double*>(peer[3][r]);
-    e->peer_c[r] = static_cast<double*>(peer[4][r]);
+    e->peer_c[r] = peer[4][r] ? static_cast<double*>(peer[4][r]) + e->c_pad : nullptr;
   }
-  CU(cudaMalloc(&e->d_peer_wsend, sizeof(double*) * G));
-  CU(cudaMalloc(&e->d_peer_flag, sizeof(unsigned long long*) * G));
+  CU(ds_malloc(&e->d_peer_wsend, sizeof(double*) * G));
+  CU(ds_malloc(&e->d_peer_flag, sizeof(unsigned long long*) * G));
   CU(cudaMemcpy(e->d_peer_wsend, e->peer_wsend.data(), sizeof(double*) * G, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(e->d_peer_flag, e->peer_flag.data(), sizeof(unsigned long long*) * G,
                 cudaMemcpyHostToDevice));
@@ -760,7 +811,7 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
       p2p_signal_kernel<<<1, 32, 0, e->s>>>(e->flag, e->seq);
       CU(cudaGetLastError());
     } else {
-      p2p_wait_kernel<<<1, 32, 0, e->s>>>(e->peer_flag[owner], e->seq);
+      p2p_wait_kernel<<<1, 32, 0, e->s>>>(e->peer_flag[owner], e->seq, e->d_abort);
       CU(cudaGetLastError());
       if (kcols > 0)
         CU(cudaMemcpyAsync(e->Wkn, e->peer_wsend[owner], sizeof(double) * (size_t)kcols * e->k_mpad,
@@ -814,7 +865,7 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
       // start from K(own, k) (the pristine panels), output to cbuf
       UpdateWSArgs ua{};
       ua.C = e->stream ? nullptr : e->C;  // streaming: accumulate from 0, K added below
-      ua.ldc = e->n;
+      ua.geom = e->geom();
       ua.Wt = e->Wkn;
       ua.Wnt = e->Wown;
       ua.mpad = e->k_mpad;
@@ -941,8 +992,10 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
 }
 
 void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
+  if (e->aborted.load()) throw Fail{DSEL_E_NCCL, "aborted: a peer rank failed (dsel_abort)"};
   if (e->finished || (int)e->chosen.size() >= e->eff_budget)
     throw Fail{DSEL_E_STATE, "selection already finished"};
+  if (e->G > 1 && !e->comm) throw Fail{DSEL_E_STATE, "world_size > 1: dsel_connect first"};
   CU(cudaSetDevice(e->dev));
   const int round = (int)e->chosen.size();
   const int nt = e->nt;
@@ -994,6 +1047,14 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   CU(cudaEventRecord(ev[2], e->s));
   e->d2h_bytes += sizeof(ArgRec) * (uint64_t)e->G;
   CU(cudaStreamSynchronize(e->s));
+  if (e->aborted.load()) throw Fail{DSEL_E_NCCL, "aborted: a peer rank failed (dsel_abort)"};
+  // fault injection for the peer-failure tests: DSEL_FAULT="round,rank" fails
+  // that rank after the round's argmax exchange (its peers then wait on it)
+  if (const char* fault = getenv("DSEL_FAULT")) {
+    int fr = 0, fk = -1;
+    if (std::sscanf(fault, "%d,%d", &fr, &fk) == 2 && fr == round + 1 && fk == e->rank)
+      throw Fail{DSEL_E_CUDA, "injected fault (DSEL_FAULT) in round " + std::to_string(fr)};
+  }
   // identical fold on every rank (reduce_argmax, parallel.hpp:61-74, top-2)
   dsel_argrec fold{};
   dsel_fold_records(e->h_recs, e->G, &fold);
@@ -1129,7 +1190,7 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
     if (n_gather > 0) {  // every listed block is held by this rank
       const int tpb = (nt + 31) / 32;
       gather_panel_sym_tiled_kernel<<<(unsigned)((long long)n_gather * tpb * tpb), 256, 0, e->s>>>(
-          e->C, e->n, nt, gpos, p, e->G, e->Pbuf);
+          e->geom(), gpos, p, e->Pbuf);
       CU(cudaGetLastError());
       e->launches += 1;
     }
@@ -1149,8 +1210,15 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       PanelArgs pa{};
       pa.P = P;
       pa.ldp = e->n;
-      pa.P2 = (owner == e->rank ? e->C : e->p2p ? e->peer_c[owner] : nullptr);
-      if (pa.P2) pa.P2 += (size_t)q * nt * e->n;
+      // the owner's panel k (its geometry: rank = owner)
+      PanelGeom og = e->geom();
+      og.base = owner == e->rank ? e->C : e->p2p ? e->peer_c[owner] : nullptr;
+      og.rank = owner;
+      if (og.base) {
+        pa.P2 = og.panel(q);
+        pa.ldp2 = og.ld(q);
+        pa.p2_row0 = og.start(q);
+      }
       pa.pk = p;
       pa.Linv = e->Linv;
       pa.ldl = e->ldw;
@@ -1180,7 +1248,7 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
                               256, 0, e->s>>>(
           e->d_peer_wsend, e->d_peer_flag, e->seq, e->G, e->d_hboff, e->ldw, e->d_hb, e->row_pos(), R, nt,
           e->Wt, e->Wnt, e->mpad, e->export_factor ? e->hist : nullptr, (long long)e->eff_budget * nt * nt,
-          (long long)round * nt * nt, e->rank);
+          (long long)round * nt * nt, e->rank, e->d_abort);
       CU(cudaGetLastError());
       e->launches += 2;
       for (int r = 0; r < e->G; ++r)
@@ -1212,7 +1280,10 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       pa.P = P;
       pa.ldp = e->n;
       if (e->sym) {  // G == 1: this rank owns panel k
-        pa.P2 = e->C + (size_t)q * nt * e->n;
+        const PanelGeom g = e->geom();
+        pa.P2 = g.panel(q);
+        pa.ldp2 = g.ld(q);
+        pa.p2_row0 = g.start(q);
         pa.pk = p;
       }
       pa.Linv = e->Linv;
@@ -1258,7 +1329,7 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
     if (nt % 2 == 0) {
       UpdateWSArgs ua{};
       ua.C = e->C;
-      ua.ldc = e->n;
+      ua.geom = e->geom();
       ua.Wt = e->Wt;
       ua.Wnt = e->Wnt;
       ua.mpad = e->mpad;
@@ -1354,7 +1425,7 @@ void destroy_impl(dsel_engine* e) {
   if (e->s) cudaStreamSynchronize(e->s);
   if (e->cs) cudaStreamSynchronize(e->cs);
   for (auto ev : e->ev) cudaEventDestroy(ev);
-  double* dptr[] = {e->cpart, e->Wown, e->Wkn, e->D, e->cbuf, e->ldiag, e->C, e->K0, e->W, e->Wn, e->Wt, e->Wnt, e->Pbuf, e->Lk, e->Linv, e->Lscr, e->gains, e->hist,
+  double* dptr[] = {e->cpart, e->Wown, e->Wkn, e->D, e->cbuf, e->ldiag, e->Craw, e->K0, e->W, e->Wn, e->Wt, e->Wnt, e->Pbuf, e->Lk, e->Linv, e->Lscr, e->gains, e->hist,
                     e->kgain, e->stage, e->xbuf};
   for (double* d : dptr)
     if (d) cudaFree(d);
@@ -1379,7 +1450,8 @@ void destroy_impl(dsel_engine* e) {
   if (e->Kk) cudaFree(e->Kk);
   if (e->ev_tab) cudaEventDestroy(e->ev_tab);
   if (e->h_stage) cudaFreeHost(e->h_stage);
-  if (e->comm) ncclCommDestroy(e->comm);
+  if (e->comm && !e->aborted.load()) ncclCommDestroy(e->comm);
+  if (e->h_abort) cudaFreeHost(e->h_abort);
   for (int b = 0; b < 2; ++b) {
     if (e->ev_copy[b]) cudaEventDestroy(e->ev_copy[b]);
     if (e->ev_scat[b]) cudaEventDestroy(e->ev_scat[b]);
@@ -1395,6 +1467,90 @@ void destroy_impl(dsel_engine* e) {
   delete e;
 }
 
+// per-round table block: [row/col tables | block-lower tile schedule | W holder lists]
+size_t round_ints(const dsel_engine* e, size_t* tab = nullptr, size_t* sym = nullptr, size_t* hb = nullptr) {
+  size_t n_tab = ((size_t)e->nc + 2 * e->nloc + 1 + 3) / 4 * 4, n_sym = 0, n_hb = 0;
+  if (e->sym) {
+    const size_t nct = (size_t)(e->nloc * e->nt + ws::BC - 1) / ws::BC + 2;
+    n_sym = (nct + nct / e->ws_group + 4 + 3) / 4 * 4;
+    if (e->G > 1) n_hb = 2 * (size_t)e->nc + e->G + 1;
+  }
+  if (tab) *tab = n_tab;
+  if (sym) *sym = n_sym;
+  if (hb) *hb = n_hb;
+  return n_tab + n_sym + n_hb;
+}
+
+// Storage plan: algorithm, residency and panel layout, and everything sized
+// from them (create_impl allocates exactly what plan_bytes counts).
+void apply_plan(dsel_engine* e, const dsel_config* cfg, bool ll, bool stream) {
+  e->ll = ll;
+  e->stream = stream;
+  e->keep = cfg->keep_pristine != 0 && !ll;
+  e->sym = cfg->full_square == 0 && e->nt % 2 == 0 && !ll;
+  e->packed = e->sym && cfg->panel_layout == 0;
+  e->full_panels = !e->packed;
+  e->c_elems = (size_t)e->geom().total(e->nloc);
+  e->c_pad = e->packed ? (size_t)e->n : 0;
+  e->mpad = round_up((int)e->n, ws::BR);
+}
+
+uint64_t plan_bytes(const dsel_engine* e, const dsel_config* cfg) {
+  uint64_t b = 0;
+  auto add = [&](uint64_t count, uint64_t size) { b += std::max<uint64_t>(count, 1) * size; };
+  const uint64_t nt = e->nt, n = (uint64_t)e->n, ldw = e->ldw, nloc1 = std::max(e->nloc, 1);
+  const uint64_t B = std::max(e->eff_budget, 1);
+  if (!e->stream) add(e->c_pad + e->c_elems, 8);
+  if (e->keep) add(e->c_elems, 8);
+  if (nt % 2 && !e->ll) add(n * ldw, 8);
+  if (!e->ll) {
+    if (nt % 2 == 0) {
+      add((uint64_t)e->mpad * ldw, 8);
+      add((uint64_t)e->mpad * ldw, 8);
+    } else {
+      add(n * ldw, 8);
+    }
+  }
+  if ((e->G > 1 || e->sym) && !e->ll) add(n * nt, 8);
+  if (e->ll) {
+    const uint64_t own_mpad = round_up((int)(nloc1 * nt), 128), k_mpad = round_up(e->nt, ws::BR);
+    const uint64_t ldo = nloc1 * nt;
+    add(own_mpad * B * ldw, 8);
+    add(k_mpad * B * ldw, 8);
+    add(nloc1 * nt * nt, 8);
+    add(ldo * nt, 8);
+    const int max_nk = (int)(B * ldw / 16);
+    const int ns = std::max(1, std::min(kLLMaxSplits, (max_nk + kLLSplitChunks - 1) / kLLSplitChunks));
+    const int np = nt % 2 ? ns : kLLMaxSplits;
+    if (np > 1) add((uint64_t)np * ldo * nt, 8);
+    add(B * nt * nt, 8);
+    add(nloc1, 4);
+  }
+  add(round_ints(e), 4);
+  if (e->sym && e->G > 1) {
+    add(n * ldw, 8);
+    add(n * ldw, 8);
+  }
+  add(nt * nt, 8);
+  add(ldw * ldw, 8);
+  add(nloc1 * nt * nt, 8);
+  add(e->nloc + 1, 8);
+  add(e->nloc + 1, 4);
+  add(1, 8);
+  add(1, 4);
+  add(3 * (uint64_t)(e->nloc + 1), 8);
+  if (cfg->export_factor && !e->ll) add(nloc1 * B * nt * nt, 8);
+  add(e->nc, 4);
+  add(e->nloc + 1, 4);
+  add(1, sizeof(ArgRec));
+  add(1, 4);
+  add(e->G, sizeof(ArgRec));
+  if (e->stream) add(nloc1 * nt * nt, 8);
+  return b;
+}
+
+void connect_impl(dsel_engine* e);
+
 void create_impl(const dsel_config* cfg, dsel_engine** out) {
   if (!cfg || !out) throw Fail{DSEL_E_INVALID, "null argument"};
   if (cfg->n_sensors < 1 || cfg->n_steps < 1) throw Fail{DSEL_E_INVALID, "n_sensors and n_steps must be >= 1"};
@@ -1405,6 +1561,7 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     throw Fail{DSEL_E_INVALID, "storage=stream streams one K column per round and needs the "
                                "left-looking W-resident algorithm (algorithm = 1, SURVEY 7.3-4)"};
   if (cfg->n_steps > 1024) throw Fail{DSEL_E_INVALID, "n_steps > 1024 is not supported by the gain kernel"};
+  if (cfg->algorithm < 0 || cfg->algorithm > 1) throw Fail{DSEL_E_INVALID, "unknown algorithm"};
   auto* e = new dsel_engine();
   try {
     e->nd = cfg->n_sensors;
@@ -1413,7 +1570,6 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     e->G = cfg->world_size;
     e->rank = cfg->rank;
     e->dev = cfg->device;
-    e->keep = cfg->keep_pristine != 0 && cfg->algorithm != 1;
     e->export_factor = cfg->export_factor != 0;
     e->tau = cfg->near_tie_tau > 0 ? cfg->near_tie_tau : 1e-9;
     // candidates (selector.hpp:142-151 check_candidates semantics)
@@ -1460,11 +1616,37 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
       CU(cudaEventCreateWithFlags(&e->ev_copy[b], cudaEventDisableTiming));
       CU(cudaEventCreateWithFlags(&e->ev_scat[b], cudaEventDisableTiming));
     }
+    if (const char* wc = getenv("DSEL_WS_CFG")) e->ws_cfg = std::max(-1, std::min(2, atoi(wc)));
+    e->ws_br = e->ws_cfg == 1 ? 64 : 128;
+    if (const char* wg = getenv("DSEL_WS_GROUP")) e->ws_group = std::max(1, atoi(wg));
+    // the storage plan decides every allocation below. AUTO: K resident in
+    // HBM with the requested algorithm when that fits the budget, else the
+    // streaming store (left-looking, K in host memory, north star (1))
+    {
+      size_t free_b = 0, total_b = 0;
+      CU(cudaMemGetInfo(&free_b, &total_b));
+      const uint64_t reserve = 2ull << 30;
+      e->plan_budget = cfg->hbm_budget ? cfg->hbm_budget : (free_b > reserve ? free_b - reserve : 0);
+      const bool want_ll = cfg->algorithm == 1;
+      apply_plan(e, cfg, want_ll, cfg->storage == DSEL_STORAGE_STREAM);
+      e->planned = plan_bytes(e, cfg);
+      if (cfg->storage == DSEL_STORAGE_AUTO && e->planned > e->plan_budget) {
+        apply_plan(e, cfg, true, true);
+        e->planned = plan_bytes(e, cfg);
+        if (e->planned > e->plan_budget)
+          throw Fail{DSEL_E_OOM, "storage=auto: even the streaming store needs " +
+                                     std::to_string(e->planned) + " device bytes > budget " +
+                                     std::to_string(e->plan_budget)};
+      }
+    }
     uint64_t& tot = e->dev_bytes;
-    const size_t shard = (size_t)e->n * (size_t)e->nloc * e->nt;
-    if (!e->stream) e->C = dmalloc<double>(shard, tot);
+    const size_t shard = e->c_elems;
+    if (!e->stream) {
+      e->Craw = dmalloc<double>(e->c_pad + shard, tot);
+      e->C = e->Craw + e->c_pad;
+    }
     if (e->keep) e->K0 = dmalloc<double>(shard, tot);
-    if (e->nt % 2) e->W = dmalloc<double>((size_t)e->n * e->ldw, tot);  // odd-nt update path
+    if (e->nt % 2 && !e->ll) e->W = dmalloc<double>((size_t)e->n * e->ldw, tot);  // odd-nt update path
     e->mpad = round_up((int)e->n, ws::BR);
     if (e->ll) {
       // left-looking: no resident conditional covariance, no right-looking W
@@ -1474,13 +1656,6 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     } else {
       e->Wn = dmalloc<double>((size_t)e->n * e->ldw, tot);
     }
-    e->ll = cfg->algorithm == 1;
-    e->stream = cfg->storage == DSEL_STORAGE_STREAM;
-    if (cfg->algorithm < 0 || cfg->algorithm > 1) throw Fail{DSEL_E_INVALID, "unknown algorithm"};
-    e->sym = cfg->full_square == 0 && e->nt % 2 == 0 && !e->ll;
-    if (const char* wc = getenv("DSEL_WS_CFG")) e->ws_cfg = std::max(-1, std::min(2, atoi(wc)));
-    e->ws_br = e->ws_cfg == 1 ? 64 : 128;
-    if (const char* wg = getenv("DSEL_WS_GROUP")) e->ws_group = std::max(1, atoi(wg));
     if ((e->G > 1 || e->sym) && !e->ll) e->Pbuf = dmalloc<double>((size_t)e->n * e->nt, tot);
     if (e->ll) {
       const int B = std::max(e->eff_budget, 1);
@@ -1509,19 +1684,14 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     // per-round host tables, one pinned staging block and one device block so a
     // round uploads them with a single copy: [row/col tables | block-lower tile
     // schedule | W holder lists (symmetric, G > 1)]
-    size_t n_tab = ((size_t)e->nc + 2 * e->nloc + 1 + 3) / 4 * 4, n_sym = 0, n_hb = 0;
-    if (e->sym) {
-      const size_t nct = (size_t)(e->nloc * e->nt + ws::BC - 1) / ws::BC + 2;
-      n_sym = (nct + nct / e->ws_group + 4 + 3) / 4 * 4;
-      if (e->G > 1) {
-        e->Wsend = dmalloc<double>((size_t)e->n * e->ldw, tot);
-        e->Wrecv = dmalloc<double>((size_t)e->n * e->ldw, tot);
-        n_hb = 2 * (size_t)e->nc + e->G + 1;
-      }
+    size_t n_tab, n_sym, n_hb;
+    e->round_ints = round_ints(e, &n_tab, &n_sym, &n_hb);
+    if (e->sym && e->G > 1) {
+      e->Wsend = dmalloc<double>((size_t)e->n * e->ldw, tot);
+      e->Wrecv = dmalloc<double>((size_t)e->n * e->ldw, tot);
     }
-    e->round_ints = n_tab + n_sym + n_hb;
     e->d_round = dmalloc<int>(e->round_ints, tot);
-    CU(cudaMallocHost(&e->h_round, sizeof(int) * e->round_ints));
+    CU(ds_malloc_host(&e->h_round, sizeof(int) * e->round_ints));
     e->d_tab = e->d_round;
     e->h_tab = e->h_round;
     if (n_sym) {
@@ -1551,14 +1721,14 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     e->d_counter = reinterpret_cast<unsigned*>(dmalloc<int>(1, tot));
     CU(cudaMemsetAsync(e->d_counter, 0, sizeof(unsigned), e->s));
     e->d_recs = dmalloc<ArgRec>(e->G, tot);
-    CU(cudaMallocHost(&e->h_recs, sizeof(ArgRec) * e->G));
+    CU(ds_malloc_host(&e->h_recs, sizeof(ArgRec) * e->G));
     if (e->W) CU(cudaMemsetAsync(e->W, 0, sizeof(double) * (size_t)e->n * e->ldw, e->s));
     if (e->Wn) CU(cudaMemsetAsync(e->Wn, 0, sizeof(double) * (size_t)e->n * e->ldw, e->s));
     if (e->Wt) {
       CU(cudaMemsetAsync(e->Wt, 0, sizeof(double) * (size_t)e->mpad * e->ldw, e->s));
       CU(cudaMemsetAsync(e->Wnt, 0, sizeof(double) * (size_t)e->mpad * e->ldw, e->s));
     }
-    if (e->C) CU(cudaMemsetAsync(e->C, 0, sizeof(double) * shard, e->s));
+    if (e->Craw) CU(cudaMemsetAsync(e->Craw, 0, sizeof(double) * (e->c_pad + shard), e->s));
     if (e->stream) {
       e->Kk = dmalloc<double>((size_t)std::max(e->nloc, 1) * e->nt * e->nt, tot);
       CU(cudaEventCreateWithFlags(&e->ev_tab, cudaEventDisableTiming));
@@ -1570,30 +1740,51 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
                          cudaMemcpyHostToDevice, e->s));
     e->ev.resize((size_t)std::max(e->eff_budget, 1) * kEv);
     for (auto& x : e->ev) CU(cudaEventCreate(&x));
+    // peer-failure word (host-mapped pinned): dsel_abort sets it, the
+    // NVLink flag waits poll it
+    CU(ds_host_alloc_mapped(&e->h_abort, sizeof(int)));
+    *e->h_abort = 0;
+    {
+      void* dp = nullptr;
+      CU(cudaHostGetDevicePointer(&dp, e->h_abort, 0));
+      e->d_abort = static_cast<const volatile int*>(dp);
+    }
     if (e->G > 1) {
       if (!cfg->nccl_id) throw Fail{DSEL_E_INVALID, "world_size > 1 requires nccl_id"};
-      ncclUniqueId id;
-      std::memcpy(&id, cfg->nccl_id, sizeof(id));
-      NC(ncclCommInitRank(&e->comm, e->G, id, e->rank));
-      // establish NCCL's peer connections now (lazily done by the first call of
-      // each collective), so round 1 of the first selection is not charged for it
-      double* wb = e->Pbuf ? e->Pbuf : e->Lk;
-      const size_t wn = std::min<size_t>(e->Pbuf ? (size_t)e->n * e->nt : (size_t)e->nt * e->nt, 1 << 20);
-      NC(ncclGroupStart());
-      NC(ncclAllGather(e->d_rec, e->d_recs, sizeof(ArgRec), ncclUint8, e->comm, e->s));
-      NC(ncclGroupEnd());
-      NC(ncclAllReduce(wb, wb, wn, ncclDouble, ncclSum, e->comm, e->s));
-      NC(ncclBroadcast(wb, wb, wn, ncclDouble, 0, e->comm, e->s));
-      CU(cudaMemsetAsync(wb, 0, sizeof(double) * wn, e->s));
-      setup_p2p(e);
+      std::memcpy(e->nccl_id, cfg->nccl_id, sizeof(e->nccl_id));
     }
     build_tables(e);
     CU(cudaStreamSynchronize(e->s));
+    if (e->G > 1 && !cfg->defer_connect) connect_impl(e);
   } catch (...) {
     destroy_impl(e);
     throw;
   }
   *out = e;
+}
+
+// The collective half of create (world_size > 1): NCCL communicator, warm
+// collectives and the NVLink peer mappings. Split from the allocations so a
+// caller can agree that every rank created its engine before any rank blocks
+// in ncclCommInitRank (dsel_config.defer_connect + dsel_connect).
+void connect_impl(dsel_engine* e) {
+  if (e->G == 1 || e->comm) return;
+  CU(cudaSetDevice(e->dev));
+  ncclUniqueId id;
+  std::memcpy(&id, e->nccl_id, sizeof(id));
+  NC(ncclCommInitRank(&e->comm, e->G, id, e->rank));
+  // establish NCCL's peer connections now (lazily done by the first call of
+  // each collective), so round 1 of the first selection is not charged for it
+  double* wb = e->Pbuf ? e->Pbuf : e->Lk;
+  const size_t wn = std::min<size_t>(e->Pbuf ? (size_t)e->n * e->nt : (size_t)e->nt * e->nt, 1 << 20);
+  NC(ncclGroupStart());
+  NC(ncclAllGather(e->d_rec, e->d_recs, sizeof(ArgRec), ncclUint8, e->comm, e->s));
+  NC(ncclGroupEnd());
+  NC(ncclAllReduce(wb, wb, wn, ncclDouble, ncclSum, e->comm, e->s));
+  NC(ncclBroadcast(wb, wb, wn, ncclDouble, 0, e->comm, e->s));
+  CU(cudaMemsetAsync(wb, 0, sizeof(double) * wn, e->s));
+  setup_p2p(e);
+  CU(cudaStreamSynchronize(e->s));
 }
 
 void ensure_stage(dsel_engine* e, size_t elems) {
@@ -1605,7 +1796,7 @@ void ensure_stage(dsel_engine* e, size_t elems) {
   e->stage = nullptr;
   e->h_stage = nullptr;
   e->stage = dmalloc<double>(2 * elems, e->dev_bytes);
-  CU(cudaMallocHost(&e->h_stage, elems * sizeof(double)));
+  CU(ds_malloc_host(&e->h_stage, elems * sizeof(double)));
   e->stage_elems = elems;
 }
 
@@ -1623,7 +1814,7 @@ void ensure_hstore(dsel_engine* e) {
   e->hk_user = nullptr;  // loading data detaches a caller's K
   if (!e->hstore) {
     CU(cudaSetDevice(e->dev));
-    CU(cudaMallocHost(&e->hstore, sizeof(double) * (size_t)e->nc * std::max(e->nloc, 1) * e->nt * e->nt));
+    CU(ds_malloc_host(&e->hstore, sizeof(double) * (size_t)e->nc * std::max(e->nloc, 1) * e->nt * e->nt));
   }
 }
 
@@ -1683,21 +1874,22 @@ void load_panel(dsel_engine* e, int j, const double* host, bool as_column) {
   if (e->sym) e->full_panels = false;
   CU(cudaEventRecord(e->ev_copy[b], e->cs));
   CU(cudaStreamWaitEvent(e->s, e->ev_copy[b], 0));
-  double* panel = e->C + (size_t)q * e->nt * e->n;
+  const PanelGeom g = e->geom();
+  double* panel = g.panel(q);
   const long long total = (long long)(e->nc - p_first) * e->nt * e->nt;
   const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
   if (total > 0) {
     if (as_column)
       scatter_block_col_kernel<<<blocks, 256, 0, e->s>>>(buf, e->nt, e->d_pos_sensor, e->nc,
-                                                         panel, e->n, p_first, s_off);
+                                                         panel, g.ld(q), g.start(q), p_first, s_off);
     else
       scatter_block_row_kernel<<<blocks, 256, 0, e->s>>>(buf, e->nt, e->d_pos_sensor, e->nc,
-                                                         panel, e->n, p_first, s_off);
+                                                         panel, g.ld(q), g.start(q), p_first, s_off);
   }
   CU(cudaGetLastError());
   CU(cudaEventRecord(e->ev_scat[b], e->s));
   if (e->keep)
-    CU(cudaMemcpyAsync(e->K0 + (size_t)q * e->nt * e->n, panel, sizeof(double) * e->n * e->nt,
+    CU(cudaMemcpyAsync(e->K0 + g.off(q), panel, sizeof(double) * g.ld(q) * e->nt,
                        cudaMemcpyDeviceToDevice, e->s));
 }
 
@@ -1768,6 +1960,36 @@ const char* dsel_last_error(const dsel_engine* e) {
 
 uint64_t dsel_device_bytes(const dsel_engine* e) { return e ? e->dev_bytes : 0; }
 
+uint64_t dsel_alloc_count(void) { return g_allocs.load(); }
+
+dsel_status dsel_get_plan(const dsel_engine* e, dsel_plan* out) {
+  if (!e || !out) return DSEL_E_INVALID;
+  dsel_plan p{};
+  p.storage = e->stream ? DSEL_STORAGE_STREAM : DSEL_STORAGE_HBM;
+  p.algorithm = e->ll ? 1 : 0;
+  p.symmetric = e->sym ? 1 : 0;
+  p.packed = e->packed ? 1 : 0;
+  p.device_bytes = e->dev_bytes;
+  p.planned_bytes = e->planned;
+  p.budget_bytes = e->plan_budget;
+  p.host_store_bytes = e->hstore ? sizeof(double) * (uint64_t)e->nc * std::max(e->nloc, 1) * e->nt * e->nt : 0;
+  *out = p;
+  return DSEL_OK;
+}
+
+dsel_status dsel_connect(dsel_engine* e) {
+  return guard(e, [&] { connect_impl(e); });
+}
+
+dsel_status dsel_abort(dsel_engine* e) {
+  if (!e) return DSEL_E_INVALID;
+  bool expect = false;
+  if (!e->aborted.compare_exchange_strong(expect, true)) return DSEL_OK;
+  if (e->h_abort) *reinterpret_cast<volatile int*>(e->h_abort) = 1;  // releases NVLink flag waits
+  if (e->comm) ncclCommAbort(e->comm);  // releases collectives blocked on the failed peer
+  return DSEL_OK;
+}
+
 dsel_status dsel_sync(dsel_engine* e) {
   return guard(e, [&] {
     CU(cudaSetDevice(e->dev));
@@ -1800,7 +2022,7 @@ void attach_host(dsel_engine* e, const double* host_k, bool rows) {
     cudaGetLastError();
     // pageable: pin in place (read-only) so the per-round copies are DMA
     void* base = const_cast<double*>(host_k);
-    CU(cudaHostRegister(base, bytes, cudaHostRegisterReadOnly));
+    CU(ds_host_register(base, bytes, cudaHostRegisterReadOnly));
     e->hk_registered = base;
   }
   if (e->hstore) {  // the caller's K replaces a filled store
@@ -1892,7 +2114,7 @@ void load_kbf_impl(dsel_engine* e, const char* path, bool exact_columns, int thr
   cudaEvent_t freed[2] = {nullptr, nullptr};
   try {
     for (int b = 0; b < 2; ++b) {
-      CU(cudaMallocHost(&hb[b], row_bytes));
+      CU(ds_malloc_host(&hb[b], row_bytes));
       CU(cudaEventCreateWithFlags(&freed[b], cudaEventDisableTiming));
     }
     if (threads <= 0) threads = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
@@ -1976,10 +2198,10 @@ dsel_status dsel_read_block_row(dsel_engine* e, int j, double* host_row) {
       if (e->G != 1)
         throw Fail{DSEL_E_STATE, "read_block_row of a sharded symmetric store needs full panels "
                                  "and no rounds (or world_size 1)"};
-      gather_block_row_sym_kernel<<<blocks, 256, 0, e->s>>>(e->C, e->n, e->nt, p, e->d_pos_sensor,
-                                                            e->nc, e->stage);
+      gather_block_row_sym_kernel<<<blocks, 256, 0, e->s>>>(e->geom(), p, e->d_pos_sensor, e->nc,
+                                                            e->stage);
     } else {
-      gather_block_row_kernel<<<blocks, 256, 0, e->s>>>(e->C + (size_t)q * e->nt * e->n, e->n,
+      gather_block_row_kernel<<<blocks, 256, 0, e->s>>>(e->geom().panel(q), e->n,
                                                         e->nt, e->d_pos_sensor, e->nc, e->stage);
     }
     CU(cudaGetLastError());
@@ -2007,8 +2229,8 @@ dsel_status dsel_gen_synthetic(dsel_engine* e, const double* v_host, int rank, d
       g.n_rows = (int)e->n;
       g.col_sensor = e->d_slot_sensor;
       g.n_cols = e->nloc * e->nt;
-      g.C = e->C;
-      g.ldc = e->n;
+      g.geom = e->geom();
+      g.q0 = 0;
       dim3 grid((g.n_rows + gen::BM - 1) / gen::BM, (g.n_cols + gen::BN - 1) / gen::BN);
       synth_panel_kernel<<<grid, gen::THREADS, 0, e->s>>>(g);
       ce = cudaGetLastError();
@@ -2020,8 +2242,8 @@ dsel_status dsel_gen_synthetic(dsel_engine* e, const double* v_host, int rank, d
       ensure_hstore(e);
       double* panel = nullptr;
       double* packed = nullptr;
-      ce = cudaMalloc(&panel, sizeof(double) * (size_t)e->n * e->nt);
-      if (ce == cudaSuccess) ce = cudaMalloc(&packed, sizeof(double) * (size_t)e->nc * n2);
+      ce = ds_malloc(&panel, sizeof(double) * (size_t)e->n * e->nt);
+      if (ce == cudaSuccess) ce = ds_malloc(&packed, sizeof(double) * (size_t)e->nc * n2);
       for (int q = 0; q < e->nloc && ce == cudaSuccess; ++q) {
         GenArgs g{};
         g.V = V;
@@ -2032,8 +2254,8 @@ dsel_status dsel_gen_synthetic(dsel_engine* e, const double* v_host, int rank, d
         g.n_rows = (int)e->n;
         g.col_sensor = e->d_slot_sensor + q;
         g.n_cols = e->nt;
-        g.C = panel;
-        g.ldc = e->n;
+        g.geom = PanelGeom{panel, e->n, e->nt, 1, 0, 0};  // one full-height temporary panel
+        g.q0 = 0;
         dim3 grid((g.n_rows + gen::BM - 1) / gen::BM, (g.n_cols + gen::BN - 1) / gen::BN);
         synth_panel_kernel<<<grid, gen::THREADS, 0, e->s>>>(g);
         const long long total = (long long)e->nc * n2;
@@ -2051,10 +2273,9 @@ dsel_status dsel_gen_synthetic(dsel_engine* e, const double* v_host, int rank, d
     }
     cudaFree(V);
     if (ce != cudaSuccess) throw Fail{DSEL_E_CUDA, std::string("synthetic K: ") + cudaGetErrorString(ce)};
-    e->full_panels = true;
+    e->full_panels = !e->packed;
     if (e->keep && e->C)
-      CU(cudaMemcpyAsync(e->K0, e->C, sizeof(double) * e->n * e->nloc * e->nt,
-                         cudaMemcpyDeviceToDevice, e->s));
+      CU(cudaMemcpyAsync(e->K0, e->C, sizeof(double) * e->c_elems, cudaMemcpyDeviceToDevice, e->s));
     CU(cudaStreamSynchronize(e->s));
   });
 }
@@ -2073,11 +2294,11 @@ dsel_status dsel_gen_synthetic_device(dsel_engine* e, int rank, double sigma, ui
     const int n_rows = R * nt, n_cols = Rl * nt;
     const bool sym = e->sym;
     if (sym) sym_tables(e);
-    CU(cudaMemsetAsync(e->C, 0, sizeof(double) * e->n * e->nloc * nt, e->s));
+    CU(cudaMemsetAsync(e->C, 0, sizeof(double) * e->c_elems, e->s));
     if (e->nloc > 0) {
       const long long total = (long long)e->nloc * nt;
       add_diag_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 1024), 256, 0, e->s>>>(
-          e->C, e->n, nt, e->nloc, e->G, e->rank, sigma * sigma);
+          e->geom(), e->nloc, sigma * sigma);
       CU(cudaGetLastError());
     }
     constexpr int kch = 512;  // rank columns per update launch
@@ -2093,7 +2314,7 @@ dsel_status dsel_gen_synthetic_device(dsel_engine* e, int rank, double sigma, ui
       // C += V V^T: the update kernel with W = +V on both sides
       UpdateWSArgs ua{};
       ua.C = e->C;
-      ua.ldc = e->n;
+      ua.geom = e->geom();
       ua.Wt = Vt;
       ua.Wnt = Vt;
       ua.mpad = mpad;
@@ -2123,8 +2344,7 @@ dsel_status dsel_gen_synthetic_device(dsel_engine* e, int rank, double sigma, ui
     e->gen_flops = gen_flops;
     e->full_panels = !sym;
     if (e->keep && e->C)
-      CU(cudaMemcpyAsync(e->K0, e->C, sizeof(double) * e->n * e->nloc * e->nt,
-                         cudaMemcpyDeviceToDevice, e->s));
+      CU(cudaMemcpyAsync(e->K0, e->C, sizeof(double) * e->c_elems, cudaMemcpyDeviceToDevice, e->s));
     CU(cudaStreamSynchronize(e->s));
   });
 }
@@ -2195,15 +2415,15 @@ dsel_status dsel_assemble_lti(dsel_engine* e, const dsel_lti* lp, double* noise_
       lti_response_kernel<<<grid((long long)np2), 256, 0, e->s>>>(h, vf, 0, nm, nt, 0, (int)n, js, 1, p2);
       const double wc = lp->cost_weights ? lp->cost_weights[js] : 1.0;
       lti_panel_kernel<<<grid((long long)e->nc * nt * nt), 256, 0, e->s>>>(
-          p1, p2, nd, nt, js, wc * gamma2, e->d_pos_sensor, e->nc, e->C + (size_t)q * nt * e->n, e->n);
+          p1, p2, nd, nt, js, wc * gamma2, e->d_pos_sensor, e->nc, e->geom().panel(q), e->geom().ld(q),
+          e->geom().start(q));
       ce = cudaGetLastError();
     }
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(e->s);
     if (ce != cudaSuccess) throw Fail{DSEL_E_CUDA, std::string("assemble_lti: ") + cudaGetErrorString(ce)};
-    e->full_panels = true;
+    e->full_panels = !e->packed;
     if (e->keep && e->C)
-      CU(cudaMemcpyAsync(e->K0, e->C, sizeof(double) * e->n * e->nloc * e->nt,
-                         cudaMemcpyDeviceToDevice, e->s));
+      CU(cudaMemcpyAsync(e->K0, e->C, sizeof(double) * e->c_elems, cudaMemcpyDeviceToDevice, e->s));
     CU(cudaStreamSynchronize(e->s));
   });
 }
@@ -2265,6 +2485,12 @@ int dsel_get_trace(dsel_engine* e, dsel_step_info* rows, int max_rows) {
       r.ms_panel = c;
       r.ms_update = d;
       r.ms_round = tot;
+      r.ms_io = 0.0;
+      if (std::find(e->streamed_round.begin(), e->streamed_round.end(), i) != e->streamed_round.end()) {
+        float io = 0;
+        CU(cudaEventElapsedTime(&io, ev[5], ev[6]));  // streamed K blocks, copy stream
+        r.ms_io = io;
+      }
       rows[i] = r;
     }
     return n;
@@ -2294,8 +2520,7 @@ dsel_status dsel_reset(dsel_engine* e) {
     if (!e->keep && !e->ll) throw Fail{DSEL_E_STATE, "dsel_reset requires keep_pristine"};
     CU(cudaSetDevice(e->dev));
     if (!e->ll)  // the left-looking store is K itself and is never modified
-      CU(cudaMemcpyAsync(e->C, e->K0, sizeof(double) * e->n * e->nloc * e->nt,
-                         cudaMemcpyDeviceToDevice, e->s));
+      CU(cudaMemcpyAsync(e->C, e->K0, sizeof(double) * e->c_elems, cudaMemcpyDeviceToDevice, e->s));
     reset_state(e);
     CU(cudaStreamSynchronize(e->s));
   });
@@ -2338,40 +2563,66 @@ dsel_status dsel_get_stats(dsel_engine* e, dsel_stats* st) {
   });
 }
 
+namespace {
+// Block row i of L_S (nt x (i+1)*nt, row-major) into the host staging buffer
+// (collective: broadcast from the owner of the i-th chosen candidate).
+void factor_row(dsel_engine* e, int i) {
+  const int nt = e->nt;
+  const long long n2 = (long long)nt * nt;
+  const long long slot_stride = (long long)e->eff_budget * n2;
+  const int p = e->sensor_pos[e->chosen[i]];
+  const int owner = p % e->G, q = p / e->G;
+  const long long total = n2 * (i + 1);
+  ensure_stage(e, (size_t)total);
+  if (owner == e->rank) {
+    if (e->ll)
+      ll_pack_factor_row_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 2048), 256, 0,
+                                  e->s>>>(e->Wown, e->own_mpad, q * nt, nt, e->ldw, i + 1,
+                                          e->ldiag + (size_t)i * n2, e->stage);
+    else
+      pack_factor_row_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 2048), 256, 0, e->s>>>(
+          e->hist + q * slot_stride, nt, i + 1, e->stage);
+    CU(cudaGetLastError());
+  }
+  if (e->G > 1) NC(ncclBroadcast(e->stage, e->stage, (size_t)total, ncclDouble, owner, e->comm, e->s));
+  CU(cudaMemcpyAsync(e->h_stage, e->stage, sizeof(double) * total, cudaMemcpyDeviceToHost, e->s));
+  CU(cudaStreamSynchronize(e->s));
+}
+
+void check_factor_export(dsel_engine* e) {
+  if (!e->export_factor && !e->ll) throw Fail{DSEL_E_STATE, "engine created without export_factor"};
+  CU(cudaSetDevice(e->dev));
+}
+}  // namespace
+
 dsel_status dsel_export_factor(dsel_engine* e, double* host, int64_t ld) {
   return guard(e, [&] {
-    if (!e->export_factor && !e->ll)
-      throw Fail{DSEL_E_STATE, "engine created without export_factor"};
+    check_factor_export(e);
     const int k = (int)e->chosen.size();
     const int nt = e->nt;
     if (ld < (int64_t)k * nt) throw Fail{DSEL_E_INVALID, "ld smaller than k*n_steps"};
-    CU(cudaSetDevice(e->dev));
-    const long long n2 = (long long)nt * nt;
-    const long long slot_stride = (long long)e->eff_budget * n2;
     ensure_stage(e, (size_t)nt * std::max(k, 1) * nt);
     for (int i = 0; i < k; ++i) {
-      const int p = e->sensor_pos[e->chosen[i]];
-      const int owner = p % e->G, q = p / e->G;
-      const long long total = n2 * (i + 1);
-      if (owner == e->rank) {
-        if (e->ll)
-          ll_pack_factor_row_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 2048), 256,
-                                      0, e->s>>>(e->Wown, e->own_mpad, q * nt, nt, e->ldw, i + 1,
-                                                 e->ldiag + (size_t)i * n2, e->stage);
-        else
-          pack_factor_row_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 2048), 256, 0,
-                                   e->s>>>(e->hist + q * slot_stride, nt, i + 1, e->stage);
-        CU(cudaGetLastError());
-      }
-      if (e->G > 1) NC(ncclBroadcast(e->stage, e->stage, (size_t)total, ncclDouble, owner, e->comm, e->s));
-      CU(cudaMemcpyAsync(e->h_stage, e->stage, sizeof(double) * total, cudaMemcpyDeviceToHost, e->s));
-      CU(cudaStreamSynchronize(e->s));
+      factor_row(e, i);
       for (int a = 0; a < nt; ++a) {
         double* dst = host + ((int64_t)i * nt + a) * ld;
         std::memcpy(dst, e->h_stage + (size_t)a * (i + 1) * nt, sizeof(double) * (size_t)(i + 1) * nt);
         std::fill(dst + (size_t)(i + 1) * nt, dst + (size_t)k * nt, 0.0);
       }
     }
+  });
+}
+
+dsel_status dsel_export_factor_row(dsel_engine* e, int i, double* host, int64_t ld) {
+  return guard(e, [&] {
+    check_factor_export(e);
+    if (i < 0 || i >= (int)e->chosen.size()) throw Fail{DSEL_E_RANGE, "factor block row out of range"};
+    const int nt = e->nt;
+    if (ld < (int64_t)(i + 1) * nt) throw Fail{DSEL_E_INVALID, "ld smaller than (i+1)*n_steps"};
+    factor_row(e, i);
+    for (int a = 0; a < nt; ++a)
+      std::memcpy(host + (int64_t)a * ld, e->h_stage + (size_t)a * (i + 1) * nt,
+                  sizeof(double) * (size_t)(i + 1) * nt);
   });
 }
 

@@ -22,6 +22,38 @@
 namespace dsel {
 
 // ------------------------------------------------------------------------ //
+// Panel store geometry. Local slot q holds the block column of candidate   //
+// position p = q*G + rank, column-major. Full square: all n rows, ld = n.  //
+// Packed block-lower (symmetric storage): only rows from the panel's own   //
+// diagonal block down, start(q) = p*nt, ld(q) = n - p*nt, panels back to   //
+// back -- half the HBM of the full square. Element (physical row r >=      //
+// start(q), panel column c) lives at base[idx(q, c, r)].                    //
+// ------------------------------------------------------------------------ //
+struct PanelGeom {
+  double* base;
+  long long n;  // rows of a full panel (n_cand * nt)
+  int nt, G, rank;
+  int packed;
+  __host__ __device__ __forceinline__ long long start(int q) const {
+    return packed ? (long long)(q * G + rank) * nt : 0;
+  }
+  __host__ __device__ __forceinline__ long long ld(int q) const { return n - start(q); }
+  __host__ __device__ __forceinline__ long long off(int q) const {
+    if (!packed) return (long long)q * nt * n;
+    const long long qq = q;
+    return (long long)nt * (qq * n - (long long)nt * ((long long)G * qq * (qq - 1) / 2 + (long long)rank * qq));
+  }
+  // element offset; rows above start(q) give addresses that belong to other
+  // data (callers mask them) -- at most `n` elements before base under packing
+  __host__ __device__ __forceinline__ long long idx(int q, int c, long long row) const {
+    return off(q) + (long long)c * ld(q) + row - start(q);
+  }
+  __host__ __device__ __forceinline__ double* panel(int q) const { return base + off(q); }
+  // total elements of nloc panels
+  __host__ __device__ __forceinline__ long long total(int nloc) const { return off(nloc); }
+};
+
+// ------------------------------------------------------------------------ //
 // PTX helpers                                                               //
 // ------------------------------------------------------------------------ //
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
@@ -312,8 +344,8 @@ struct Cfg {
   static constexpr size_t OFF_R = 0;
   static constexpr size_t OFF_C = OFF_R + (size_t)STAGES * SC * BR * KC * 8;
   static constexpr size_t OFF_CT = OFF_C + (size_t)STAGES * SC * BC * KC * 8;
-  static constexpr size_t OFF_MAPS = OFF_CT + (size_t)BC * CP * 8;  // 2 x {colbase, rowphys, cshift}
-  static constexpr size_t MAPS_BYTES = (size_t)BC * 8 + BR * 4 + BC * 4;
+  static constexpr size_t OFF_MAPS = OFF_CT + (size_t)BC * CP * 8;  // 2 x {colbase, rowphys, cshift, colstart}
+  static constexpr size_t MAPS_BYTES = (size_t)BC * 8 + BR * 4 + BC * 4 + BC * 4;
   static constexpr size_t OFF_RUNS = OFF_MAPS + 2 * MAPS_BYTES;     // producer scratch
   static constexpr size_t OFF_BAR = OFF_RUNS + (size_t)(2 * BC + BR + 8) * 8;
   static constexpr size_t OFF_SYM = OFF_BAR + 16 * 8;
@@ -335,8 +367,9 @@ __host__ __device__ __forceinline__ size_t wt_index(int row, int k, int mpad) {
 }
 
 struct UpdateWSArgs {
-  double* C;
-  long long ldc;
+  double* C;           // = geom.base (null: accumulate from zero, left-looking streaming)
+  PanelGeom geom;      // panel store geometry of C (packed: rows above a panel's
+                       // diagonal block are not stored and never written)
   const double* Wt;   // +W tiled (r-side)
   const double* Wnt;  // -W tiled (c-side)
   int mpad;           // rows of the tiled buffers (multiple of BR)
@@ -511,6 +544,9 @@ __global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(
   auto cshift_of = [&](int b) {
     return reinterpret_cast<int*>(smem_raw + OFF_MAPS + b * MAPS_BYTES + BC * 8 + BR * 4);
   };
+  auto colstart_of = [&](int b) {  // first stored physical row of each column (packed store)
+    return reinterpret_cast<int*>(smem_raw + OFF_MAPS + b * MAPS_BYTES + BC * 8 + BR * 4 + BC * 4);
+  };
   int* cw = reinterpret_cast<int*>(smem_raw + OFF_RUNS);        // [BC] W row of each c column
   int* runs = cw + BC;                                          // row runs: start,len pairs
   const int nt = a.nt;
@@ -569,6 +605,7 @@ __global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(
       long long* colbase = colbase_of(b);
       int* rowphys = rowphys_of(b);
       int* cshift = cshift_of(b);
+      int* colstart = colstart_of(b);
       int rp[BR / 32];
 #pragma unroll
       for (int m = 0; m < BR / 32; ++m) {
@@ -590,10 +627,13 @@ __global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(
         if (i < ncv) {
           const int blk = c / nt;
           const int off = c - blk * nt;
-          colbase[i] = (long long)(a.col_slot[blk] * nt + off) * a.ldc;
+          const int q = a.col_slot[blk];
+          colbase[i] = a.geom.idx(q, off, 0);
+          colstart[i] = (int)a.geom.start(q);
           cwl[m] = a.col_g[blk] * nt + off;
         } else {
           colbase[i] = -1;
+          colstart[i] = 0;
           cwl[m] = 0;  // columns past the edge read W row 0 (never stored)
         }
         cw[i] = cwl[m];
@@ -771,15 +811,19 @@ __global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(
         }
       }
     } else {
+      // packed store: rows above the column's diagonal block are not stored
+      // (their slots hold the previous column's data) -- never written
+      const int* cst = colstart_of(b);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const long long cb = colbase[wc + i * 8 + g];
         if (cb < 0) continue;
         double* col = a.C + cb;
+        const int c_lo = cst[wc + i * 8 + g];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int p0 = rowphys[wr + j * 8 + 2 * t];
-          if (p0 < 0) continue;
+          if (p0 < c_lo) continue;  // also p0 < 0 (rows past the edge)
           __stcs(reinterpret_cast<double2*>(col + p0), make_double2(acc[i][j][0], acc[i][j][1]));
         }
       }
@@ -832,9 +876,11 @@ struct PanelArgs {
   const double* P;      // panel, column-major, element (row, m) at P[m*ldp + row]
   long long ldp;
   // symmetric storage: rows of blocks below the chosen one (position > pk)
-  // are read in place from the chosen candidate's own panel P2 (same ldp);
-  // only the transposed blocks above it were gathered into P (null: all P)
+  // are read in place from the chosen candidate's own panel P2 (column stride
+  // ldp2, first stored row p2_row0 -- PanelGeom of the owner); only the
+  // transposed blocks above it were gathered into P (null: all P)
   const double* P2;
+  long long ldp2, p2_row0;
   int pk;
   const double* Linv;   // row-major [c][m], ld = ldl, zero above the diagonal and in pads
   int ldl;
@@ -899,7 +945,9 @@ __global__ void __launch_bounds__(pw::THREADS, 2) panel_w_kernel(PanelArgs a) {
         const int rr = (idx - k * (BR / 2)) * 2;
         const int pr = rowphys[rr];
         const bool ok = pr >= 0 && kc + k < nt;
-        const double* src = (rowsrc[rr] ? a.P2 : a.P) + (ok ? (size_t)(kc + k) * a.ldp + pr : 0);
+        const double* src = !ok ? a.P
+                            : rowsrc[rr] ? a.P2 + (size_t)(kc + k) * a.ldp2 + (pr - a.p2_row0)
+                                         : a.P + (size_t)(kc + k) * a.ldp + pr;
         cp_async16(dA + k * LDA + rr, src, ok);
       }
     } else {
@@ -908,7 +956,9 @@ __global__ void __launch_bounds__(pw::THREADS, 2) panel_w_kernel(PanelArgs a) {
         const int rr = idx - k * BR;
         const int pr = rowphys[rr];
         const bool ok = pr >= 0 && kc + k < nt;
-        const double* src = (rowsrc[rr] ? a.P2 : a.P) + (ok ? (size_t)(kc + k) * a.ldp + pr : 0);
+        const double* src = !ok ? a.P
+                            : rowsrc[rr] ? a.P2 + (size_t)(kc + k) * a.ldp2 + (pr - a.p2_row0)
+                                         : a.P + (size_t)(kc + k) * a.ldp + pr;
         cp_async8(dA + k * LDA + rr, src, ok);
       }
     }
@@ -1292,8 +1342,8 @@ __global__ void ll_extract_wk_kernel(const double* Wown, int own_mpad, int row0,
 }
 
 // Gain-kernel input for the left-looking mode: D blocks live in their own
-// buffer; the chol kernel reads them through (src_col, src_row) = (slot*nt, 0)
-// with lds = nt (column-major nt x nt per slot, slots side by side).
+// buffer; the chol kernel reads them at src_off = slot*nt*nt with ld = nt
+// (column-major nt x nt per slot, slots side by side).
 
 // ------------------------------------------------------------------------ //
 // Local top-2 argmax with the reference tie rule (selector.hpp:132-134):   //
@@ -1377,10 +1427,9 @@ __global__ void __launch_bounds__(256) argmax_kernel(const double* gain, const i
 // (linalg.hpp:16-35, :117-128): pivot <= 0 or nonfinite -> infeasible.    //
 // ------------------------------------------------------------------------ //
 struct CholArgs {
-  const double* src;        // C base (column-major, ld = lds)
-  long long lds;
-  const int* src_col;       // per batch entry: first column (local) of the block
-  const int* src_row;       // per batch entry: first row of the block
+  const double* src;        // panel store base
+  const long long* src_off; // per batch entry: element offset of the block's (0,0)
+  const long long* src_ld;  // per batch entry: column stride of its panel
   double* L;                // scratch, column-major nt x nt per batch entry
   long long l_stride;       // doubles between batch entries of L
   double* gain;             // out: 2*sum(log diag) or -inf when infeasible
@@ -1417,6 +1466,10 @@ __device__ __forceinline__ void gain_epilogue(const CholArgs& a) {
 // (relative error ~1e-16; shorter dependency chain than the library rsqrt,
 // which handles special cases the caller has already excluded).
 __device__ __forceinline__ double fast_rsqrt(double p) {
+  // the float seed needs p inside float range; any other finite positive
+  // pivot (the reference accepts all, linalg.hpp:22-24) takes the exact path.
+  // The pivot is warp-uniform here, so the branch is too.
+  if (p < 1e-36 || p > 1e36) return 1.0 / sqrt(p);
   double y = (double)rsqrtf((float)p);
   const double h = 0.5 * p;
   y = y * fma(-h * y, y, 1.5);
@@ -1509,7 +1562,8 @@ __global__ void __launch_bounds__(256, MINB) chol_logdet_kernel(CholArgs a) {
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const double* src = a.src + (size_t)a.src_col[b] * a.lds + a.src_row[b];
+  const double* src = a.src + a.src_off[b];
+  const long long lds = a.src_ld[b];
   double* L = a.L + (size_t)b * a.l_stride;  // column-major nt x nt
   if (tid == 0) s_fail = -1;
 #ifdef DSEL_PROBE
@@ -1531,7 +1585,7 @@ __global__ void __launch_bounds__(256, MINB) chol_logdet_kernel(CholArgs a) {
     __syncthreads();  // previous panel's readers of S are done
     for (int e = tid; e < nb * m; e += 256) {
       const int j = e / m, i = e - j * m;
-      cp_async8(S + j * mp + i, src + (size_t)(J0 + j) * a.lds + J0 + i, true);
+      cp_async8(S + j * mp + i, src + (size_t)(J0 + j) * lds + J0 + i, true);
     }
     cp_async_commit();
     // left-looking: S -= L[J0:, 0:J0] * L[J0:J0+nb, 0:J0]^T on DMMA, the factor
@@ -1691,7 +1745,8 @@ __global__ void __launch_bounds__(256, MINB) chol_logdet_tri_kernel(CholArgs a) 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const double* src = a.src + (size_t)a.src_col[b] * a.lds + a.src_row[b];
+  const double* src = a.src + a.src_off[b];
+  const long long lds = a.src_ld[b];
   double* L = a.L + (size_t)b * a.l_stride;  // column-major nt x nt
   if (tid == 0) s_fail = -1;
   // the lower triangle (by panels, rows from each panel's diagonal down), one async load
@@ -1700,7 +1755,7 @@ __global__ void __launch_bounds__(256, MINB) chol_logdet_tri_kernel(CholArgs a) 
     double* Sq = T + tri_offset(nt, q);
     for (int e = tid; e < nb * m; e += 256) {
       const int j = e / m, i = e - j * m;
-      cp_async8(Sq + j * P + i, src + (size_t)(J0 + j) * a.lds + J0 + i, true);
+      cp_async8(Sq + j * P + i, src + (size_t)(J0 + j) * lds + J0 + i, true);
     }
   }
   cp_async_commit();
@@ -1950,9 +2005,10 @@ __global__ void hist_diag_kernel(const double* Lk, int nt, double* dst) {
 // KBF / DataSpaceHessian order, kstore.hpp:22-35) -> panel of candidate j,  //
 // using K(i,j)[r][c] = K(j,i)[c][r] (exact for symmetric K).               //
 __global__ void scatter_block_row_kernel(const double* row, int nt, const int* pos_sensor,
-                                         int n_cand, double* panel, long long ldc, int p_first,
-                                         int s_off) {
-  // panel[(c)*ldc + p*nt + r] = row[(sensor(p) - s_off)*nt*nt + c*nt + r], p >= p_first
+                                         int n_cand, double* panel, long long ldc, long long row0,
+                                         int p_first, int s_off) {
+  // panel[c*ldc + p*nt + r - row0] = row[(sensor(p) - s_off)*nt*nt + c*nt + r], p >= p_first
+  // (row0: the panel's first stored row, PanelGeom::start)
   const int np = n_cand - p_first;
   const long long total = (long long)np * nt * nt;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
@@ -1961,7 +2017,7 @@ __global__ void scatter_block_row_kernel(const double* row, int nt, const int* p
     const long long rest = e / nt;
     const int p = p_first + (int)(rest % np);
     const int c = (int)(rest / np);
-    panel[(size_t)c * ldc + (size_t)p * nt + r] =
+    panel[(size_t)c * ldc + (size_t)p * nt + r - row0] =
         row[(size_t)(pos_sensor[p] - s_off) * nt * nt + (size_t)c * nt + r];
   }
 }
@@ -1970,8 +2026,8 @@ __global__ void scatter_block_row_kernel(const double* row, int nt, const int* p
 // (exact reference semantics: read_test_column reads blocks (S[t], s),
 // kaccess.hpp:27-35).
 __global__ void scatter_block_col_kernel(const double* colblk, int nt, const int* pos_sensor,
-                                         int n_cand, double* panel, long long ldc, int p_first,
-                                         int s_off) {
+                                         int n_cand, double* panel, long long ldc, long long row0,
+                                         int p_first, int s_off) {
   const int np = n_cand - p_first;
   const long long total = (long long)np * nt * nt;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
@@ -1980,7 +2036,7 @@ __global__ void scatter_block_col_kernel(const double* colblk, int nt, const int
     const long long rest = e / nt;
     const int p = p_first + (int)(rest % np);
     const int c = (int)(rest / np);
-    panel[(size_t)c * ldc + (size_t)p * nt + r] =
+    panel[(size_t)c * ldc + (size_t)p * nt + r - row0] =
         colblk[(size_t)(pos_sensor[p] - s_off) * nt * nt + (size_t)r * nt + c];
   }
 }
@@ -2006,9 +2062,10 @@ __global__ void gather_block_row_kernel(const double* panel, long long ldc, int 
 // One CTA per 32 x 32 sub-tile of a block, both the direct
 // (p_i > p_k) and the transposed (p_i < p_k) sources read along their
 // contiguous dimension, the transpose through shared memory.
-__global__ void __launch_bounds__(256) gather_panel_sym_tiled_kernel(const double* C, long long ldc, int nt,
-                                                                     const int* row_pos, int pk, int G,
-                                                                     double* P) {
+__global__ void __launch_bounds__(256) gather_panel_sym_tiled_kernel(PanelGeom geom, const int* row_pos,
+                                                                     int pk, double* P) {
+  const int nt = geom.nt, G = geom.G;
+  const long long ldc = geom.n;  // P is a full-height panel
   __shared__ double tile[32][33];
   const int tpb = (nt + 31) / 32;
   const int blk = blockIdx.x / (tpb * tpb);
@@ -2017,16 +2074,20 @@ __global__ void __launch_bounds__(256) gather_panel_sym_tiled_kernel(const doubl
   const int pi = row_pos[blk];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
   if (pi > pk) {  // P[(pi*nt + r), c] = panel k (column c), row pi*nt + r: rows contiguous
-    const double* srcb = C + (size_t)((pk / G) * nt) * ldc + (size_t)pi * nt;
+    const int q = pk / G;
+    const double* srcb = geom.base + geom.idx(q, 0, (long long)pi * nt);
+    const long long ld = geom.ld(q);
     for (int cc = ty; cc < 32; cc += 8) {
       const int c = c0 + cc, r = r0 + tx;
-      if (c < nt && r < nt) P[(size_t)c * ldc + (size_t)pi * nt + r] = srcb[(size_t)c * ldc + r];
+      if (c < nt && r < nt) P[(size_t)c * ldc + (size_t)pi * nt + r] = srcb[(size_t)c * ld + r];
     }
   } else {  // P[(pi*nt + r), c] = panel i (column r), row pk*nt + c: contiguous in c
-    const double* srcb = C + (size_t)((pi / G) * nt) * ldc + (size_t)pk * nt;
+    const int q = pi / G;
+    const double* srcb = geom.base + geom.idx(q, 0, (long long)pk * nt);
+    const long long ld = geom.ld(q);
     for (int rr = ty; rr < 32; rr += 8) {
       const int r = r0 + rr, c = c0 + tx;
-      tile[rr][tx] = (r < nt && c < nt) ? srcb[(size_t)r * ldc + c] : 0.0;
+      tile[rr][tx] = (r < nt && c < nt) ? srcb[(size_t)r * ld + c] : 0.0;
     }
     __syncthreads();
     for (int cc = ty; cc < 32; cc += 8) {
@@ -2076,9 +2137,12 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   return v;
 }
 
-__global__ void p2p_wait_kernel(const unsigned long long* flag, unsigned long long v) {
+// abort: host-mapped word set by dsel_abort when a peer rank failed, so no
+// spin-wait outlives the run it belongs to
+__global__ void p2p_wait_kernel(const unsigned long long* flag, unsigned long long v,
+                                const volatile int* abort) {
   if (threadIdx.x == 0)
-    while (ld_acquire_sys(flag) < v) {
+    while (ld_acquire_sys(flag) < v && !*abort) {
     }
 }
 
@@ -2089,13 +2153,21 @@ __global__ void w_peer_scatter_kernel(const double* const* peer_w, unsigned long
                                       unsigned long long seq, int G, const int* hb_off, int ldw,
                                       const int* hb, const int* row_pos, int n_blocks, int nt, double* Wt,
                                       double* Wnt, int mpad, double* hist, long long slot_stride,
-                                      long long step_off, int rank) {
+                                      long long step_off, int rank, const volatile int* abort) {
+  __shared__ int s_abort;
+  if (threadIdx.x == 0) s_abort = 0;
+  __syncthreads();
   if (threadIdx.x < G) {
     const unsigned long long* f = peer_flag[threadIdx.x];
     while (ld_acquire_sys(f) < seq) {
+      if (*abort) {
+        s_abort = 1;
+        break;
+      }
     }
   }
   __syncthreads();
+  if (s_abort) return;
   const int half = nt / 2;
   const long long per = (long long)nt * half;
   const long long total = per * n_blocks;
@@ -2127,8 +2199,9 @@ __global__ void w_peer_scatter_kernel(const double* const* peer_w, unsigned long
 
 // Block row j of the current C in symmetric storage (single rank): block
 // (j,i) = panel j's block (i,j)^T when p_i >= p_j, else panel i's block (j,i).
-__global__ void gather_block_row_sym_kernel(const double* C, long long ldc, int nt, int pj,
-                                            const int* pos_sensor, int n_cand, double* row) {
+__global__ void gather_block_row_sym_kernel(PanelGeom geom, int pj, const int* pos_sensor,
+                                            int n_cand, double* row) {
+  const int nt = geom.nt;
   const long long total = (long long)n_cand * nt * nt;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
@@ -2138,9 +2211,9 @@ __global__ void gather_block_row_sym_kernel(const double* C, long long ldc, int 
     const int c = (int)(rest / n_cand);  // row index inside block (j,i)
     double v;
     if (p >= pj)
-      v = C[(size_t)(pj * nt + c) * ldc + (size_t)p * nt + r];
+      v = geom.base[geom.idx(pj, c, (long long)p * nt + r)];
     else
-      v = C[(size_t)(p * nt + r) * ldc + (size_t)pj * nt + c];
+      v = geom.base[geom.idx(p, r, (long long)pj * nt + c)];
     row[(size_t)pos_sensor[p] * nt * nt + (size_t)c * nt + r] = v;
   }
 }
@@ -2226,13 +2299,14 @@ __global__ void gen_v_tiled_kernel(double* Vt, int mpad, int kch, int k0, int ra
 }
 
 // C = sigma^2 on the diagonal of every own slot's diagonal block (C zeroed first)
-__global__ void add_diag_kernel(double* C, long long ldc, int nt, int nloc, int G, int rank, double v) {
+__global__ void add_diag_kernel(PanelGeom geom, int nloc, double v) {
+  const int nt = geom.nt;
   const long long total = (long long)nloc * nt;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const int q = (int)(e / nt), c = (int)(e - (long long)q * nt);
-    const long long p = (long long)q * G + rank;
-    C[((long long)q * nt + c) * ldc + p * nt + c] += v;
+    const long long p = (long long)q * geom.G + geom.rank;
+    geom.base[geom.idx(q, c, p * nt + c)] += v;
   }
 }
 
@@ -2298,13 +2372,15 @@ __global__ void lti_response_kernel(const double* h, const double* vf, int vc0, 
 // ([col][t]): noise on the diagonal block, then the exact block
 // symmetrization of hessian.hpp:129-141: K(js,i)(r,c) = 0.5 (K(i,js)(c,r) + K(js,i)(r,c)).
 __global__ void lti_panel_kernel(const double* p1, const double* p2, int nd, int nt, int js, double noise,
-                                 const int* pos_sensor, int nc, double* panel, long long ldc) {
+                                 const int* pos_sensor, int nc, double* panel, long long ldc,
+                                 long long row0) {
   const long long total = (long long)nc * nt * nt;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const int c = (int)(e % nt);
     const int p = (int)((e / nt) % nc);
     const int r = (int)(e / ((long long)nt * nc));
+    if ((long long)p * nt < row0) continue;  // packed store: above the diagonal block
     const int i = pos_sensor[p];
     double a, b;
     if (i == js) {  // A = block(js, js) + noise I; K = 0.5 (A(r,c) + A(c,r))
@@ -2318,7 +2394,7 @@ __global__ void lti_panel_kernel(const double* p1, const double* p2, int nd, int
       a = p1[((size_t)r * nd + i) * nt + c];            // block(i, js)(c, r): column (js, r), sensor i, time c
       b = p2[((size_t)i * nt + c) * nt + r];            // block(js, i)(r, c): column (i, c), sensor js, time r
     }
-    panel[((size_t)r) * ldc + (size_t)p * nt + c] = __dmul_rn(0.5, __dadd_rn(a, b));
+    panel[((size_t)r) * ldc + (size_t)p * nt + c - row0] = __dmul_rn(0.5, __dadd_rn(a, b));
   }
 }
 
@@ -2331,8 +2407,8 @@ struct GenArgs {
   int n_rows;             // n_cand * nt
   const int* col_sensor;  // local slot q -> sensor id
   int n_cols;             // n_loc * nt
-  double* C;
-  long long ldc;
+  PanelGeom geom;         // output panels (packed: only rows from each diagonal block down)
+  int q0;                 // first slot of column 0 (one-panel launches)
 };
 
 __global__ void __launch_bounds__(gen::THREADS) synth_panel_kernel(GenArgs a) {
@@ -2343,6 +2419,7 @@ __global__ void __launch_bounds__(gen::THREADS) synth_panel_kernel(GenArgs a) {
   const int r0 = blockIdx.x * BM, c0 = blockIdx.y * BN;
   const int tid = threadIdx.x;
   const int nt = a.nt;
+  if (r0 + BM <= a.geom.start(a.q0 + c0 / nt)) return;  // whole tile above the stored rows
   for (int i = tid; i < BM; i += THREADS) {
     const int r = r0 + i;
     arow[i] = r < a.n_rows ? a.row_sensor[r / nt] * nt + r % nt : -1;
@@ -2389,8 +2466,9 @@ __global__ void __launch_bounds__(gen::THREADS) synth_panel_kernel(GenArgs a) {
       if (c >= a.n_cols) continue;
       double v = acc[i][j];
       if (arow[tr + i] == brow[tc + j]) v = __dadd_rn(v, a.noise2);
-      const int q = c / nt, cc = c % nt;
-      a.C[(size_t)(q * nt + cc) * a.ldc + r] = v;
+      const int q = a.q0 + c / nt, cc = c % nt;
+      if (r < a.geom.start(q)) continue;
+      a.geom.base[a.geom.idx(q, cc, r)] = v;
     }
   }
 }

@@ -19,7 +19,10 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._abi import DSEL_OK, STATUS_NAMES, DselArgRec, DselConfig, DselLti, DselStats, DselStepInfo, lib
+from ._abi import (DSEL_OK, STATUS_NAMES, DselArgRec, DselConfig, DselLti, DselPlan, DselStats,
+                   DselStepInfo, lib)
+
+STORAGE = {"auto": 0, "hbm": 1, "stream": 2}
 
 
 # ---- errors (errors.hpp:10-86) -------------------------------------------- #
@@ -74,6 +77,11 @@ def _host_ptr(a):
             raise InvalidConfig(1, "host K must be C-contiguous float64")
         return C.c_void_p(a.ctypes.data)
     return C.c_void_p(a.data_ptr())
+
+
+def alloc_count() -> int:
+    """Device/pinned allocations made by libdsel so far (all engines)."""
+    return int(lib.dsel_alloc_count())
 
 
 def nccl_unique_id() -> bytes:
@@ -146,8 +154,8 @@ class Engine:
     def __init__(self, n_sensors: int, n_steps: int, budget: int, candidates=None, device: int = 0,
                  world_size: int = 1, rank: int = 0, nccl_id: bytes | None = None,
                  keep_pristine: bool = False, export_factor: bool = False,
-                 near_tie_tau: float = 1e-9, storage: int = 0, full_square: bool = False,
-                 algorithm: str = "right"):
+                 near_tie_tau: float = 1e-9, storage: int | str = 0, full_square: bool = False,
+                 algorithm: str = "right", packed: bool = True, hbm_budget: int = 0):
         cfg = DselConfig()
         cfg.n_sensors, cfg.n_steps, cfg.budget = n_sensors, n_steps, budget
         self._cands = None
@@ -160,7 +168,9 @@ class Engine:
         if nccl_id is not None:
             self._id = (C.c_ubyte * 128).from_buffer_copy(nccl_id)
             cfg.nccl_id = C.cast(self._id, C.c_void_p)
-        cfg.storage = storage
+        cfg.storage = STORAGE[storage] if isinstance(storage, str) else int(storage)
+        cfg.panel_layout = 0 if packed else 1
+        cfg.hbm_budget = int(hbm_budget)
         cfg.keep_pristine = int(keep_pristine)
         cfg.export_factor = int(export_factor)
         cfg.near_tie_tau = near_tie_tau
@@ -198,6 +208,15 @@ class Engine:
     @property
     def device_bytes(self) -> int:
         return int(lib.dsel_device_bytes(self.h))
+
+    def plan(self) -> dict:
+        """Storage plan dsel_create resolved (AUTO -> hbm | stream) and its sizes."""
+        p = DselPlan()
+        _check(lib.dsel_get_plan(self.h, C.byref(p)), self.h)
+        d = p.as_dict()
+        d["storage"] = {1: "hbm", 2: "stream"}.get(d["storage"], d["storage"])
+        d["algorithm"] = "left" if d["algorithm"] else "right"
+        return d
 
     # -- panel store ingest --
     def load_k(self, k) -> None:

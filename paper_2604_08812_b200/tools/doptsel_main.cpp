@@ -8,8 +8,13 @@
 //
 //   doptsel select <kbf> --budget B [--mode schur|gpu] [--gpus G] [--workers N]
 //                  [--algorithm right|left] [--storage auto|hbm|stream]
-//                  [--seed S] [--pipeline on|off] [--precision f64]
+//                  [--hbm-budget BYTES] [--seed S] [--pipeline on|off] [--precision f64]
 //                  [--config cfg | --noise-logdets file] [--kbf-rows] [--out DIR]
+//
+// Extra output beside the reference's three files: near_ties.csv (k,
+// chosen_index, gain, runner_up, runner_up_gain, rel_gap, near_tie) -- the
+// top-2 gap of every round, flagged when (g1-g2)/max(|g1|,1) < 1e-9 (the
+// reference tie rule, selector.hpp:132-134, decides exact ties only).
 //   doptsel select --synthetic nd,nt,rank,sigma,seed --budget B ...
 //   doptsel build <config> <out.kbf>     (doptsel_main.cpp:63-75; K on the GPU)
 //
@@ -18,6 +23,8 @@
 // reference and are rejected. --workers is accepted (the reference's CPU
 // worker count) and ignored. evaluate and bench are outside the hot path.
 #include <algorithm>
+#include <atomic>
+#include <limits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -69,7 +76,7 @@ struct SelectArgs {
                    noise_file, synthetic;
   int budget = -1, workers = 1, gpus = 1;
   std::string algorithm = "right", storage = "auto";
-  unsigned long long seed = 0;
+  unsigned long long seed = 0, hbm_budget = 0;
   bool kbf_rows = false;
 };
 
@@ -159,6 +166,7 @@ int cmd_build(const std::string& config, const std::string& out_path) {
 
 struct RankResult {
   dsel_status st = DSEL_OK;
+  bool aborted = false;  // stopped because a peer failed
   std::string err;
   std::vector<dsel_step_info> rows;
 };
@@ -257,6 +265,21 @@ int run_select(const SelectArgs& a) {
     dsel_synthetic_v(nd, nt, rank, syn_seed, v.data(), 0);
   }
   std::vector<RankResult> res(G);
+  std::vector<dsel_engine*> engines(G, nullptr);
+  std::vector<char> created(G, 0);
+  std::atomic<int> arrived{0};
+  std::atomic<bool> failed{false};
+  // every rank creates and loads before any rank enters NCCL; a rank failing
+  // later aborts its peers (dsel_abort) instead of leaving them blocked
+  auto wait_all = [&](int phase) {
+    arrived.fetch_add(1);
+    while (arrived.load() < phase * G) std::this_thread::yield();
+  };
+  auto abort_peers = [&](int r) {
+    failed = true;
+    for (int g = 0; g < G; ++g)
+      if (g != r && engines[g]) dsel_abort(engines[g]);
+  };
   auto worker = [&](int r) {
     RankResult& out = res[r];
     if (a.budget == 0) return;
@@ -273,29 +296,52 @@ int run_select(const SelectArgs& a) {
     cfg.storage = a.storage == "stream" ? DSEL_STORAGE_STREAM
                                         : (a.storage == "hbm" ? DSEL_STORAGE_HBM : DSEL_STORAGE_AUTO);
     if (cfg.storage == DSEL_STORAGE_STREAM) cfg.algorithm = 1;  // streaming is left-looking
+    cfg.hbm_budget = a.hbm_budget;
+    cfg.defer_connect = 1;
     dsel_engine* e = nullptr;
     out.st = dsel_create(&cfg, &e);
-    if (out.st != DSEL_OK) {
-      out.err = dsel_last_error(nullptr);
-      return;
+    if (out.st != DSEL_OK) out.err = dsel_last_error(nullptr);
+    engines[r] = e;
+    if (out.st == DSEL_OK) {
+      out.st = a.synthetic.empty() ? dsel_load_kbf(e, a.kbf.c_str(), a.kbf_rows ? 0 : 1, 0)
+                                   : dsel_gen_synthetic(e, v.data(), rank, sigma);
+      if (out.st != DSEL_OK) out.err = dsel_last_error(e);
     }
-    out.st = a.synthetic.empty() ? dsel_load_kbf(e, a.kbf.c_str(), a.kbf_rows ? 0 : 1, 0)
-                                 : dsel_gen_synthetic(e, v.data(), rank, sigma);
+    created[r] = out.st == DSEL_OK;
+    wait_all(1);
+    bool all = true;
+    for (char c : created) all = all && c;
     int done = 0;
-    if (out.st == DSEL_OK) out.st = dsel_run(e, &done);
-    if (out.st != DSEL_OK) {
-      out.err = dsel_last_error(e);
+    if (all) {
+      out.st = dsel_connect(e);
+      if (out.st == DSEL_OK) out.st = dsel_run(e, &done);
+      if (out.st != DSEL_OK) {
+        out.err = dsel_last_error(e);
+        if (!failed.load()) abort_peers(r);
+        else out.aborted = true;
+      }
+    }
+    if (out.st != DSEL_OK || !all) {
+      if (out.err.empty()) out.err = "a peer rank failed before the selection started";
+      if (out.st == DSEL_OK) out.aborted = true, out.st = DSEL_E_STATE;
     } else {
       out.rows.resize(std::max(a.budget, 1));
       const int n = dsel_get_trace(e, out.rows.data(), (int)out.rows.size());
       out.rows.resize(n > 0 ? n : 0);
     }
-    dsel_destroy(e);
+    wait_all(2);  // no engine is destroyed while a peer may still abort it
+    if (e) dsel_destroy(e);
   };
   std::vector<std::thread> pool;
   for (int r = 0; r < G; ++r) pool.emplace_back(worker, r);
   for (auto& t : pool) t.join();
+  // report the original failure, not the ranks it aborted
+  std::vector<int> order;
   for (int r = 0; r < G; ++r)
+    if (!res[r].aborted) order.push_back(r);
+  for (int r = 0; r < G; ++r)
+    if (res[r].aborted) order.push_back(r);
+  for (int r : order)
     if (res[r].st != DSEL_OK) {
       std::cerr << "error: " << res[r].err << "\n";
       switch (res[r].st) {
@@ -329,13 +375,29 @@ int run_select(const SelectArgs& a) {
     }
   }
   {
+    // near-ties (SURVEY 8(b) trace semantics): a separate file, so trace.csv's
+    // header stays the reference's
+    std::ofstream nf(fs::path(a.out) / "near_ties.csv");
+    nf << "k,chosen_index,gain,runner_up,runner_up_gain,rel_gap,near_tie\n";
+    for (size_t i = 0; i < chosen.size(); ++i) {
+      const auto& r = rows[i];
+      const double gap = r.runner_up >= 0 ? (r.gain - r.runner_up_gain) / std::max(std::fabs(r.gain), 1.0)
+                                          : std::numeric_limits<double>::infinity();
+      nf << r.k << ',' << r.chosen_index << ',' << num17(r.gain) << ',' << r.runner_up << ','
+         << (r.runner_up >= 0 ? num17(r.runner_up_gain) : std::string("")) << ','
+         << (r.runner_up >= 0 ? num17(gap) : std::string("")) << ',' << r.near_tie << '\n';
+    }
+  }
+  {
+    // io_ms: H2D of the round's streamed K blocks (0 when K is resident in HBM);
+    // compute_ms: the round's device work (gains, argmax exchange, W, update)
     std::ofstream rf(fs::path(a.out) / "timing.csv");
     rf << "round,worker,io_ms,compute_ms,wall_ms,overlap\n";
     for (size_t i = 0; i < chosen.size(); ++i)
       for (int g = 0; g < G; ++g) {
         if (i >= res[g].rows.size()) continue;
         const auto& r = res[g].rows[i];
-        const double io = r.ms_exchange, comp = r.ms_gain + r.ms_panel + r.ms_update;
+        const double io = r.ms_io, comp = r.ms_gain + r.ms_exchange + r.ms_panel + r.ms_update;
         const double ov = io + comp > 0 ? std::max(0.0, 1.0 - r.ms_round / (io + comp)) : 0.0;
         rf << (i + 1) << ',' << g << ',' << io << ',' << comp << ',' << r.ms_round << ',' << ov
            << '\n';
@@ -402,7 +464,7 @@ int run_select(const SelectArgs& a) {
 int usage() {
   std::cerr << "usage: doptsel select <kbf> --budget B [--mode schur|gpu] [--gpus G] [--workers N]\n"
                "                      [--algorithm right|left] [--storage auto|hbm|stream]\n"
-               "                      [--seed S] [--pipeline on|off] [--precision f64]\n"
+               "                      [--hbm-budget BYTES] [--seed S] [--pipeline on|off] [--precision f64]\n"
                "                      [--config cfg | --noise-logdets file] [--kbf-rows] [--out DIR]\n"
                "       doptsel select --synthetic nd,nt,rank,sigma,seed --budget B [...]\n"
                "       doptsel build <config> <out.kbf>      (K assembled on the GPU)\n";
@@ -459,6 +521,7 @@ int main(int argc, char** argv) {
         a.storage = val();
         if (a.storage != "auto" && a.storage != "hbm" && a.storage != "stream") return usage();
       }
+      else if (s == "--hbm-budget") a.hbm_budget = std::stoull(val());
       else if (s == "--out") a.out = val();
       else if (!s.empty() && s[0] == '-') return usage();
       else if (a.kbf.empty()) a.kbf = s;

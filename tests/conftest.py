@@ -13,11 +13,11 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running")
 
 
-def gpu_available() -> bool:
+def gpu_available(count: int = 1) -> bool:
     try:
         import torch
 
-        return torch.cuda.is_available()
+        return torch.cuda.is_available() and torch.cuda.device_count() >= count
     except Exception:
         return False
 

@@ -34,7 +34,24 @@ def test_library_exports_every_declared_symbol():
     exported = set(re.findall(r"\bT (dsel_[a-z0-9_]+)", out))
     missing = [s for s in declared_symbols() if s not in exported]
     assert not missing, missing
-    assert d.lib.dsel_abi_version() == 1
+    assert d.lib.dsel_abi_version() == 2
+
+
+def test_every_allocation_goes_through_the_counted_wrappers():
+    """The zero-allocation check on dsel_step (tests/test_gpu_parity.py) reads
+    dsel_alloc_count(); it covers every device/pinned allocation only if no
+    raw cudaMalloc / cudaMallocHost / cudaHostAlloc / cudaHostRegister call
+    bypasses the counted wrappers (ds_malloc, ds_malloc_host, ds_host_register)."""
+    csrc = os.path.join(ROOT, "paper_2604_08812_b200", "csrc")
+    raw = re.compile(r"\b(cudaMalloc|cudaMallocHost|cudaHostAlloc|cudaHostRegister|cudaMallocAsync|"
+                     r"cudaMallocManaged|cudaMallocPitch)\s*\(")
+    offenders = []
+    for name in sorted(os.listdir(csrc)):
+        lines = open(os.path.join(csrc, name)).read().splitlines()
+        for i, line in enumerate(lines):
+            if raw.search(line) and "return cuda" not in line:  # the wrappers' own calls
+                offenders.append(f"{name}:{i + 1}: {line.strip()}")
+    assert not offenders, offenders
 
 
 def test_library_is_sm100a_and_uses_dmma():

@@ -21,6 +21,18 @@ def test_cpp_dropin_against_reference():
     assert r.returncode == 0, r.stdout + r.stderr
 
 
+@pytest.mark.gpu
+@pytest.mark.skipif(not gpu_available(2), reason="needs 2 GPUs")
+@pytest.mark.skipif(not os.path.exists(BIN), reason="built only where /root/reference exists")
+def test_cpp_peer_failure_aborts_instead_of_hanging():
+    """A rank failing mid-run (DSEL_FAULT) surfaces as one WorkerFailure; its
+    peer, blocked on it in the NVLink exchange / NCCL, is released by
+    dsel_abort (advisor r1: failures used to hang)."""
+    r = subprocess.run([BIN, "--fault"], capture_output=True, text=True, timeout=240)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 def test_dropin_header_compiles_against_reference(tmp_path):
     """Compile-only check here (no GPU): the adapter header builds against the
     reference headers."""

@@ -516,8 +516,11 @@ def test_out_of_memory_is_a_clean_error(dsel):
     """A store that cannot fit in HBM fails at create with DSEL_E_OOM (WorkerFailure),
     frees what it allocated, and the device stays usable."""
     with pytest.raises(dsel.WorkerFailure) as ei:
-        dsel.Engine(4000, 420, 10)          # n = 1.68M: a 22 TB panel store
+        dsel.Engine(4000, 420, 10, storage="hbm")  # n = 1.68M: an 11 TB packed panel store
     assert "OOM" in str(ei.value) or "cudaMalloc" in str(ei.value)
+    with pytest.raises(dsel.WorkerFailure) as ei:  # AUTO: not even the streaming store fits
+        dsel.Engine(4000, 420, 100)                # (W_own 0.58 TB)
+    assert "OOM" in str(ei.value) and "streaming" in str(ei.value)
     with dsel.Engine(8, 2, 2) as eng:       # the device is still usable
         eng.load_k(np.eye(16).reshape(8, 2, 8, 2).transpose(0, 2, 1, 3).copy().reshape(-1) * 2.0)
         eng.run()
