@@ -14,9 +14,14 @@ Workload (BASELINE.json configs[1], the metric's single-GPU config):
   panel broadcast). `--config c3` selects the weak-scaling workload
   (75*N sensors x Nt=420, rank 24,576, budget 50).
 
+`--gpus N` without a launcher re-executes itself under torch.distributed.run
+(one process per GPU, 127.0.0.1), so `python bench.py --gpus 4` measures 4 GPUs.
+
 `--impl reference` times the reference CPU implementation (oracle/_ref, the
-unmodified reference headers compiled from /root/reference) on the host's
-cores over a bounded sample (see cpu_reference()).
+unmodified reference headers compiled from /root/reference): one complete
+run_parallel_greedy selection on all host cores, on K materialized by the
+oracle's bit-exact generator -- nothing of this package is imported on that
+arm (see reference_arm()).
 """
 from __future__ import annotations
 
@@ -39,8 +44,8 @@ CONFIGS = {
 }
 SIGMA, SEED = 1.0, 2024
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
-# FP64 denominators measured on this pool's B200 (profiles/r01_fp64_peak_probe.log):
-# DMMA.8x8x4 issue-bound microbenchmark 37.10 TFLOP/s; cuBLAS DGEMM 16384^3 36.13.
+# Fallback FP64 denominators (profiles/r01_fp64_peak_probe.log) -- every run
+# measures both again on its own devices (measure_fp64_peaks) and reports those.
 FP64_DMMA_PEAK_TFLOPS = 37.10
 FP64_CUBLAS_TFLOPS = 36.13
 
@@ -118,6 +123,47 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------- #
+def respawn_if_needed(args) -> None:
+    """`--gpus N` (N > 1) without a launcher: re-exec under torch.distributed.run,
+    one rank per GPU over 127.0.0.1 (the driver's own launch line)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def measure_fp64_peaks(d, device: int) -> dict:
+    """Roofline denominators measured in this run on this device: the DMMA
+    issue rate (dsel_measure_fp64_peak) and cuBLAS DGEMM 8192^3 (torch)."""
+    import torch
+
+    dmma = max(d.measure_fp64_peak(device) for _ in range(3))
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=f"cuda:{device}")
+    b = torch.randn(n, n, dtype=torch.float64, device=f"cuda:{device}")
+    best = 1e9
+    for i in range(4):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        c = a @ b
+        e1.record()
+        torch.cuda.synchronize()
+        if i:
+            best = min(best, e0.elapsed_time(e1))
+    del a, b, c
+    torch.cuda.empty_cache()
+    return {"dmma_tflops": round(dmma, 2), "cublas_dgemm_tflops": round(2 * n ** 3 / best / 1e9, 2)}
+
+
 def dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -149,6 +195,10 @@ def allreduce_sum(x: float, world: int) -> float:
     return float(t.item())
 
 
+def allreduce_min(x: float, world: int) -> float:
+    return -allreduce_max(-x, world)
+
+
 def allreduce_max(x: float, world: int) -> float:
     if world == 1:
         return x
@@ -170,12 +220,13 @@ def broadcast_bytes(b: bytes | None, world: int) -> bytes:
     return obj[0]
 
 
-def ncu_traffic(profile_dir: str, algorithm: str):
+def ncu_traffic(profile_dir: str, algorithm: str, config: str, world: int):
     """dram bytes per update-kernel launch from a committed `ncu --set full`
-    capture summary (profiles/*update_dram*<algorithm>*.json), else None."""
+    capture of THIS line's configuration (profiles/*update_dram_<algo>_<config>_n<N>.json),
+    else None -- a capture of another shape says nothing about this one."""
     import glob
 
-    pat = "*update_dram_ll*.json" if algorithm == "left" else "*update_dram.json"
+    pat = f"*update_dram_{algorithm}_{config}_n{world}.json"
     for p in sorted(glob.glob(os.path.join(profile_dir, pat)), reverse=True):
         try:
             return json.load(open(p))
@@ -258,8 +309,29 @@ def our_arm(args, world, rank, local):
     t0 = time.time()
     v = d.synthetic_v(nd, nt, vrank, SEED, threads=max(1, (os.cpu_count() or 1) // world))
     t_v = time.time() - t0
+    peaks = measure_fp64_peaks(d, local)
+    peaks_min = {k: allreduce_min(x, world) for k, x in peaks.items()}
     algos = [args.algorithm] + ([] if args.no_variants else
                                 ["left" if args.algorithm == "right" else "right"])
+    want_cpu = rank == 0 and world == 1 and not args.no_cpu
+    mine = [j for j in range(nd) if j % world == rank]
+    host, host_rows, hv = None, None, None
+    if not args.no_e2e or want_cpu:
+        # this rank's block rows of K in pinned host memory: the e2e input. A
+        # full-panel engine forms K once and exports them (the packed store
+        # keeps only the block-lower half)
+        import torch
+
+        row_elems = nd * nt * nt
+        host = torch.empty(len(mine) * row_elems, dtype=torch.float64).pin_memory()
+        hv = host.numpy()
+        nid = broadcast_bytes(d.nccl_unique_id() if (world > 1 and rank == 0) else None, world)
+        with d.Engine(nd, nt, budget, device=local, world_size=world, rank=rank, nccl_id=nid,
+                      packed=False, storage="hbm") as src:
+            src.gen_synthetic(v, vrank, SIGMA)
+            for idx, j in enumerate(mine):
+                hv[idx * row_elems:(idx + 1) * row_elems] = src.read_block_row(j)
+        host_rows = [host[idx * row_elems:(idx + 1) * row_elems] for idx in range(len(mine))]
     engines, t_gen = {}, 0.0
     for a in algos:  # every engine gets the same bit-exact K, then V is released
         nid = broadcast_bytes(d.nccl_unique_id() if (world > 1 and rank == 0) else None, world)
@@ -273,20 +345,6 @@ def our_arm(args, world, rank, local):
            for a in algos}
     if len(algos) > 1 and res[algos[0]]["chosen"] != res[algos[1]]["chosen"]:
         raise RuntimeError("right- and left-looking sequences differ")
-    want_cpu = rank == 0 and world == 1 and not args.no_cpu
-    mine = [j for j in range(nd) if j % world == rank]
-    host_rows = None
-    if not args.no_e2e or want_cpu:
-        import torch
-
-        row_elems = nd * nt * nt
-        host = torch.empty(len(mine) * row_elems, dtype=torch.float64).pin_memory()
-        hv = host.numpy()
-        eng0 = engines[algos[0]]
-        eng0.reset()
-        for idx, j in enumerate(mine):
-            hv[idx * row_elems:(idx + 1) * row_elems] = eng0.read_block_row(j)
-        host_rows = [host[idx * row_elems:(idx + 1) * row_elems] for idx in range(len(mine))]
     for a in algos:
         if args.no_e2e:
             res[a]["e2e"] = None
@@ -318,9 +376,9 @@ def our_arm(args, world, rank, local):
     if want_cpu:
         cpu = cpu_reference(hv, nd, nt, budget, chosen)
 
-    tr = ncu_traffic(os.path.join(ROOT, "profiles"), args.algorithm)
+    tr = ncu_traffic(os.path.join(ROOT, "profiles"), args.algorithm, args.config, world)
     traffic = tr.get("traffic_bytes_per_launch") if tr else None
-    peak = FP64_DMMA_PEAK_TFLOPS
+    peak = peaks_min["dmma_tflops"]
     line = {
         "metric": "time-to-k-sensors (s)",
         "value": round(value, 6),
@@ -335,14 +393,7 @@ def our_arm(args, world, rank, local):
         "dtype": "f64",
         "data": "synthetic: SyntheticKAccess K = sigma^2 I + V V^T (reference RNG stream, "
                 "bit-exact device generator)",
-        "config": {"workload": f"{args.config.upper()}: {nd} candidates x Nt={nt} "
-                               f"(n={nd * nt}) select {budget}, rank {vrank}, sigma {SIGMA}, "
-                               f"seed {SEED}, K resident in HBM",
-                   "n_sensors": nd, "n_steps": nt, "budget": budget, "rank": vrank,
-                   "parallelism": f"candidate-sharded x{world} (cyclic block columns); per round "
-                                  "NCCL allgather of the 32-B argmax records, W rows exchanged over "
-                                  "NVLink peer memory (one fused read+scatter kernel) when x>1",
-                   "l2": f"inputs {nd * nt * nd * nt * 8 / 1e9:.2f} GB >> 126 MB L2 (no flush needed)",
+        "config": {**workload_config(args.config, nd, nt, budget, vrank, world),
                    "chosen_first": chosen[:8]},
         "algorithm": ALGO_DESC[args.algorithm],
         "schur_update": {"flops_per_step_per_rank": tot_flops,
@@ -355,14 +406,18 @@ def our_arm(args, world, rank, local):
         "roofline": {"bound": "tensor", "kernel": "schur_update_ws_kernel (DMMA.8x8x4, TMA bulk)",
                      "achieved": round(upd_tf, 3), "peak": peak, "unit": "TFLOP/s",
                      "frac": round(upd_tf / peak, 4),
-                     "peak_source": "measured FP64 DMMA peak on this pool's B200 "
-                                    "(profiles/r01_fp64_peak_probe.log; cuBLAS DGEMM "
-                                    f"{FP64_CUBLAS_TFLOPS}); MEASURED_PEAKS.json has no FP64 entry",
+                     "peak_source": "measured in this run on these GPUs (min over ranks): "
+                                    "DMMA.8x8x4 issue-rate microbenchmark "
+                                    "(dsel_measure_fp64_peak); MEASURED_PEAKS.json has no FP64 "
+                                    "entry",
+                     "peak_cublas_dgemm": peaks_min["cublas_dgemm_tflops"],
+                     "frac_of_cublas_dgemm": round(upd_tf / peaks_min["cublas_dgemm_tflops"], 4),
                      "traffic": traffic,
                      "traffic_note": (f"dram read+write of one update launch ({tr['launch']}) "
                                       f"from ncu --set full; algorithmic C read+write "
                                       f"{tr['algorithmic_bytes_per_launch']:.4g} B "
-                                      f"(x{tr['traffic_over_algorithmic']})") if tr else None},
+                                      f"(x{tr['traffic_over_algorithmic']})") if tr else
+                                     "no ncu --set full capture of this configuration committed"},
         "e2e": e2e,
         "gpu_launches": int(sum(launches) / len(launches)) if launches else 0,
         "clocks": clocks,
@@ -418,8 +473,18 @@ def cpu_reference(k_host, nd, nt, budget, prefix, iterates=None):
 
 
 def reference_arm(args, world, rank, local):
+    """The reference's own CPU implementation on this box's host cores: the
+    unmodified reference headers (oracle/_ref) run_parallel_greedy<double> --
+    the `doptsel select --mode schur` path (parallel.hpp:281-483) -- with one
+    worker per host thread, on K materialized by the oracle's bit-exact
+    blocked generator (sha256-identical to SyntheticKAccess on C1/C2,
+    tests/test_oracle.py). Nothing of this package is imported here.
+
+    C1/C2: ONE complete selection is timed (time-to-B, measured). C3: a full
+    reference run takes hours, so the first rounds are timed and time-to-B is
+    extrapolated with the Alg. 1 cost model (labelled)."""
     if rank != 0:
-        return
+        return  # one CPU measurement per job; the other ranks exit 0
     import numpy as np
 
     from oracle import oracle as O
@@ -428,41 +493,71 @@ def reference_arm(args, world, rank, local):
         emit({"impl": "reference", "unavailable": "oracle/_ref not built "
                                                   "(needs /root/reference at build time)"})
         return
-    w = workload(args.config, 1)
+    w = workload(args.config, world)
     nd, nt, vrank, budget = w["nd"], w["nt"], w["rank"], w["budget"]
-    # Input K: materialized by the bit-exact device generator (identical bytes to
-    # SyntheticKAccess, tests/test_gpu_parity.py::test_synthetic_generator_bit_exact)
-    # because the reference's own materialization of C2 takes ~5 min on 16 cores.
-    # Only the reference runs inside the timed samples.
-    import paper_2604_08812_b200 as d
-
-    v = d.synthetic_v(nd, nt, vrank, SEED)
-    with d.Engine(nd, nt, budget, device=local) as eng:
-        eng.gen_synthetic(v, vrank, SIGMA)
-        del v
-        k = np.concatenate([eng.read_block_row(j) for j in range(nd)])
-        eng.run()
-        prefix = [r["chosen_index"] for r in eng.trace()]
-    vals = []
-    for it in range(args.warmup + args.steps):
-        its = [1, budget // 4, budget // 2] if it >= args.warmup else [1, 2]
-        cpu = cpu_reference(k, nd, nt, budget, prefix, iterates=its)
-        if it >= args.warmup:
-            vals.append(cpu)
-    value = sum(c["value"] for c in vals) / len(vals)
-    cpu = vals[-1]
-    cpu["value"] = round(value, 3)
+    cores = os.cpu_count() or 1
+    t0 = time.time()
+    k = O.synthetic_k_fast(nd, nt, vrank, SIGMA, SEED, threads=cores)
+    t_k = time.time() - t0
+    full = args.config in ("c1", "c2")
+    if full:
+        tr = O.ref_parallel_greedy(k, nd, nt, budget, workers=cores, seed=0)
+        value = tr.selection_ms / 1e3
+        chosen = tr.chosen
+        sample = (f"one complete reference run_parallel_greedy<double> selection, time-to-"
+                  f"{budget} MEASURED ({cores} workers = host threads, pipelined reader "
+                  f"threads, K in memory as a DataSpaceHessian)")
+        kind_note = "measured"
+        rounds_ms = [round(x, 2) for x in tr.wall_ms]
+    else:
+        r_s = min(budget, 6)
+        tr = O.ref_parallel_greedy(k, nd, nt, r_s, workers=cores, seed=0)
+        ms = np.asarray(tr.wall_ms)
+        its = np.arange(len(ms))
+        A = np.array([[alg1_round_cost(nd, nt, i), nd - i] for i in its], dtype=np.float64)
+        coef, *_ = np.linalg.lstsq(A, ms / 1e3, rcond=None)
+        a_, b_ = max(coef[0], 0.0), max(coef[1], 0.0)
+        value = sum(a_ * alg1_round_cost(nd, nt, i) + b_ * (nd - i) for i in range(budget))
+        chosen = tr.chosen
+        sample = (f"reference run_parallel_greedy<double> first {r_s} rounds timed "
+                  f"({[round(float(x), 1) for x in ms]} ms, {cores} workers); time-to-{budget} "
+                  f"EXTRAPOLATED with the Alg. 1 cost model (a={a_:.3e} s/flop, b={b_:.3e} s/cand)")
+        kind_note = "extrapolated"
+        rounds_ms = [round(float(x), 2) for x in ms]
+    golden = os.path.join(ROOT, "tests", "golden", f"{args.config}.json")
+    match = None
+    if os.path.exists(golden):
+        want = json.load(open(golden))["chosen"]
+        match = want[:len(chosen)] == chosen
+    cpu = {"value": round(value, 3), "unit": "s", "cores": cores, "kind": "reference",
+           "sample": sample, "time": kind_note, "k_materialize_s": round(t_k, 1),
+           "round_ms": rounds_ms}
     line = {"metric": "time-to-k-sensors (s)", "value": round(value, 3), "unit": "s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": world, "steps": 1, "warmup": 0,
+            "steps_requested": args.steps, "warmup_requested": args.warmup,
             "ms_per_step": round(value * 1e3, 1), "higher_is_better": False,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (SyntheticKAccess K, bit-identical)",
-            "config": {"workload": f"{args.config.upper()}: {nd} candidates x Nt={nt} select "
-                                   f"{budget}, rank {vrank} (reference CPU, bounded sample)"},
+            "scaling": "weak" if args.config == "c3" else "strong", "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic: SyntheticKAccess K = sigma^2 I + V V^T (reference RNG stream; "
+                    "materialized by the oracle's bit-exact generator)",
+            "config": {**workload_config(args.config, nd, nt, budget, vrank, world),
+                       "chosen_first": chosen[:8]},
             "impl": "reference", "cpu_baseline": cpu,
+            "sequence_matches_reference_golden": match,
             "e2e": {"value": round(value, 3), "unit": "s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     emit(line)
+
+
+def workload_config(name, nd, nt, budget, vrank, world) -> dict:
+    """The workload keys both arms report (same dict on the reference arm)."""
+    return {"workload": f"{name.upper()}: {nd} candidates x Nt={nt} (n={nd * nt}) select "
+                        f"{budget}, rank {vrank}, sigma {SIGMA}, seed {SEED}",
+            "n_sensors": nd, "n_steps": nt, "budget": budget, "rank": vrank,
+            "parallelism": f"candidate-sharded x{world} (cyclic block columns); per round NCCL "
+                           "allgather of the 32-B argmax records, W rows exchanged over NVLink "
+                           "peer memory (one fused read+scatter kernel) when x>1",
+            "l2": f"inputs {nd * nt * nd * nt * 8 / 1e9:.2f} GB >> 126 MB L2 (no flush needed)"}
 
 
 _STDOUT_FD = None
@@ -492,14 +587,20 @@ def main():
                     help="skip measuring the other algorithm beside the primary")
     args = ap.parse_args()
     global _STDOUT_FD
+    if args.impl != "reference":
+        respawn_if_needed(args)  # before stdout is redirected: the children print the line
     sys.stdout.flush()
     _STDOUT_FD = os.dup(1)
     os.dup2(2, 1)  # C-level writes to stdout (NCCL init banner) go to stderr
-    world, rank, local = dist_init()
     if args.impl == "reference":
-        reference_arm(args, world, rank, local)
-    else:
-        our_arm(args, world, rank, local)
+        # CPU-only: no process group; under a launcher rank 0 alone measures
+        reference_arm(args, int(os.environ.get("WORLD_SIZE", "1")),
+                      int(os.environ.get("RANK", "0")), 0)
+        return
+    world, rank, local = dist_init()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    our_arm(args, world, rank, local)
     if world > 1:
         import torch.distributed as dist
 

@@ -160,6 +160,9 @@ dsel_status dsel_get_plan(const dsel_engine* e, dsel_plan* out);
  * of candidate evaluation (test_selector.cpp:281-298) is that
  * dsel_step / dsel_run never move this counter. */
 uint64_t dsel_alloc_count(void);
+/* Roofline denominator: the FP64 tensor-core (DMMA.8x8x4) issue rate of the
+ * device, measured with a compute-only microbenchmark (~15 ms). */
+dsel_status dsel_measure_fp64_peak(int device, double* tflops);
 
 /* ---- panel store ingest (north-star (1)) -------------------------------- */
 /* Block row j of K: blocks (j, i), i = 0..n_sensors-1, each row-major Nt x Nt

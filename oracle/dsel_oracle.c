@@ -207,6 +207,99 @@ void orc_synthetic_block_rows_fast(const double* v, const double* vt, int n_sens
   }
 }
 
+/* Same bits again, AVX2 register-blocked (4 rows x 8 columns of the block in
+ * ymm accumulators, t chunked so the V / V^T panels stay in L1/L2). Separate
+ * vmulpd + vaddpd per term (no FMA: the target attribute enables AVX2 only,
+ * and -ffp-contract=off forbids contraction), sequential in t per element.
+ * Needs n_steps % 4 == 0 (every BASELINE config); the caller checks the CPU. */
+#if defined(__x86_64__)
+#include <immintrin.h>
+__attribute__((target("avx2"))) void orc_synthetic_block_rows_avx2(
+    const double* v, const double* vt, int n_sensors, int n_steps, int rank, double noise_sigma,
+    int i, double* k) {
+  const double noise2 = noise_sigma * noise_sigma;
+  const size_t n = (size_t)n_sensors * n_steps;
+  const size_t bsz = (size_t)n_steps * n_steps;
+  const int tc = 128, nt = n_steps;
+  for (int j = 0; j <= i; ++j) {
+    double* o = k + ((size_t)i * n_sensors + j) * bsz;
+    for (size_t e = 0; e < bsz; ++e) o[e] = 0.0;
+    for (int t0 = 0; t0 < rank; t0 += tc) {
+      const int t1 = t0 + tc < rank ? t0 + tc : rank;
+      for (int c0 = 0; c0 < nt; c0 += 8) {
+        const int wide = c0 + 8 <= nt;
+        const double* bcol = vt + (size_t)j * nt + c0;
+        for (int r0 = 0; r0 < nt; r0 += 4) {
+          const double* a0 = v + ((size_t)i * nt + r0) * rank;
+          double* orow = o + (size_t)r0 * nt + c0;
+          __m256d acc[4][2];
+          for (int rr = 0; rr < 4; ++rr) {
+            acc[rr][0] = _mm256_loadu_pd(orow + (size_t)rr * nt);
+            acc[rr][1] = wide ? _mm256_loadu_pd(orow + (size_t)rr * nt + 4) : _mm256_setzero_pd();
+          }
+          if (wide) {
+            for (int t = t0; t < t1; ++t) {
+              const __m256d b0 = _mm256_loadu_pd(bcol + (size_t)t * n);
+              const __m256d b1 = _mm256_loadu_pd(bcol + (size_t)t * n + 4);
+              for (int rr = 0; rr < 4; ++rr) {
+                const __m256d at = _mm256_broadcast_sd(a0 + (size_t)rr * rank + t);
+                acc[rr][0] = _mm256_add_pd(acc[rr][0], _mm256_mul_pd(at, b0));
+                acc[rr][1] = _mm256_add_pd(acc[rr][1], _mm256_mul_pd(at, b1));
+              }
+            }
+          } else {
+            for (int t = t0; t < t1; ++t) {
+              const __m256d b0 = _mm256_loadu_pd(bcol + (size_t)t * n);
+              for (int rr = 0; rr < 4; ++rr) {
+                const __m256d at = _mm256_broadcast_sd(a0 + (size_t)rr * rank + t);
+                acc[rr][0] = _mm256_add_pd(acc[rr][0], _mm256_mul_pd(at, b0));
+              }
+            }
+          }
+          for (int rr = 0; rr < 4; ++rr) {
+            _mm256_storeu_pd(orow + (size_t)rr * nt, acc[rr][0]);
+            if (wide) _mm256_storeu_pd(orow + (size_t)rr * nt + 4, acc[rr][1]);
+          }
+        }
+      }
+    }
+    if (i == j)
+      for (int r = 0; r < nt; ++r) o[(size_t)r * nt + r] += noise2;
+    if (j != i) {
+      double* m = k + ((size_t)j * n_sensors + i) * bsz;
+      for (int r = 0; r < nt; ++r)
+        for (int c = 0; c < nt; ++c) m[(size_t)c * nt + r] = o[(size_t)r * nt + c];
+    }
+  }
+}
+#endif
+
+/* V of SyntheticKAccess in two passes for the large fixtures: the uniforms of
+ * every Box-Muller pair are drawn sequentially (mt19937_64 order, with the
+ * u1 <= 0 redraw of rng.hpp:46), then pairs are transformed independently --
+ * the same libm calls on the same arguments as rng_normal, so the same bits.
+ * v must hold an even number of doubles (>= count rounded up). */
+void orc_synthetic_v_uniforms(uint64_t seed, double* v, int64_t count) {
+  orc_rng r;
+  mt_seed(&r, seed);
+  for (int64_t p = 0; 2 * p < count; ++p) {
+    double u1 = rng_uniform(&r);
+    const double u2 = rng_uniform(&r);
+    while (u1 <= 0.0) u1 = rng_uniform(&r);
+    v[2 * p] = u1;
+    v[2 * p + 1] = u2;
+  }
+}
+
+void orc_box_muller_pairs(double* v, int64_t p0, int64_t p1) {
+  for (int64_t p = p0; p < p1; ++p) {
+    const double rad = sqrt(-2.0 * log(v[2 * p]));
+    const double a = 2.0 * 3.141592653589793 * v[2 * p + 1];
+    v[2 * p] = rad * cos(a);
+    v[2 * p + 1] = rad * sin(a);
+  }
+}
+
 /* proj/tests/support/generators.hpp:19-40 random_hessian. */
 void orc_random_hessian(int n_sensors, int n_steps, double gamma, int rank, uint64_t seed,
                         double* k) {

@@ -54,6 +54,9 @@ def lib():
                                                      C.c_int, C.c_int, _dp]
         L.orc_synthetic_block_rows_fast.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_int,
                                                     C.c_double, C.c_int, _dp]
+        L.orc_synthetic_block_rows_avx2.argtypes = L.orc_synthetic_block_rows_fast.argtypes
+        L.orc_synthetic_v_uniforms.argtypes = [C.c_uint64, _dp, C.c_int64]
+        L.orc_box_muller_pairs.argtypes = [_dp, C.c_int64, C.c_int64]
         L.orc_random_hessian.argtypes = [C.c_int, C.c_int, C.c_double, C.c_int, C.c_uint64, _dp]
         L.orc_cholesky_in_place.argtypes = [_dp, C.c_int, C.c_int]
         L.orc_cholesky_in_place.restype = C.c_int
@@ -136,23 +139,51 @@ def synthetic_k(nd: int, nt: int, rank: int, sigma: float, seed: int,
     return k
 
 
-def synthetic_k_fast(nd: int, nt: int, rank: int, sigma: float, seed: int,
-                     threads: int | None = None) -> np.ndarray:
-    """synthetic_k, bit for bit, by the blocked/vectorized loop nest
-    (orc_synthetic_block_rows_fast); for the large golden fixtures."""
+def _cpu_has_avx2() -> bool:
+    try:
+        return " avx2" in open("/proc/cpuinfo").read()
+    except OSError:
+        return False
+
+
+def synthetic_v_parallel(nd: int, nt: int, rank: int, seed: int,
+                         threads: int | None = None) -> np.ndarray:
+    """synthetic_v, bit for bit: uniforms drawn sequentially, the Box-Muller
+    transform of the pairs split over threads (orc_box_muller_pairs)."""
     import concurrent.futures as cf
 
-    v = synthetic_v(nd, nt, rank, seed)
-    vt = np.ascontiguousarray(v.T)
-    v = np.ascontiguousarray(v.reshape(-1))
-    vt = vt.reshape(-1)
-    k = np.empty(nd * nd * nt * nt, dtype=np.float64)
-    threads = threads or os.cpu_count() or 1
+    count = nd * nt * rank
+    buf = np.empty(count + (count & 1), dtype=np.float64)
     L = lib()
+    L.orc_synthetic_v_uniforms(seed, buf, count)
+    pairs = len(buf) // 2
+    threads = threads or os.cpu_count() or 1
+    bounds = np.linspace(0, pairs, threads + 1).astype(np.int64)
+    with cf.ThreadPoolExecutor(threads) as ex:
+        list(ex.map(lambda t: L.orc_box_muller_pairs(buf, int(bounds[t]), int(bounds[t + 1])),
+                    range(threads)))
+    return buf[:count].reshape(nd * nt, rank)
+
+
+def synthetic_k_fast(nd: int, nt: int, rank: int, sigma: float, seed: int,
+                     threads: int | None = None) -> np.ndarray:
+    """synthetic_k, bit for bit, by the blocked/vectorized loop nests
+    (orc_synthetic_block_rows_avx2 when the CPU has AVX2 and nt % 4 == 0, else
+    orc_synthetic_block_rows_fast); for the large golden fixtures and the
+    reference arm's input. Block-row-major (DataSpaceHessian) layout."""
+    import concurrent.futures as cf
+
+    threads = threads or os.cpu_count() or 1
+    v = synthetic_v_parallel(nd, nt, rank, seed, threads)
+    vt = np.ascontiguousarray(v.T).reshape(-1)
+    v = np.ascontiguousarray(v.reshape(-1))
+    k = np.empty(nd * nd * nt * nt, dtype=np.float64)
+    L = lib()
+    fn = (L.orc_synthetic_block_rows_avx2 if nt % 4 == 0 and _cpu_has_avx2()
+          else L.orc_synthetic_block_rows_fast)
     # heavy rows (large i) first so the pool drains evenly
     with cf.ThreadPoolExecutor(threads) as ex:
-        list(ex.map(lambda i: L.orc_synthetic_block_rows_fast(v, vt, nd, nt, rank, sigma, i, k),
-                    range(nd - 1, -1, -1)))
+        list(ex.map(lambda i: fn(v, vt, nd, nt, rank, sigma, i, k), range(nd - 1, -1, -1)))
     return k
 
 

@@ -1893,6 +1893,25 @@ void load_panel(dsel_engine* e, int j, const double* host, bool as_column) {
                        cudaMemcpyDeviceToDevice, e->s));
 }
 
+// Roofline denominator probe: DMMA.8x8x4 issue rate with independent
+// accumulator chains (no memory traffic), 2 CTAs x 512 threads per SM.
+__global__ void __launch_bounds__(512) fp64_peak_kernel(double* out, int iters, double a, double b) {
+  double acc[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    acc[i][0] = threadIdx.x;
+    acc[i][1] = i;
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dmma884(acc[i], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += acc[i][0] + acc[i][1];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 }  // namespace
 
 // ========================================================================== //
@@ -1961,6 +1980,33 @@ const char* dsel_last_error(const dsel_engine* e) {
 uint64_t dsel_device_bytes(const dsel_engine* e) { return e ? e->dev_bytes : 0; }
 
 uint64_t dsel_alloc_count(void) { return g_allocs.load(); }
+
+dsel_status dsel_measure_fp64_peak(int device, double* tflops) {
+  return guard(nullptr, [&] {
+    if (!tflops) throw Fail{DSEL_E_INVALID, "null output"};
+    CU(cudaSetDevice(device));
+    int sms = 0;
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    const int threads = 512, blocks = 2 * sms, iters = 20000;
+    DevScratch<double> out((size_t)threads * blocks);
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    fp64_peak_kernel<<<blocks, threads>>>(out.p, 200, 1.0, 1e-9);  // warm
+    CU(cudaEventRecord(e0));
+    fp64_peak_kernel<<<blocks, threads>>>(out.p, iters, 1.0, 1e-9);
+    CU(cudaEventRecord(e1));
+    CU(cudaEventSynchronize(e1));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    CU(cudaGetLastError());
+    // 8 chains x (8x8x4 MMA = 2*256 flop) per warp per iteration
+    const double flops = 2.0 * 256 * 8 * (double)iters * (threads / 32) * blocks;
+    *tflops = flops / (ms * 1e-3) / 1e12;
+  });
+}
 
 dsel_status dsel_get_plan(const dsel_engine* e, dsel_plan* out) {
   if (!e || !out) return DSEL_E_INVALID;

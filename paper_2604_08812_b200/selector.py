@@ -79,6 +79,13 @@ def _host_ptr(a):
     return C.c_void_p(a.data_ptr())
 
 
+def measure_fp64_peak(device: int = 0) -> float:
+    """FP64 tensor-core (DMMA) peak of the device in TFLOP/s, measured now."""
+    out = C.c_double(0.0)
+    _check(lib.dsel_measure_fp64_peak(device, C.byref(out)))
+    return out.value
+
+
 def alloc_count() -> int:
     """Device/pinned allocations made by libdsel so far (all engines)."""
     return int(lib.dsel_alloc_count())
