@@ -187,3 +187,30 @@ def test_c3mini_golden_is_reference_output(golden_dir):
         row = g["replay_gains"][rnd]
         best = max((x, -j) for j, x in enumerate(row) if x is not None)
         assert -best[1] == s and best[0] == g["gains"][rnd]
+
+
+def test_fast_generators_bit_identical(golden_dir, c1_k):
+    """The blocked generators that materialize the large fixtures and the
+    reference arm's K (synthetic_k_fast: AVX2 4x8 register tiles or the
+    portable blocked loop; synthetic_v_parallel) reproduce SyntheticKAccess
+    bit for bit -- including ragged widths (nt % 8 == 4) and odd nt."""
+    k = O.synthetic_k_fast(64, 32, 2048, 1.0, 2024, threads=4)
+    assert np.array_equal(k.view(np.uint64), c1_k.view(np.uint64))
+    for (nd, nt, rank, seed) in [(5, 12, 301, 3), (4, 20, 77, 9), (3, 7, 50, 1)]:
+        a = O.synthetic_k(nd, nt, rank, 1.0, seed)
+        b = O.synthetic_k_fast(nd, nt, rank, 1.0, seed, threads=3)
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), (nd, nt)
+    v1 = O.synthetic_v(6, 5, 33, 2024)  # odd count: the last pair's sine is dropped
+    v2 = O.synthetic_v_parallel(6, 5, 33, 2024, threads=4)
+    assert np.array_equal(v1.view(np.uint64), v2.view(np.uint64))
+
+
+def test_edge_golden_is_reference_output(golden_dir):
+    """tests/golden/edge.json: exact ties go to the lower index, exact zero
+    pivots are infeasible, the run ends with a partial selection -- as the
+    reference produced it (and the C restatement agrees)."""
+    for c in json.load(open(os.path.join(golden_dir, "edge.json")))["cases"]:
+        k = np.array(c["k_raw"])
+        t = O.greedy_select(k, c["n_sensors"], c["n_steps"], c["budget"])
+        assert t.chosen == c["chosen"] and t.gains == c["gains"], c["name"]
+        assert t.n_infeasible[:len(c["chosen"])] == c["n_infeasible"], c["name"]
