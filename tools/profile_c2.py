@@ -16,10 +16,12 @@ ap.add_argument("--budget", type=int, default=50)
 ap.add_argument("--runs", type=int, default=2)
 ap.add_argument("--algorithm", default="right")
 ap.add_argument("--full-square", action="store_true")
+ap.add_argument("--full-panels", action="store_true", help="full-height panels (no packing)")
 args = ap.parse_args()
 v = d.synthetic_v(args.nd, args.nt, args.rank, 2024)
 eng = d.Engine(args.nd, args.nt, args.budget, keep_pristine=True, export_factor=True,
-               algorithm=args.algorithm, full_square=args.full_square)
+               algorithm=args.algorithm, full_square=args.full_square,
+               packed=not args.full_panels)
 eng.gen_synthetic(v, args.rank, 1.0)
 for r in range(args.runs):
     eng.reset()
