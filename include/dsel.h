@@ -160,6 +160,16 @@ dsel_status dsel_get_plan(const dsel_engine* e, dsel_plan* out);
  * of candidate evaluation (test_selector.cpp:281-298) is that
  * dsel_step / dsel_run never move this counter. */
 uint64_t dsel_alloc_count(void);
+/* Batched log-det of independent SPD matrices already in device memory --
+ * the refactorizing baseline's per-candidate potrf (naive_select,
+ * selector.hpp:253-357) on this library's gain kernel (batched Cholesky,
+ * warp-level pivots, DMMA panel updates). mats: batch column-major m x m
+ * matrices, matrix b at mats + b*stride (device pointer, stride >= m*m);
+ * logdet[b] (device) = 2 sum log diag L, -inf when a pivot is <= 0 or not
+ * finite (status[b] = that pivot, -1 = positive definite). m <= 2800.
+ * Synchronous; allocates its scratch (not a selection-round entry point). */
+dsel_status dsel_batched_logdet(int device, const double* mats, int m, int64_t stride, int batch,
+                                double* logdet, int* status);
 /* Roofline denominator: the FP64 tensor-core (DMMA.8x8x4) issue rate of the
  * device, measured with a compute-only microbenchmark (~15 ms). */
 dsel_status dsel_measure_fp64_peak(int device, double* tflops);

@@ -8,8 +8,8 @@ from .selector import (CorruptFile, DselError, Engine, IoError, GpuOptions, Inde
                        LtiProblem,
                        InfeasibleRound, InvalidConfig, ParallelRunReport, SelectionState,
                        SelectionTrace, TraceRow, WorkerFailure, gpu_greedy_select,
-                       alloc_count, fold_records, measure_fp64_peak, nccl_unique_id, synthetic_v)
+                       alloc_count, batched_logdet, fold_records, measure_fp64_peak, nccl_unique_id, synthetic_v)
 
-__all__ = ["Engine", "LtiProblem", "GpuOptions", "gpu_greedy_select", "synthetic_v", "nccl_unique_id", "fold_records", "alloc_count", "measure_fp64_peak",
+__all__ = ["Engine", "LtiProblem", "GpuOptions", "gpu_greedy_select", "synthetic_v", "nccl_unique_id", "fold_records", "alloc_count", "batched_logdet", "measure_fp64_peak",
            "DselError", "IoError", "CorruptFile", "InvalidConfig", "IndexOutOfRange", "InfeasibleRound", "WorkerFailure",
            "SelectionState", "SelectionTrace", "ParallelRunReport", "TraceRow", "LIB_PATH"]

@@ -419,6 +419,7 @@ struct GainTabs {
 
 // panel width of the gain kernel: two NB x mp panels must fit in 227 KB
 int chol_nb(int nt) { return nt <= 436 ? 32 : 8; }
+constexpr int kBatchedLogdetMaxDim = 2800;  // NB = 8 panel + pivots within 227 KB
 
 // smem pitch of the gain kernel panels: >= nt rounded to 8, == 4 or 12 mod 16
 // so the DMMA fragment loads are bank-conflict free
@@ -1980,6 +1981,58 @@ const char* dsel_last_error(const dsel_engine* e) {
 uint64_t dsel_device_bytes(const dsel_engine* e) { return e ? e->dev_bytes : 0; }
 
 uint64_t dsel_alloc_count(void) { return g_allocs.load(); }
+
+// Batched log-det of independent SPD matrices on the device: the gain kernel
+// (batched Cholesky, warp-level pivots, DMMA panel updates) over arbitrary
+// matrices -- the refactorizing baseline's potrf (selector.hpp:253-357).
+namespace {
+__global__ void batch_tables_kernel(int batch, long long stride, int m, long long* off, long long* ld,
+                                    int* sensor) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  off[b] = (long long)b * stride;
+  ld[b] = m;
+  sensor[b] = b;
+}
+}  // namespace
+
+dsel_status dsel_batched_logdet(int device, const double* mats, int m, int64_t stride, int batch,
+                                double* logdet, int* status) {
+  return guard(nullptr, [&] {
+    if (!mats || !logdet || !status || m < 1 || batch < 0 || stride < (int64_t)m * m)
+      throw Fail{DSEL_E_INVALID, "batched_logdet: bad arguments"};
+    if (m > kBatchedLogdetMaxDim)
+      throw Fail{DSEL_E_INVALID, "batched_logdet: m > " + std::to_string(kBatchedLogdetMaxDim)};
+    if (batch == 0) return;
+    CU(cudaSetDevice(device));
+    int sms = 148, optin = 0;
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    set_smem_limits(device);
+    DevScratch<double> L((size_t)batch * m * m);
+    DevScratch<long long> tabs((size_t)2 * batch);
+    DevScratch<int> sens((size_t)batch);
+    batch_tables_kernel<<<(batch + 127) / 128, 128>>>(batch, stride, m, tabs.p, tabs.p + batch, sens.p);
+    CU(cudaGetLastError());
+    CholArgs a{};
+    a.src = mats;
+    a.src_off = tabs.p;
+    a.src_ld = tabs.p + batch;
+    a.L = L.p;
+    a.l_stride = (long long)m * m;
+    a.gain = logdet;
+    a.status = status;
+    a.nt = m;
+    a.n = batch;
+    a.mp = chol_mp(m);
+    a.sensor = sens.p;
+    a.rec = nullptr;
+    a.counter = nullptr;
+    launch_chol(a, batch, nullptr, sms);
+    CU(cudaGetLastError());
+    CU(cudaDeviceSynchronize());
+  });
+}
 
 dsel_status dsel_measure_fp64_peak(int device, double* tflops) {
   return guard(nullptr, [&] {

@@ -86,6 +86,26 @@ def measure_fp64_peak(device: int = 0) -> float:
     return out.value
 
 
+def batched_logdet(mats, logdet=None, status=None):
+    """log det of a batch of SPD matrices on the GPU (dsel_batched_logdet).
+    mats: a CUDA float64 torch tensor (batch, m, m); symmetric, so row- and
+    column-major agree. Returns (logdet, status) tensors; logdet = -inf and
+    status = failing pivot for a matrix that is not positive definite."""
+    import torch
+
+    if mats.dtype != torch.float64 or not mats.is_cuda or mats.dim() != 3:
+        raise InvalidConfig(1, "batched_logdet needs a (batch, m, m) float64 CUDA tensor")
+    mats = mats.contiguous()
+    b, m, _ = mats.shape
+    if logdet is None:
+        logdet = torch.empty(b, dtype=torch.float64, device=mats.device)
+    if status is None:
+        status = torch.empty(b, dtype=torch.int32, device=mats.device)
+    _check(lib.dsel_batched_logdet(mats.device.index or 0, C.c_void_p(mats.data_ptr()), m, m * m, b,
+                                   C.c_void_p(logdet.data_ptr()), C.c_void_p(status.data_ptr())))
+    return logdet, status
+
+
 def alloc_count() -> int:
     """Device/pinned allocations made by libdsel so far (all engines)."""
     return int(lib.dsel_alloc_count())

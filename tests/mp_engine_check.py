@@ -145,6 +145,31 @@ eng.run()
 rows = eng.trace()
 L = eng.export_factor(len(rows))
 eng.close()
+
+
+def single_gpu_rows():
+    """The same selection on one GPU (world_size 1): the reference asserts
+    worker-count invariance (test_parallel.cpp:109-124, acceptance.cpp:219-252);
+    here every gain must be BIT-identical across GPU counts."""
+    if which == "wave":
+        e1 = d.Engine(32, 16, 12, device=local)
+        e1.load_kbf(os.path.join(ROOT, "tests", "golden", "wave.kbf"))
+    else:
+        e1 = d.Engine(nd, nt, b, device=local)
+        e1.gen_synthetic(v, rk, gold["sigma"])
+    with e1:
+        e1.run()
+        return e1.trace()
+
+
+invariant = True
+if rank == 0:
+    one = single_gpu_rows()
+    invariant = ([(r["chosen_index"], r["gain"], r["objective"]) for r in one] ==
+                 [(r["chosen_index"], r["gain"], r["objective"]) for r in rows])
+inv = [invariant]
+dist.broadcast_object_list(inv, src=0)
+invariant = inv[0]
 chosen = [r["chosen_index"] for r in rows]
 ok = chosen == gold["chosen"]
 for r, g in zip(rows, gold["gains"]):
@@ -159,6 +184,7 @@ allf = [torch.zeros_like(fsum) for _ in range(world)]
 dist.all_gather(allf, fsum)
 same = same and all(torch.equal(allf[0], x) for x in allf)
 print(f"rank {rank}/{world} {which}: sequence {'OK' if ok else 'MISMATCH'} ranks-agree {same} "
+      f"gains bit-identical to 1 GPU {invariant} "
       f"bytes_exchanged(r1)={rows[0]['bytes_exchanged']}", flush=True)
 dist.destroy_process_group()
-sys.exit(0 if (ok and same) else 1)
+sys.exit(0 if (ok and same and invariant) else 1)

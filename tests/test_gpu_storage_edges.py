@@ -236,3 +236,24 @@ def test_baseline_sizes_against_reference_golden(dsel, golden_dir, name, kw):
         assert gain_close(r["gain"], g["gains"][i]), (i, r["gain"], g["gains"][i])
         assert gain_close(r["objective"], g["objectives"][i])
         assert r["n_evaluated"] == g["n_evaluated"][i]
+
+
+def test_batched_logdet_against_numpy(dsel):
+    """dsel_batched_logdet (the refactorizing baseline's potrf on this
+    library's gain kernel): log-dets within 1e-9 of LAPACK
+    for m from 3 to 2000; a zero row/column is infeasible at exactly that
+    pivot, like cholesky_in_place (linalg.hpp:16-35)."""
+    import torch
+
+    rng = np.random.default_rng(5)
+    for m in (3, 40, 128, 420, 1100, 2000):
+        a = rng.standard_normal((3, m, m + 7)) / np.sqrt(m)
+        mats = a @ a.transpose(0, 2, 1) + np.eye(m)
+        mats[2, m // 2, :] = 0.0
+        mats[2, :, m // 2] = 0.0
+        ld, st = dsel.batched_logdet(torch.tensor(mats, device="cuda"))
+        ld, st = ld.cpu().numpy(), st.cpu().numpy()
+        for b in (0, 1):
+            want = np.linalg.slogdet(mats[b])[1]
+            assert st[b] == -1 and abs(ld[b] - want) <= 1e-9 * max(abs(want), 1.0), (m, b, ld[b], want)
+        assert st[2] == m // 2 and ld[2] == -np.inf, (m, st[2], ld[2])

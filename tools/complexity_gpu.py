@@ -8,17 +8,23 @@ from scratch, O(k^3 Nt^3) per candidate; `doptsel bench complexity`
 the iterate k grows -- the paper's Fig. 2.
 
 On the GPU, as a baseline beside the engine:
-  naive_select_gpu  the refactorizing greedy selection, batched over candidates
-                    (torch.linalg.cholesky_ex = cuSOLVER potrf: a library
-                    baseline, not the product path), same tie rule;
-  sweep             per-candidate time vs k for (1) refactorizing, (2) the
-                    reference's left-looking Schur scoring (batched triangular
-                    solve + Cholesky), (3) this engine's right-looking round
-                    (libdsel: gains + update of the remaining candidates) per
-                    remaining candidate, with log-log slopes over the top decade
-                    (fit_loglog_slopes, bench.hpp:180-205).
+  naive_select_gpu  the refactorizing greedy selection, batched over candidates:
+                    every augmented matrix is factored from scratch by this
+                    library's batched Cholesky log-det (dsel_batched_logdet --
+                    the gain kernel: warp-level pivots, DMMA panel updates);
+                    torch only gathers the augmented matrices. Same tie rule;
+  sweep             per-candidate time vs k for (1) refactorizing (the same
+                    kernel), (2) the reference's left-looking Schur scoring
+                    emulated with torch (triangular solve + Cholesky: the
+                    reference formulation, not this engine), (3) this engine's
+                    right-looking round (libdsel: gains + update of the
+                    remaining candidates) per remaining candidate, with log-log
+                    slopes over the top decade (fit_loglog_slopes,
+                    bench.hpp:180-205). The reference default k_max = 100 at
+                    Nt = 32 needs 3232-wide factorizations; the batched kernel
+                    stops at 2800, so the GPU sweep caps k at 2800/Nt - 1 (86).
 
-    python tools/complexity_gpu.py --nt 32 --kmax 100 --step 5 [--out complexity.csv]
+    python tools/complexity_gpu.py --nt 32 --kmax 85 --step 5 [--out complexity.csv]
 """
 from __future__ import annotations
 
@@ -47,6 +53,8 @@ def naive_select_gpu(k_blocks: np.ndarray, nd: int, nt: int, budget: int, candid
                      chunk: int = 64, device: str = "cuda"):
     """Refactorizing greedy selection (naive_select, selector.hpp:253-348) on the GPU.
     Returns (chosen, gains, objectives); gains are raw log-det increments."""
+    import paper_2604_08812_b200 as d
+
     kd = torch.as_tensor(_dense(k_blocks, nd, nt), dtype=torch.float64, device=device)
     remaining = list(range(nd)) if candidates is None else list(candidates)
     chosen, gains, objs = [], [], []
@@ -57,9 +65,9 @@ def naive_select_gpu(k_blocks: np.ndarray, nd: int, nt: int, budget: int, candid
             cs = remaining[c0:c0 + chunk]
             idx = torch.stack([_idx(chosen + [s], nt, device) for s in cs])   # (b, dim)
             m = kd[idx[:, :, None], idx[:, None, :]]                          # (b, dim, dim)
-            lf, info = torch.linalg.cholesky_ex(m)
-            ld = 2.0 * torch.log(torch.diagonal(lf, dim1=1, dim2=2)).sum(dim=1) - logdet_prev
-            ld = torch.where(info == 0, ld, torch.full_like(ld, -math.inf)).cpu().numpy()
+            lds, status = d.batched_logdet(m)   # refactorized from scratch, this library's kernel
+            ld = lds - logdet_prev
+            ld = torch.where(status < 0, ld, torch.full_like(ld, -math.inf)).cpu().numpy()
             for s, d in zip(cs, ld):   # better_candidate (selector.hpp:132-134)
                 if d == -math.inf:
                     continue
@@ -108,6 +116,7 @@ def sweep(nt=32, k_max=100, step=5, reps=5, seed=2024, batch=32):
     nt, rank=nt, sigma=1, seed), chosen = 0..k-1, candidate k."""
     import paper_2604_08812_b200 as d
 
+    k_max = min(k_max, 2800 // nt - 1)  # dsel_batched_logdet handles m <= 2800
     nd = k_max + 1
     v = d.synthetic_v(nd, nt, nt, seed)
     with d.Engine(nd, nt, nd, keep_pristine=True) as eng:
@@ -121,8 +130,7 @@ def sweep(nt=32, k_max=100, step=5, reps=5, seed=2024, batch=32):
             m = kd[:dim, :dim].expand(batch, dim, dim).contiguous()
 
             def naive():
-                lf, _ = torch.linalg.cholesky_ex(m)
-                return torch.log(torch.diagonal(lf, dim1=1, dim2=2)).sum(dim=1)
+                return d.batched_logdet(m)[0]
 
             ls = torch.linalg.cholesky(kd[:kdim, :kdim])
             col = kd[:kdim, kdim:dim].expand(batch, kdim, nt).contiguous()
@@ -155,7 +163,7 @@ def sweep(nt=32, k_max=100, step=5, reps=5, seed=2024, batch=32):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--nt", type=int, default=32)
-    ap.add_argument("--kmax", type=int, default=100)
+    ap.add_argument("--kmax", type=int, default=85)
     ap.add_argument("--step", type=int, default=5)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--batch", type=int, default=32, help="candidates per batched launch")
