@@ -241,6 +241,15 @@ dsel_status dsel_assemble_lti(dsel_engine* e, const dsel_lti* problem, double* n
  * reference reads); 0 reads contiguous block rows and relies on symmetry
  * (write_kbf guarantees |K - K^T| <= 1e-10). threads = pread threads (0 = auto). */
 dsel_status dsel_load_kbf(dsel_engine* e, const char* path, int exact_columns, int threads);
+/* File-backed streaming store (storage = DSEL_STORAGE_STREAM): the KBF file is
+ * validated like KStoreReader (E_CORRUPT / E_IO) and kept open; each round
+ * reads only the chosen column's true blocks (s_q, s_k) of this rank's
+ * candidates -- what read_test_column reads through KStoreReader::read_block
+ * (kaccess.hpp:27-35, kstore.hpp:141-158) -- with `threads` parallel preads
+ * into a pinned buffer while the round's column GEMM runs, then H2D on the copy
+ * stream. K is never held whole in host or device memory (beyond the page
+ * cache). threads = 0: auto. */
+dsel_status dsel_attach_kbf(dsel_engine* e, const char* path, int threads);
 /* Export block row j (same layout as dsel_load_block_row) of the CURRENT
  * conditional covariance (= K before the first step); owner rank only. */
 dsel_status dsel_read_block_row(dsel_engine* e, int j, double* host_row);

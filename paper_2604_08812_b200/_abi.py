@@ -19,7 +19,7 @@ STATUS_NAMES = {0: "DSEL_OK", 1: "DSEL_E_INVALID", 2: "DSEL_E_RANGE", 3: "DSEL_E
 # every entry point declared in include/dsel.h (tests check the exports)
 EXPORTS = ["dsel_abi_version", "dsel_fold_records", "dsel_nccl_unique_id", "dsel_create", "dsel_destroy",
            "dsel_last_error", "dsel_sync", "dsel_connect", "dsel_abort", "dsel_device_bytes", "dsel_get_plan", "dsel_alloc_count", "dsel_measure_fp64_peak", "dsel_batched_logdet", "dsel_load_block_row",
-           "dsel_load_block_col", "dsel_load_k", "dsel_attach_host_k", "dsel_attach_host_rows", "dsel_load_kbf", "dsel_read_block_row", "dsel_synthetic_v",
+           "dsel_load_block_col", "dsel_load_k", "dsel_attach_host_k", "dsel_attach_host_rows", "dsel_load_kbf", "dsel_attach_kbf", "dsel_read_block_row", "dsel_synthetic_v",
            "dsel_gen_synthetic", "dsel_gen_synthetic_device", "dsel_lti_from_config", "dsel_lti_free",
            "dsel_assemble_lti", "dsel_step", "dsel_step_forced", "dsel_run", "dsel_peek_gains",
            "dsel_get_trace", "dsel_reset", "dsel_get_stats", "dsel_export_factor",
@@ -117,6 +117,7 @@ def _load():
     L.dsel_lti_free.restype = None
     L.dsel_assemble_lti.argtypes = [vp, C.POINTER(DselLti), vp]
     L.dsel_load_kbf.argtypes = [vp, C.c_char_p, C.c_int, C.c_int]
+    L.dsel_attach_kbf.argtypes = [vp, C.c_char_p, C.c_int]
     L.dsel_read_block_row.argtypes = [vp, C.c_int, vp]
     L.dsel_synthetic_v.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, vp, C.c_int]
     L.dsel_gen_synthetic.argtypes = [vp, vp, C.c_int, C.c_double]

@@ -171,6 +171,19 @@ struct dsel_engine {
   // k's blocks are copied into Kk on the copy stream, overlapped with the GEMM
   bool stream = false;
   double *hstore = nullptr, *Kk = nullptr;
+  // world_size 1: the host store keeps only the block-lower half of K --
+  // hstore panel p = blocks K(q, p) for q >= p, row-major, back to back; a
+  // round reads panel p contiguously plus block (p, q) of every earlier panel
+  // q (K(q, p) transposed). Half the host memory, so K up to twice the host
+  // RAM it would otherwise need (a K larger than HBM fits a 1-GPU host)
+  bool hpacked = false;
+  // file-backed store (dsel_attach_kbf): per round the chosen column's own
+  // blocks are pread from the KBF file into a pinned staging buffer while the
+  // column GEMM runs, then copied H2D (KStoreReader::read_block, kstore.hpp:141-158)
+  int kbf_fd = -1;
+  std::string kbf_path;
+  int kbf_threads = 0;
+  double* h_kstage = nullptr;
   // dsel_attach_host_k: the caller's block-row-major K in (pinned) host
   // memory is the store; blocks are read in place, only those a round needs
   const double* hk_user = nullptr;
@@ -285,6 +298,41 @@ struct dsel_engine {
 };
 
 namespace {
+
+void pread_exact(int fd, void* dst, size_t bytes, off_t off, const std::string& path) {
+  unsigned char* p = static_cast<unsigned char*>(dst);
+  size_t done = 0;
+  while (done < bytes) {
+    const ssize_t got = ::pread(fd, p + done, bytes - done, off + (off_t)done);
+    if (got < 0) {
+      if (errno == EINTR) continue;
+      throw Fail{DSEL_E_IO, path + ": pread failed: " + std::strerror(errno)};
+    }
+    if (got == 0) throw Fail{DSEL_E_CORRUPT, path + ": unexpected end of file"};
+    done += (size_t)got;
+  }
+}
+
+// Host store geometry (streaming). Full (world_size > 1): hstore[pk][own q] =
+// K(own q, k), nc * nloc blocks. Packed (world_size 1): panel pk holds K(q, pk)
+// for q >= pk, nc (nc + 1) / 2 blocks.
+size_t hstore_blocks(const dsel_engine* e) {
+  return e->hpacked ? (size_t)e->nc * (e->nc + 1) / 2 : (size_t)e->nc * std::max(e->nloc, 1);
+}
+size_t hpanel_off(const dsel_engine* e, int pk) {  // blocks before packed panel pk
+  return (size_t)pk * e->nc - (size_t)pk * (pk - 1) / 2;
+}
+double* hpacked_block(const dsel_engine* e, int pk, int q) {  // K(q, pk), q >= pk, row-major
+  return e->hstore + (hpanel_off(e, pk) + (q - pk)) * (size_t)e->nt * e->nt;
+}
+
+void detach_kbf(dsel_engine* e) {
+  if (e->kbf_fd >= 0) ::close(e->kbf_fd);
+  e->kbf_fd = -1;
+  e->kbf_path.clear();
+  if (e->h_kstage) cudaFreeHost(e->h_kstage);
+  e->h_kstage = nullptr;
+}
 
 void build_tables(dsel_engine* e, bool upload = true) {
   // compact global live list (ascending position) and local live list
@@ -781,6 +829,71 @@ void h2d_blocks(dsel_engine* e, double* dst, Src src, cudaStream_t st) {
   }
 }
 
+// Own blocks (row slot q, column sensor kcol(q)) of the KBF file into the pinned
+// staging buffer, Kstage[q] = block (rowsens(q), kcol(q)) row-major: parallel
+// pread (KStoreReader::read_block, kstore.hpp:141-158), one block per call.
+template <class RowS, class ColS>
+void kbf_read_blocks(dsel_engine* e, RowS rowsens, ColS colsens) {
+  const size_t bsz = sizeof(double) * e->nt * e->nt;
+  const int threads = std::max(1, std::min(e->kbf_threads, e->nloc));
+  std::vector<std::thread> pool;
+  std::vector<std::string> errs(threads);
+  std::vector<int> codes(threads, 0);
+  for (int w = 0; w < threads; ++w)
+    pool.emplace_back([&, w] {
+      try {
+        for (int qq = w; qq < e->nloc; qq += threads)
+          pread_exact(e->kbf_fd, reinterpret_cast<unsigned char*>(e->h_kstage) + (size_t)qq * bsz, bsz,
+                      (off_t)(32 + ((size_t)rowsens(qq) * e->nd + colsens(qq)) * bsz), e->kbf_path);
+      } catch (const Fail& f) {
+        codes[w] = f.st;
+        errs[w] = f.msg;
+      }
+    });
+  for (auto& t : pool) t.join();
+  for (int w = 0; w < threads; ++w)
+    if (codes[w]) throw Fail{(dsel_status)codes[w], errs[w]};
+}
+
+// The chosen column's blocks K(own q, k) for this round (north star (1)) into
+// Kk on the copy stream, ordered after this round's table upload (which would
+// otherwise queue behind it on the copy engine). Called after the column GEMM
+// is launched, so a file read on this thread overlaps the GEMM.
+void stream_column(dsel_engine* e, int p, int round, cudaEvent_t* ev) {
+  const size_t n2 = (size_t)e->nt * e->nt;
+  const int ks = e->pos_sensor[p];
+  CU(cudaStreamWaitEvent(e->cs, e->ev_tab, 0));
+  if (e->kbf_fd >= 0) {
+    // every own slot's true block (s_q, s_k), exactly what read_test_column
+    // reads (kaccess.hpp:27-35); the copy stream then moves it H2D
+    kbf_read_blocks(e, [&](int qq) { return e->slot_sensor[qq]; }, [&](int) { return ks; });
+    CU(cudaEventRecord(ev[5], e->cs));
+    CU(cudaMemcpyAsync(e->Kk, e->h_kstage, sizeof(double) * (size_t)e->nloc * n2, cudaMemcpyHostToDevice, e->cs));
+  } else if (e->hk_user) {
+    // blocks (s_q, s_k) of the caller's K: one strided copy when the own
+    // slots are evenly spaced sensors (cyclic ownership of all sensors)
+    CU(cudaEventRecord(ev[5], e->cs));
+    h2d_blocks(e, e->Kk, [&](int qq) { return user_block(e, qq, ks); }, e->cs);
+  } else if (e->hpacked) {
+    // panel p (blocks q >= p) in one copy; K(q, p) of the live earlier q is
+    // block (p, q) of panel q, copied as stored (ll_addk reads it transposed)
+    CU(cudaEventRecord(ev[5], e->cs));
+    CU(cudaMemcpyAsync(e->Kk + (size_t)p * n2, hpacked_block(e, p, p), sizeof(double) * n2 * (e->nc - p),
+                       cudaMemcpyHostToDevice, e->cs));
+    for (int q = 0; q < p; ++q)
+      if (e->alive[q])
+        CU(cudaMemcpyAsync(e->Kk + (size_t)q * n2, hpacked_block(e, q, p), sizeof(double) * n2,
+                           cudaMemcpyHostToDevice, e->cs));
+  } else {
+    CU(cudaEventRecord(ev[5], e->cs));
+    CU(cudaMemcpyAsync(e->Kk, e->hstore + (size_t)p * e->nloc * n2, sizeof(double) * (size_t)e->nloc * n2,
+                       cudaMemcpyHostToDevice, e->cs));
+  }
+  CU(cudaEventRecord(ev[6], e->cs));
+  e->streamed_round.push_back(round);
+  e->h2d_bytes += (uint64_t)e->nloc * n2 * sizeof(double);
+}
+
 // Left-looking round tail: W_k + L_k from the owner, then this rank's rows of
 // the new conditional column, W_t, and the D (gain input) downdate.
 void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, const double* Lk,
@@ -839,25 +952,9 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
   double flops = 0.0;
   if (!last) launch_trinv(e, Lk);
   CU(cudaEventRecord(ev[3], e->s));
-  // H2D copies share the copy engine: the column copy waits for this round's
-  // table upload on e->s, which would otherwise queue behind it (~0.5 ms)
-  if (e->stream && !last && e->nloc > 0 && Rl > 0) {
-    // the chosen column's blocks for this rank's rows, on the copy stream
-    CU(cudaStreamWaitEvent(e->cs, e->ev_tab, 0));
-    CU(cudaEventRecord(ev[5], e->cs));
-    if (e->hk_user) {
-      // blocks (s_q, s_k) of the caller's K: one strided copy when the own
-      // slots are evenly spaced sensors (cyclic ownership of all sensors)
-      const int ks = e->pos_sensor[p];
-      h2d_blocks(e, e->Kk, [&](int qq) { return user_block(e, qq, ks); }, e->cs);
-    } else {
-      CU(cudaMemcpyAsync(e->Kk, e->hstore + (size_t)p * e->nloc * n2,
-                         sizeof(double) * (size_t)e->nloc * n2, cudaMemcpyHostToDevice, e->cs));
-    }
-    CU(cudaEventRecord(ev[6], e->cs));
-    e->streamed_round.push_back(round);
-    e->h2d_bytes += (uint64_t)e->nloc * n2 * sizeof(double);
-  }
+  // the streamed column is copied after the column GEMM is launched (below):
+  // a file-backed store reads it from disk on this thread while the GEMM runs
+  const bool streamed = e->stream && !last && e->nloc > 0 && Rl > 0;
   if (!last && Rl > 0) {
     const int n_rows = Rl * nt;
     if (nt % 2 == 0) {
@@ -901,12 +998,13 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
         CU(cudaGetLastError());
         e->launches += 1;
       }
-      if (e->stream) {
+      if (streamed) {
+        stream_column(e, p, round, ev);
         const long long total = (long long)nt * n_rows;
         CU(cudaEventRecord(ev[7], e->s));
         CU(cudaStreamWaitEvent(e->s, ev[6], 0));
         ll_addk_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 8), 256, 0, e->s>>>(
-            nullptr, 0, 1, e->Kk, e->col_slot(), nt, n_rows, e->ldo, e->cbuf);
+            nullptr, 0, 1, e->Kk, e->col_slot(), nt, n_rows, e->ldo, e->cbuf, e->hpacked ? p : -1);
         CU(cudaGetLastError());
         e->launches += 1;
       }
@@ -933,12 +1031,14 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
       dim3 gg((n_rows + llg::BM - 1) / llg::BM, (nt + llg::BN - 1) / llg::BN, ga.n_splits);
       ll_gemm_kernel<<<gg, llg::THREADS, llg::SMEM, e->s>>>(ga);
       CU(cudaGetLastError());
-      if (e->stream) {
+      if (streamed) {
+        stream_column(e, p, round, ev);
         const long long total = (long long)nt * n_rows;
         CU(cudaEventRecord(ev[7], e->s));
         CU(cudaStreamWaitEvent(e->s, ev[6], 0));
         ll_addk_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 8), 256, 0, e->s>>>(
-            e->cpart, ga.part_stride, ga.n_splits, e->Kk, e->col_slot(), nt, n_rows, e->ldo, e->cbuf);
+            e->cpart, ga.part_stride, ga.n_splits, e->Kk, e->col_slot(), nt, n_rows, e->ldo, e->cbuf,
+            e->hpacked ? p : -1);
         CU(cudaGetLastError());
         e->launches += 1;
       } else if (ga.n_splits > 1) {
@@ -1003,17 +1103,24 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   cudaEvent_t* ev = &e->ev[(size_t)round * kEv];
   const bool last = round + 1 == e->eff_budget;
 
-  if (e->stream && e->nloc > 0 && !e->hstore && !e->hk_user)
+  if (e->stream && e->nloc > 0 && !e->hstore && !e->hk_user && e->kbf_fd < 0)
     throw Fail{DSEL_E_STATE, "no K loaded (streaming store)"};
   // ---- gains + local argmax ----
   CU(cudaEventRecord(ev[0], e->s));
   if (e->stream && round == 0 && e->nloc > 0) {
     // D[q] = K(own_q, own_q)^T = K(own_q, own_q) (symmetric), from the host store;
     // store block is row-major, D is column-major: equal for a symmetric block
-    h2d_blocks(e, e->D, [&](int qq) {
-      return e->hk_user ? user_block(e, qq, e->slot_sensor[qq])
-                        : e->hstore + ((size_t)(qq * e->G + e->rank) * e->nloc + qq) * nt * nt;
-    }, e->s);
+    if (e->kbf_fd >= 0) {  // diagonal blocks (s_q, s_q) from the file
+      kbf_read_blocks(e, [&](int qq) { return e->slot_sensor[qq]; }, [&](int qq) { return e->slot_sensor[qq]; });
+      CU(cudaMemcpyAsync(e->D, e->h_kstage, sizeof(double) * (size_t)e->nloc * nt * nt, cudaMemcpyHostToDevice,
+                         e->s));
+    } else {
+      h2d_blocks(e, e->D, [&](int qq) {
+        return e->hk_user  ? user_block(e, qq, e->slot_sensor[qq])
+               : e->hpacked ? hpacked_block(e, qq, qq)
+                            : e->hstore + ((size_t)(qq * e->G + e->rank) * e->nloc + qq) * nt * nt;
+      }, e->s);
+    }
     e->h2d_bytes += (uint64_t)e->nloc * nt * nt * sizeof(double);
   } else if (e->ll && round == 0 && e->nloc > 0) {
     const long long total = (long long)e->nloc * nt * nt;
@@ -1440,6 +1547,7 @@ void destroy_impl(dsel_engine* e) {
   if (e->h_round) cudaFreeHost(e->h_round);
   if (e->hstore) cudaFreeHost(e->hstore);
   if (e->hk_registered) cudaHostUnregister(e->hk_registered);
+  detach_kbf(e);
   for (void* ptr : e->ipc_opened) cudaIpcCloseMemHandle(ptr);
   if (e->flag) cudaFree(e->flag);
   if (e->d_peer_wsend) cudaFree(e->d_peer_wsend);
@@ -1494,6 +1602,7 @@ void apply_plan(dsel_engine* e, const dsel_config* cfg, bool ll, bool stream) {
   e->c_elems = (size_t)e->geom().total(e->nloc);
   e->c_pad = e->packed ? (size_t)e->n : 0;
   e->mpad = round_up((int)e->n, ws::BR);
+  e->hpacked = stream && e->G == 1;
 }
 
 uint64_t plan_bytes(const dsel_engine* e, const dsel_config* cfg) {
@@ -1801,6 +1910,7 @@ void ensure_stage(dsel_engine* e, size_t elems) {
   e->stage_elems = elems;
 }
 
+
 // Panel store ingest: H2D of one block row/column into device staging on the
 // copy stream (double-buffered, event-ordered), scatter into the panel on the
 // compute stream, so consecutive panels overlap copy and scatter.
@@ -1813,9 +1923,10 @@ void ensure_hstore(dsel_engine* e) {
     e->hk_registered = nullptr;
   }
   e->hk_user = nullptr;  // loading data detaches a caller's K
+  detach_kbf(e);
   if (!e->hstore) {
     CU(cudaSetDevice(e->dev));
-    CU(ds_malloc_host(&e->hstore, sizeof(double) * (size_t)e->nc * std::max(e->nloc, 1) * e->nt * e->nt));
+    CU(ds_malloc_host(&e->hstore, sizeof(double) * hstore_blocks(e) * e->nt * e->nt));
   }
 }
 
@@ -1824,6 +1935,16 @@ void store_fill(dsel_engine* e, int j, const double* host, bool as_column) {
   ensure_hstore(e);
   const int p = e->sensor_pos[j];
   if (p < 0) return;
+  if (e->hpacked) {
+    if (!as_column) {  // block row p: K(p, pk) for pk <= p -> panel pk, index p - pk
+      for (int pk = 0; pk <= p; ++pk)
+        std::memcpy(hpacked_block(e, pk, p), host + (size_t)e->pos_sensor[pk] * n2, n2 * sizeof(double));
+    } else {  // block column p: K(q, p) for q >= p -> panel p
+      for (int q = p; q < e->nc; ++q)
+        std::memcpy(hpacked_block(e, p, q), host + (size_t)e->pos_sensor[q] * n2, n2 * sizeof(double));
+    }
+    return;
+  }
   if (!as_column) {
     if (p % e->G != e->rank) return;
     const int q = p / e->G;
@@ -1835,6 +1956,27 @@ void store_fill(dsel_engine* e, int j, const double* host, bool as_column) {
       std::memcpy(e->hstore + ((size_t)p * e->nloc + q) * n2, host + (size_t)e->slot_sensor[q] * n2,
                   n2 * sizeof(double));
   }
+}
+
+// Own panel q of K (full height, column-major, ld = ldp) from the device into
+// the host store: packed (world_size 1) keeps K(i, q), i >= q; full keeps
+// K(q, pk) for every pk. `packed` is nc blocks of device scratch.
+cudaError_t store_panel_d2h(dsel_engine* e, const double* panel, long long ldp, int q, double* packed) {
+  const size_t n2 = (size_t)e->nt * e->nt;
+  const long long total = (long long)e->nc * n2;
+  const unsigned grid = (unsigned)std::min<long long>((total + 255) / 256, 148 * 16);
+  if (e->hpacked) {
+    stream_pack_lower_kernel<<<grid, 256, 0, e->s>>>(panel, ldp, e->nt, q, e->nc, packed);
+    cudaError_t ce = cudaGetLastError();
+    if (ce != cudaSuccess) return ce;
+    return cudaMemcpyAsync(hpacked_block(e, q, q), packed, sizeof(double) * n2 * (e->nc - q),
+                           cudaMemcpyDeviceToHost, e->s);
+  }
+  stream_pack_kernel<<<grid, 256, 0, e->s>>>(panel, ldp, e->nt, e->nc, packed);
+  cudaError_t ce = cudaGetLastError();
+  if (ce != cudaSuccess) return ce;
+  return cudaMemcpy2DAsync(e->hstore + (size_t)q * n2, (size_t)e->nloc * n2 * sizeof(double), packed,
+                           n2 * sizeof(double), n2 * sizeof(double), e->nc, cudaMemcpyDeviceToHost, e->s);
 }
 
 void load_panel(dsel_engine* e, int j, const double* host, bool as_column) {
@@ -2071,7 +2213,7 @@ dsel_status dsel_get_plan(const dsel_engine* e, dsel_plan* out) {
   p.device_bytes = e->dev_bytes;
   p.planned_bytes = e->planned;
   p.budget_bytes = e->plan_budget;
-  p.host_store_bytes = e->hstore ? sizeof(double) * (uint64_t)e->nc * std::max(e->nloc, 1) * e->nt * e->nt : 0;
+  p.host_store_bytes = e->hstore ? sizeof(double) * (uint64_t)hstore_blocks(e) * e->nt * e->nt : 0;
   *out = p;
   return DSEL_OK;
 }
@@ -2128,6 +2270,7 @@ void attach_host(dsel_engine* e, const double* host_k, bool rows) {
     cudaFreeHost(e->hstore);
     e->hstore = nullptr;
   }
+  detach_kbf(e);
   e->hk_user = host_k;
   e->hk_rows = rows;
 }
@@ -2145,6 +2288,13 @@ dsel_status dsel_load_k(dsel_engine* e, const double* host_k) {
     if (e->stream) {  // hstore[pk][q] = K(own_q, k): block (s_q, s_k) of the block-row-major K
       const size_t n2 = (size_t)e->nt * e->nt;
       ensure_hstore(e);
+      if (e->hpacked) {
+        for (int pk = 0; pk < e->nc; ++pk)
+          for (int q = pk; q < e->nc; ++q)
+            std::memcpy(hpacked_block(e, pk, q),
+                        host_k + ((size_t)e->pos_sensor[q] * e->nd + e->pos_sensor[pk]) * n2, n2 * sizeof(double));
+        return;
+      }
       for (int pk = 0; pk < e->nc; ++pk)
         for (int q = 0; q < e->nloc; ++q)
           std::memcpy(e->hstore + ((size_t)pk * e->nloc + q) * n2,
@@ -2167,19 +2317,6 @@ dsel_status dsel_load_k(dsel_engine* e, const double* host_k) {
 // semantics) into two pinned host buffers, alternated so the pread of panel
 // q+1 overlaps the H2D + scatter of panel q.
 namespace {
-void pread_exact(int fd, void* dst, size_t bytes, off_t off, const std::string& path) {
-  unsigned char* p = static_cast<unsigned char*>(dst);
-  size_t done = 0;
-  while (done < bytes) {
-    const ssize_t got = ::pread(fd, p + done, bytes - done, off + (off_t)done);
-    if (got < 0) {
-      if (errno == EINTR) continue;
-      throw Fail{DSEL_E_IO, path + ": pread failed: " + std::strerror(errno)};
-    }
-    if (got == 0) throw Fail{DSEL_E_CORRUPT, path + ": unexpected end of file"};
-    done += (size_t)got;
-  }
-}
 
 void load_kbf_impl(dsel_engine* e, const char* path, bool exact_columns, int threads) {
   const std::string ps(path ? path : "");
@@ -2266,6 +2403,55 @@ void load_kbf_impl(dsel_engine* e, const char* path, bool exact_columns, int thr
 }
 }  // namespace
 
+// File-backed streaming store: validate like KStoreReader and keep the file;
+// each round reads only the chosen column's own blocks (stream_column).
+void attach_kbf_impl(dsel_engine* e, const char* path, int threads) {
+  if (!e->stream) throw Fail{DSEL_E_INVALID, "attach_kbf needs storage = DSEL_STORAGE_STREAM"};
+  const std::string ps(path ? path : "");
+  const int fd = ::open(ps.c_str(), O_RDONLY);
+  if (fd < 0) throw Fail{DSEL_E_IO, "cannot open " + ps + ": " + std::strerror(errno)};
+  try {
+    unsigned char h[32];
+    if (::pread(fd, h, 32, 0) != 32) throw Fail{DSEL_E_CORRUPT, ps + ": header truncated"};
+    auto u32 = [&](int o) {
+      return (uint32_t)h[o] | ((uint32_t)h[o + 1] << 8) | ((uint32_t)h[o + 2] << 16) | ((uint32_t)h[o + 3] << 24);
+    };
+    if (std::memcmp(h, "KBF1", 4) != 0) throw Fail{DSEL_E_CORRUPT, ps + ": bad magic"};
+    const int nd = (int)u32(8), nt = (int)u32(12);
+    if (u32(4) != 1 || u32(16) != 1 || u32(20) != 1 || nd < 1 || nt < 1)
+      throw Fail{DSEL_E_CORRUPT, ps + ": unsupported header fields"};
+    struct stat st {};
+    if (::fstat(fd, &st) != 0) throw Fail{DSEL_E_IO, ps + ": fstat failed"};
+    const size_t expect = 32 + (size_t)nd * nd * nt * nt * sizeof(double);
+    if ((size_t)st.st_size != expect)
+      throw Fail{DSEL_E_CORRUPT, ps + ": size " + std::to_string(st.st_size) + " != expected " + std::to_string(expect)};
+    if (nd != e->nd || nt != e->nt)
+      throw Fail{DSEL_E_INVALID, ps + ": store shape does not match the engine configuration"};
+    CU(cudaSetDevice(e->dev));
+    if (e->hstore) {
+      cudaFreeHost(e->hstore);
+      e->hstore = nullptr;
+    }
+    if (e->hk_registered) {
+      cudaHostUnregister(e->hk_registered);
+      e->hk_registered = nullptr;
+    }
+    e->hk_user = nullptr;
+    detach_kbf(e);
+    CU(ds_malloc_host(&e->h_kstage, sizeof(double) * (size_t)std::max(e->nloc, 1) * e->nt * e->nt));
+  } catch (...) {
+    ::close(fd);
+    throw;
+  }
+  e->kbf_fd = fd;
+  e->kbf_path = ps;
+  e->kbf_threads = threads > 0 ? threads : (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+}
+
+dsel_status dsel_attach_kbf(dsel_engine* e, const char* path, int threads) {
+  return guard(e, [&] { attach_kbf_impl(e, path, threads); });
+}
+
 dsel_status dsel_load_kbf(dsel_engine* e, const char* path, int exact_columns, int threads) {
   return guard(e, [&] { load_kbf_impl(e, path, exact_columns != 0, threads); });
 }
@@ -2280,7 +2466,27 @@ dsel_status dsel_read_block_row(dsel_engine* e, int j, double* host_row) {
     if (e->stream) {  // K itself, from the pinned host store
       const size_t n2 = (size_t)e->nt * e->nt;
       std::memset(host_row, 0, elems * sizeof(double));
-      if (!e->hstore && !e->hk_user) throw Fail{DSEL_E_STATE, "no K loaded"};
+      if (!e->hstore && !e->hk_user && e->kbf_fd < 0) throw Fail{DSEL_E_STATE, "no K loaded"};
+      if (e->kbf_fd >= 0) {  // the file's block row j
+        const size_t bsz = n2 * sizeof(double);
+        for (int pk = 0; pk < e->nc; ++pk)
+          pread_exact(e->kbf_fd, host_row + (size_t)e->pos_sensor[pk] * n2, bsz,
+                      (off_t)(32 + ((size_t)j * e->nd + e->pos_sensor[pk]) * bsz), e->kbf_path);
+        return;
+      }
+      if (e->hpacked && !e->hk_user) {  // K(p, pk): panel pk when p >= pk, else panel p transposed
+        for (int pk = 0; pk < e->nc; ++pk) {
+          double* dst = host_row + (size_t)e->pos_sensor[pk] * n2;
+          if (p >= pk) {
+            std::memcpy(dst, hpacked_block(e, pk, p), n2 * sizeof(double));
+          } else {
+            const double* src = hpacked_block(e, p, pk);  // K(pk, p) row-major
+            for (int r = 0; r < e->nt; ++r)
+              for (int c = 0; c < e->nt; ++c) dst[(size_t)r * e->nt + c] = src[(size_t)c * e->nt + r];
+          }
+        }
+        return;
+      }
       for (int pk = 0; pk < e->nc; ++pk)
         std::memcpy(host_row + (size_t)e->pos_sensor[pk] * n2,
                     e->hk_user ? e->hk_user + ((size_t)(e->hk_rows ? q : j) * e->nd + e->pos_sensor[pk]) * n2
@@ -2357,14 +2563,8 @@ dsel_status dsel_gen_synthetic(dsel_engine* e, const double* v_host, int rank, d
         g.q0 = 0;
         dim3 grid((g.n_rows + gen::BM - 1) / gen::BM, (g.n_cols + gen::BN - 1) / gen::BN);
         synth_panel_kernel<<<grid, gen::THREADS, 0, e->s>>>(g);
-        const long long total = (long long)e->nc * n2;
-        stream_pack_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 16), 256, 0,
-                             e->s>>>(panel, e->n, e->nt, e->nc, packed);
         ce = cudaGetLastError();
-        if (ce == cudaSuccess)
-          ce = cudaMemcpy2DAsync(e->hstore + (size_t)q * n2, (size_t)e->nloc * n2 * sizeof(double),
-                                 packed, n2 * sizeof(double), n2 * sizeof(double), e->nc,
-                                 cudaMemcpyDeviceToHost, e->s);
+        if (ce == cudaSuccess) ce = store_panel_d2h(e, panel, e->n, q, packed);
         if (ce == cudaSuccess) ce = cudaStreamSynchronize(e->s);
       }
       if (panel) cudaFree(panel);
@@ -2381,10 +2581,103 @@ dsel_status dsel_gen_synthetic(dsel_engine* e, const double* v_host, int rank, d
 
 static void reset_state(dsel_engine* e);
 
+// Device-formed synthetic K into the streaming (host) store: chunks of this
+// rank's panels are accumulated on the device by the update kernel (W = +V,
+// the same Philox V and per-element order as the HBM path, so the same bits)
+// and copied to the pinned store -- the packed store needs only the
+// block-lower tiles. K never has to fit in HBM (north star (1) at C5 scale).
+void gen_device_stream(dsel_engine* e, int vrank, double sigma, uint64_t seed) {
+  const int nt = e->nt;
+  reset_state(e);  // every candidate live: compact row index = position
+  ensure_hstore(e);
+  const int R = e->n_rows_tab, n_rows = R * nt;
+  const size_t n2 = (size_t)nt * nt, panel = (size_t)e->n * nt;
+  constexpr int kch = 512;  // rank columns per update launch
+  const int mpad = round_up(std::max(n_rows, 1), ws::BR);
+  size_t free_b = 0, total_b = 0;
+  CU(cudaMemGetInfo(&free_b, &total_b));
+  const size_t fixed = ((size_t)mpad * kch + (size_t)e->nc * n2) * sizeof(double) + (4ull << 30);
+  const size_t room = free_b > fixed ? free_b - fixed : 0;
+  const int cp = (int)std::max<size_t>(1, std::min<size_t>((size_t)std::max(e->nloc, 1), room / (panel * sizeof(double))));
+  DevScratch<double> chunk((size_t)cp * panel), vt((size_t)mpad * kch), packed((size_t)e->nc * n2);
+  const bool sym = e->hpacked;  // the packed store keeps the block-lower half only
+  const int br = ws::BR;
+  const int nct_max = (cp * nt + ws::BC - 1) / ws::BC;
+  const int ng_max = (nct_max + e->ws_group - 1) / e->ws_group;
+  std::vector<int> h_tabs(2 * (size_t)cp + nct_max + ng_max + 1);
+  DevScratch<int> d_tabs(h_tabs.size());
+  const int nrt = (n_rows + br - 1) / br;
+  for (int q0 = 0; q0 < e->nloc; q0 += cp) {
+    const int c = std::min(cp, e->nloc - q0), n_cols = c * nt;
+    int* cs = h_tabs.data();
+    int* cg = cs + cp;
+    for (int h = 0; h < c; ++h) {
+      cs[h] = h;                          // slot inside the chunk buffer
+      cg[h] = (q0 + h) * e->G + e->rank;  // compact row block = position (all live)
+    }
+    const int nct = (n_cols + ws::BC - 1) / ws::BC, ng = (nct + e->ws_group - 1) / e->ws_group;
+    int* fr = cg + cp;
+    int* gp = fr + nct_max;
+    int sym_tiles = 0;
+    if (sym) {  // block-lower tile schedule of the chunk (sym_tables)
+      for (int ct = 0; ct < nct; ++ct) fr[ct] = (cg[(ct * ws::BC) / nt] * nt) / br;
+      gp[0] = 0;
+      for (int g = 0; g < ng; ++g) {
+        const int ct0 = g * e->ws_group, gw = std::min(e->ws_group, nct - ct0);
+        gp[g + 1] = gp[g] + (nrt - fr[ct0]) * gw;
+      }
+      sym_tiles = gp[ng];
+    }
+    CU(cudaMemcpy(d_tabs.p, h_tabs.data(), sizeof(int) * h_tabs.size(), cudaMemcpyHostToDevice));
+    const PanelGeom g{chunk.p, e->n, nt, e->G, e->rank, 0};
+    CU(cudaMemsetAsync(chunk.p, 0, sizeof(double) * (size_t)c * panel, e->s));
+    add_diag_kernel<<<(unsigned)std::min<long long>(((long long)c * nt + 255) / 256, 1024), 256, 0, e->s>>>(
+        g, c, sigma * sigma, q0);
+    CU(cudaGetLastError());
+    for (int k0 = 0; k0 < vrank; k0 += kch) {
+      const long long total = (long long)mpad * (kch / 2);
+      gen_v_tiled_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 32), 256, 0, e->s>>>(
+          vt.p, mpad, kch, k0, vrank, e->row_pos(), e->d_pos_sensor, n_rows, nt, (unsigned long long)seed);
+      UpdateWSArgs ua{};
+      ua.C = chunk.p;
+      ua.geom = g;
+      ua.Wt = vt.p;
+      ua.Wnt = vt.p;
+      ua.mpad = mpad;
+      ua.n_k = kch / ws::KC;
+      ua.row_pos = e->row_pos();
+      ua.col_slot = d_tabs.p;
+      ua.col_g = d_tabs.p + cp;
+      ua.nt = nt;
+      ua.n_rows = n_rows;
+      ua.n_cols = n_cols;
+      ua.n_row_tiles = nrt;
+      ua.n_col_tiles = nct;
+      ua.group = e->ws_group;
+      ua.sym = sym;
+      ua.first_rt = d_tabs.p + 2 * cp;
+      ua.gprefix = d_tabs.p + 2 * cp + nct_max;
+      ua.n_groups = ng;
+      ua.n_tiles = sym ? sym_tiles : nrt * nct;
+      ua.n_full = ua.n_tiles;
+      ua.split_s = 1;
+      launch_ws(e, ua, ws_pick(e, 0, ua.n_k, false));
+    }
+    for (int h = 0; h < c; ++h) CU(store_panel_d2h(e, chunk.p + (size_t)h * panel, e->n, q0 + h, packed.p));
+    CU(cudaStreamSynchronize(e->s));
+  }
+  e->full_panels = true;
+}
+
 dsel_status dsel_gen_synthetic_device(dsel_engine* e, int rank, double sigma, uint64_t seed) {
   return guard(e, [&] {
     if (rank < 1) throw Fail{DSEL_E_INVALID, "bad synthetic rank"};
-    if (e->stream) throw Fail{DSEL_E_INVALID, "gen_synthetic_device fills the HBM panel store"};
+    if (e->nt % 2) throw Fail{DSEL_E_INVALID, "gen_synthetic_device needs an even n_steps"};
+    if (e->stream) {
+      CU(cudaSetDevice(e->dev));
+      gen_device_stream(e, rank, sigma, seed);
+      return;
+    }
     if (e->nt % 2) throw Fail{DSEL_E_INVALID, "gen_synthetic_device needs an even n_steps"};
     CU(cudaSetDevice(e->dev));
     const int nt = e->nt;

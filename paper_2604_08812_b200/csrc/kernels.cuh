@@ -330,6 +330,9 @@ __global__ void __launch_bounds__(upd::THREADS, 1) schur_update_kernel(UpdateArg
 namespace ws {
 constexpr int BR = 128, BC = 64, KC = 16;  // BR: the largest tile height (row padding unit)
 constexpr int MAX_SYM_CT = 1024;  // column tiles whose schedule fits in shared memory
+// "no column" marker of the per-tile column map: a packed panel's column base
+// can be negative (rows above its first stored row start before it)
+constexpr long long kNoCol = (-9223372036854775807LL - 1);
 // One kernel configuration: BRT-row x 64-column tiles, (BRT/32) x 2 consumer
 // warps of 32 x 32, SCT k-chunks per pipeline stage, STG stages, MINB CTAs/SM.
 // Big: 128-row tiles, 8 consumer warps, 1 CTA/SM. Pair: 64-row tiles, 4
@@ -628,11 +631,11 @@ __global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(
           const int blk = c / nt;
           const int off = c - blk * nt;
           const int q = a.col_slot[blk];
-          colbase[i] = a.geom.idx(q, off, 0);
+          colbase[i] = a.geom.idx(q, off, 0);  // may be < 0: packed panel 0 of rank > 0
           colstart[i] = (int)a.geom.start(q);
           cwl[m] = a.col_g[blk] * nt + off;
         } else {
-          colbase[i] = -1;
+          colbase[i] = ws::kNoCol;
           colstart[i] = 0;
           cwl[m] = 0;  // columns past the edge read W row 0 (never stored)
         }
@@ -800,7 +803,7 @@ __global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(
       double* const out = uz < 0 ? a.cout : a.part + (size_t)uz * a.part_stride;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        if (colbase[wc + i * 8 + g] < 0) continue;
+        if (colbase[wc + i * 8 + g] == ws::kNoCol) continue;
         const int crow = c0o + wc + i * 8 + g;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -817,7 +820,7 @@ __global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const long long cb = colbase[wc + i * 8 + g];
-        if (cb < 0) continue;
+        if (cb == ws::kNoCol) continue;
         double* col = a.C + cb;
         const int c_lo = cst[wc + i * 8 + g];
 #pragma unroll
@@ -1294,9 +1297,11 @@ __global__ void __launch_bounds__(256) ll_dupdate_kernel(LLDArgs a) {
 // round's chosen candidate k arrive by H2D into Kk ([slot][nt][nt] row-major)
 // while the GEMM computes -W_own W_k^T; this adds them (and sums split-K
 // partials in split order when present): c[col][row] += Kk[q][r][col].
+// tpos: blocks of slots below it arrive transposed (packed host store: K(q, k)
+// read as block (k, q)); -1 = none
 __global__ void ll_addk_kernel(const double* part, long long part_stride, int n_splits,
                                const double* Kk, const int* row_slot, int nt, int n_rows,
-                               long long ldo, double* cout) {
+                               long long ldo, double* cout, int tpos) {
   const long long total = (long long)nt * n_rows;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
@@ -1310,7 +1315,8 @@ __global__ void ll_addk_kernel(const double* part, long long part_stride, int n_
       v = cout[o];
     }
     const int blk = r / nt, rr = r - blk * nt;
-    cout[o] = v + Kk[((size_t)row_slot[blk] * nt + rr) * nt + c];
+    const int sl = row_slot[blk];
+    cout[o] = v + (sl < tpos ? Kk[((size_t)sl * nt + c) * nt + rr] : Kk[((size_t)sl * nt + rr) * nt + c]);
   }
 }
 
@@ -1326,6 +1332,20 @@ __global__ void stream_pack_kernel(const double* panel, long long ldp, int nt, i
     const int r = (int)(w / nt), c = (int)(w - (long long)r * nt);
     // K(own_q, k)[r][c] = K[q-block row r][k col c] = K[k*nt + c][q*nt + r] (symmetric)
     out[e] = panel[(size_t)r * ldp + (size_t)pk * nt + c];
+  }
+}
+
+// Packed host store (world_size 1): device panel q (column-major, ld = ldp)
+// -> [i - q][r][c] = K(i, q)[r][c] for i = q..n_cand-1 (row-major blocks).
+__global__ void stream_pack_lower_kernel(const double* panel, long long ldp, int nt, int q, int n_cand,
+                                         double* out) {
+  const long long total = (long long)(n_cand - q) * nt * nt;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = q + (int)(e / ((long long)nt * nt));
+    const long long w = e - (long long)(i - q) * nt * nt;
+    const int r = (int)(w / nt), c = (int)(w - (long long)r * nt);
+    out[e] = panel[(size_t)c * ldp + (size_t)i * nt + r];
   }
 }
 
@@ -2299,13 +2319,14 @@ __global__ void gen_v_tiled_kernel(double* Vt, int mpad, int kch, int k0, int ra
 }
 
 // C = sigma^2 on the diagonal of every own slot's diagonal block (C zeroed first)
-__global__ void add_diag_kernel(PanelGeom geom, int nloc, double v) {
+// (q0: the panels are slots q0.. of this rank -- a chunk of the store)
+__global__ void add_diag_kernel(PanelGeom geom, int nloc, double v, int q0 = 0) {
   const int nt = geom.nt;
   const long long total = (long long)nloc * nt;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const int q = (int)(e / nt), c = (int)(e - (long long)q * nt);
-    const long long p = (long long)q * geom.G + geom.rank;
+    const long long p = (long long)(q0 + q) * geom.G + geom.rank;
     geom.base[geom.idx(q, c, p * nt + c)] += v;
   }
 }

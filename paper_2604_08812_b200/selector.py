@@ -267,6 +267,11 @@ class Engine:
         """KBF store (kstore.hpp:22-186) -> this engine's panels."""
         _check(lib.dsel_load_kbf(self.h, path.encode(), int(exact_columns), threads), self.h)
 
+    def attach_kbf(self, path: str, threads: int = 0) -> None:
+        """File-backed streaming store (storage='stream'): each round preads
+        only the chosen column's own blocks from the KBF file."""
+        _check(lib.dsel_attach_kbf(self.h, path.encode(), threads), self.h)
+
     def load_block_row(self, j: int, row) -> None:
         _check(lib.dsel_load_block_row(self.h, j, _host_ptr(row)), self.h)
 

@@ -74,6 +74,40 @@ if which == "random":
     print(f"rank {rank}/{world} random: {'OK' if not bad else 'MISMATCH'}", flush=True)
     dist.destroy_process_group()
     sys.exit(1 if bad else 0)
+if which == "replay":
+    # every remaining candidate's gain at every round (forced replay along the
+    # reference sequence), gathered over the ranks -- full gain vectors, not
+    # just winners (a wrong loser would not change the sequence), on every
+    # storage variant
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "c1.json")))
+    v = d.synthetic_v(64, 32, 2048, 2024)
+    bad = 0
+    for kw in (dict(), dict(packed=False), dict(full_square=True), dict(algorithm="left")):
+        cid = [d.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(cid, src=0)
+        with d.Engine(64, 32, 16, device=local, world_size=world, rank=rank, nccl_id=cid[0], **kw) as eng:
+            eng.gen_synthetic(v, 2048, 1.0)
+            mine = []
+            for s in gold["chosen"]:
+                mine.append(eng.peek_gains())
+                eng.step(forced=s)
+        allg = [None] * world
+        dist.all_gather_object(allg, mine)
+        for rnd in range(16):
+            for j in range(64):
+                want = gold["replay_gains"][rnd][j]
+                got = [a[rnd][j] for a in allg if not np.isnan(a[rnd][j])]
+                if want is None:
+                    ok = not got
+                else:
+                    ok = len(got) == 1 and abs(got[0] - want) <= 1e-9 * max(abs(want), 1.0)
+                if not ok:
+                    bad += 1
+                    if bad < 5:
+                        print(f"rank {rank} {kw} round {rnd} sensor {j}: {got} vs {want}", flush=True)
+    print(f"rank {rank}/{world} replay: {'OK' if not bad else 'MISMATCH'}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(1 if bad else 0)
 if which == "device":
     # K formed on every rank by the update kernel from the device Philox V; the
     # sequence must match the oracle on the same K (numpy V) at any world size

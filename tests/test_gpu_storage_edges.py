@@ -257,3 +257,64 @@ def test_batched_logdet_against_numpy(dsel):
             want = np.linalg.slogdet(mats[b])[1]
             assert st[b] == -1 and abs(ld[b] - want) <= 1e-9 * max(abs(want), 1.0), (m, b, ld[b], want)
         assert st[2] == m // 2 and ld[2] == -np.inf, (m, st[2], ld[2])
+
+
+# ---- out-of-HBM stores (north star (1)) ----------------------------------- #
+def test_file_backed_store_matches_reference(dsel, O, golden_dir, tmp_path):
+    """dsel_attach_kbf: K stays in the KBF file; every round preads the chosen
+    column's true blocks (KStoreReader::read_block) while the column GEMM runs.
+    Same sequence and gains as the reference; only the chosen columns are read."""
+    w = golden(golden_dir, "wave.json")
+    path = os.path.join(golden_dir, "wave.kbf")
+    k, nd, nt = O.read_kbf(path)
+    with dsel.Engine(nd, nt, 12, algorithm="left", storage="stream") as eng:
+        eng.attach_kbf(path, threads=4)
+        eng.run()
+        rows = eng.trace()
+        st = eng.stats()
+        assert np.array_equal(eng.read_block_row(5), k.reshape(nd, -1)[5])
+    assert [r["chosen_index"] for r in rows] == w["chosen"]
+    for r, g in zip(rows, w["gains"]):
+        assert gain_close(r["gain"], g)
+    n2b = nt * nt * 8
+    assert st["h2d_bytes"] == nd * n2b + 11 * nd * n2b  # diagonal once + one column per round
+    c1 = golden(golden_dir, "c1.json")
+    kc1 = O.synthetic_k(64, 32, 2048, 1.0, 2024)
+    kbf = str(tmp_path / "c1.kbf")
+    O.ref_write_kbf(kc1, 64, 32, kbf)
+    with dsel.Engine(64, 32, 16, algorithm="left", storage="stream") as eng:
+        eng.attach_kbf(kbf)
+        eng.run()
+        rows = eng.trace()
+    assert [r["chosen_index"] for r in rows] == c1["chosen"]
+    for r, g in zip(rows, c1["gains"]):
+        assert gain_close(r["gain"], g)
+    bad = tmp_path / "bad.kbf"
+    bad.write_bytes(open(kbf, "rb").read()[:-8])
+    with dsel.Engine(64, 32, 16, algorithm="left", storage="stream") as eng:
+        with pytest.raises(dsel.CorruptFile):
+            eng.attach_kbf(str(bad))
+
+
+def test_packed_host_store_device_generated_k(dsel):
+    """storage = stream on one GPU keeps the block-lower half of K in pinned host
+    memory (half the host bytes); K formed on the device chunk by chunk
+    (gen_synthetic_device) is bit-identical to the HBM store's, and the
+    streamed selection matches the resident one."""
+    nd, nt, b, rk, seed = 40, 64, 12, 900, 7
+    with dsel.Engine(nd, nt, b, algorithm="left", storage="stream") as s_eng, \
+            dsel.Engine(nd, nt, b, algorithm="left", storage="hbm") as h_eng:
+        s_eng.gen_synthetic_device(rk, 0.5, seed)
+        h_eng.gen_synthetic_device(rk, 0.5, seed)
+        assert s_eng.plan()["host_store_bytes"] == nd * (nd + 1) // 2 * nt * nt * 8
+        for j in (0, 17, 39):
+            a, bb = s_eng.read_block_row(j), h_eng.read_block_row(j)
+            assert np.array_equal(a.view(np.uint64), bb.view(np.uint64)), j
+        s_eng.run()
+        h_eng.run()
+        rs, rh = s_eng.trace(), h_eng.trace()
+        st = s_eng.stats()
+    assert [r["chosen_index"] for r in rs] == [r["chosen_index"] for r in rh]
+    for x, y in zip(rs, rh):
+        assert gain_close(x["gain"], y["gain"], 1e-12)
+    assert st["io_ms"] > 0
