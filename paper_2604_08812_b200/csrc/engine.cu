@@ -325,6 +325,9 @@ size_t hpanel_off(const dsel_engine* e, int pk) {  // blocks before packed panel
 double* hpacked_block(const dsel_engine* e, int pk, int q) {  // K(q, pk), q >= pk, row-major
   return e->hstore + (hpanel_off(e, pk) + (q - pk)) * (size_t)e->nt * e->nt;
 }
+// the round's K column comes from the packed host store (blocks of earlier
+// slots arrive transposed) -- not from the caller's K or a KBF file
+bool packed_host_source(const dsel_engine* e) { return e->hpacked && !e->hk_user && e->kbf_fd < 0; }
 
 void detach_kbf(dsel_engine* e) {
   if (e->kbf_fd >= 0) ::close(e->kbf_fd);
@@ -874,7 +877,7 @@ void stream_column(dsel_engine* e, int p, int round, cudaEvent_t* ev) {
     // slots are evenly spaced sensors (cyclic ownership of all sensors)
     CU(cudaEventRecord(ev[5], e->cs));
     h2d_blocks(e, e->Kk, [&](int qq) { return user_block(e, qq, ks); }, e->cs);
-  } else if (e->hpacked) {
+  } else if (packed_host_source(e)) {
     // panel p (blocks q >= p) in one copy; K(q, p) of the live earlier q is
     // block (p, q) of panel q, copied as stored (ll_addk reads it transposed)
     CU(cudaEventRecord(ev[5], e->cs));
@@ -1004,7 +1007,7 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
         CU(cudaEventRecord(ev[7], e->s));
         CU(cudaStreamWaitEvent(e->s, ev[6], 0));
         ll_addk_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 8), 256, 0, e->s>>>(
-            nullptr, 0, 1, e->Kk, e->col_slot(), nt, n_rows, e->ldo, e->cbuf, e->hpacked ? p : -1);
+            nullptr, 0, 1, e->Kk, e->col_slot(), nt, n_rows, e->ldo, e->cbuf, packed_host_source(e) ? p : -1);
         CU(cudaGetLastError());
         e->launches += 1;
       }
@@ -1038,7 +1041,7 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
         CU(cudaStreamWaitEvent(e->s, ev[6], 0));
         ll_addk_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 8), 256, 0, e->s>>>(
             e->cpart, ga.part_stride, ga.n_splits, e->Kk, e->col_slot(), nt, n_rows, e->ldo, e->cbuf,
-            e->hpacked ? p : -1);
+            packed_host_source(e) ? p : -1);
         CU(cudaGetLastError());
         e->launches += 1;
       } else if (ga.n_splits > 1) {
@@ -1117,7 +1120,7 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
     } else {
       h2d_blocks(e, e->D, [&](int qq) {
         return e->hk_user  ? user_block(e, qq, e->slot_sensor[qq])
-               : e->hpacked ? hpacked_block(e, qq, qq)
+               : packed_host_source(e) ? hpacked_block(e, qq, qq)
                             : e->hstore + ((size_t)(qq * e->G + e->rank) * e->nloc + qq) * nt * nt;
       }, e->s);
     }

@@ -53,7 +53,7 @@ def naive_select_gpu(k_blocks: np.ndarray, nd: int, nt: int, budget: int, candid
                      chunk: int = 64, device: str = "cuda"):
     """Refactorizing greedy selection (naive_select, selector.hpp:253-348) on the GPU.
     Returns (chosen, gains, objectives); gains are raw log-det increments."""
-    import paper_2604_08812_b200 as d
+    import paper_2604_08812_b200 as dsel
 
     kd = torch.as_tensor(_dense(k_blocks, nd, nt), dtype=torch.float64, device=device)
     remaining = list(range(nd)) if candidates is None else list(candidates)
@@ -65,7 +65,7 @@ def naive_select_gpu(k_blocks: np.ndarray, nd: int, nt: int, budget: int, candid
             cs = remaining[c0:c0 + chunk]
             idx = torch.stack([_idx(chosen + [s], nt, device) for s in cs])   # (b, dim)
             m = kd[idx[:, :, None], idx[:, None, :]]                          # (b, dim, dim)
-            lds, status = d.batched_logdet(m)   # refactorized from scratch, this library's kernel
+            lds, status = dsel.batched_logdet(m)   # refactorized from scratch, this library's kernel
             ld = lds - logdet_prev
             ld = torch.where(status < 0, ld, torch.full_like(ld, -math.inf)).cpu().numpy()
             for s, d in zip(cs, ld):   # better_candidate (selector.hpp:132-134)
