@@ -237,8 +237,9 @@ struct dsel_engine {
   std::vector<void*> ipc_opened;
   const double** d_peer_wsend = nullptr;
   unsigned long long** d_peer_flag = nullptr;
-  int ws_br = 128;  // update-kernel tile height: 128 (ws::Big, 1 CTA/SM) or 64 (ws::Pair, 2 CTAs/SM)
-  int ws_cfg = -1;   // -1 auto (Big for short k, Big4 from 16 k-chunks), 0 ws::Big, 1 ws::Pair, 2 ws::Big4
+  int ws_br = 128;  // tile height of the right-looking update configuration (rl_cfg)
+  int ws_cfg = -1;   // DSEL_WS_CFG: -1 auto, 0 ws::Big, 1 ws::Pair, 2 ws::Big4, 3 ws::Big6
+  int rl_cfg = 0;    // configuration of the right-looking update and K formation
   int ws_group = kWsGroupDefault;  // column tiles per rasterization group
   double gen_flops = 0.0;  // last dsel_gen_synthetic_device (K formation on the update kernel)
   bool keep = false, export_factor = false;
@@ -557,6 +558,7 @@ void set_smem_limits(int dev) {
   allow_smem(schur_update_ws_kernel<ws::Big>, optin);
   allow_smem(schur_update_ws_kernel<ws::Pair>, optin);
   allow_smem(schur_update_ws_kernel<ws::Big4>, optin);
+  allow_smem(schur_update_ws_kernel<ws::Big6>, optin);
   CU(cudaFuncSetAttribute(schur_update_ws_kernel<ws::Pair>, cudaFuncAttributePreferredSharedMemoryCarveout,
                           (int)cudaSharedmemCarveoutMaxShared));
   allow_smem(ll_gemm_kernel, optin);
@@ -700,8 +702,18 @@ void setup_p2p(dsel_engine* e) {
 // short ones (Nt = 128 right-looking); 64-row tiles (Pair) when the r-side row
 // count pads badly to 128 (left-looking r-side = Nt rows: 420 -> 82 % of 4 x
 // 128 tiles, 94 % of 7 x 64). -1 = auto.
+int cfg_br(int cfg) { return cfg == 1 ? 64 : cfg == 3 ? 192 : 128; }
+int ws_pick(const dsel_engine* e, int r_rows, int n_k, bool fixed_rows);
+// K formation on the update kernel: its tile schedule uses ws_br, so the tile
+// height must match the right-looking configuration's
+int gen_cfg(const dsel_engine* e, int n_k) {
+  return e->ws_br == 192 ? 3 : e->ws_br == 64 ? 1 : (n_k >= 16 ? 2 : 0);
+}
+
 int ws_pick(const dsel_engine* e, int r_rows, int n_k, bool fixed_rows) {
-  if (e->ws_cfg >= 0) return e->ws_cfg;
+  // Big6 (192-row tiles) only for the right-looking update: the left-looking
+  // r-side (W_k, Nt rows) is padded for 128-row tiles
+  if (e->ws_cfg >= 0 && !(fixed_rows && e->ws_cfg == 3)) return e->ws_cfg;
   if (fixed_rows) {
     const double u128 = (double)r_rows / (((r_rows + 127) / 128) * 128);
     const double u64 = (double)r_rows / (((r_rows + 63) / 64) * 64);
@@ -711,7 +723,7 @@ int ws_pick(const dsel_engine* e, int r_rows, int n_k, bool fixed_rows) {
 }
 
 void launch_ws(dsel_engine* e, UpdateWSArgs& ua, int cfg) {
-  ua.br = cfg == 1 ? 64 : 128;
+  ua.br = cfg_br(cfg);
   const long long units = (long long)ua.n_full + (long long)(ua.n_tiles - ua.n_full) * ua.split_s;
   if (units <= 0) return;
   if (cfg == 1) {
@@ -720,6 +732,9 @@ void launch_ws(dsel_engine* e, UpdateWSArgs& ua, int cfg) {
   } else if (cfg == 2) {
     const int grid = (int)std::min<long long>(e->n_sms, units);
     schur_update_ws_kernel<ws::Big4><<<grid, ws::Big4::THREADS, ws::Big4::SMEM, e->s>>>(ua);
+  } else if (cfg == 3) {
+    const int grid = (int)std::min<long long>(e->n_sms, units);
+    schur_update_ws_kernel<ws::Big6><<<grid, ws::Big6::THREADS, ws::Big6::SMEM, e->s>>>(ua);
   } else {
     const int grid = (int)std::min<long long>(e->n_sms, units);
     schur_update_ws_kernel<ws::Big><<<grid, ws::Big::THREADS, ws::Big::SMEM, e->s>>>(ua);
@@ -1095,6 +1110,36 @@ void ll_tail(dsel_engine* e, int round, bool last, int p, int owner, int q, cons
   finish_row(e, row, s1, s2, g1, g2, bytes, flops, info);
 }
 
+// Left-looking gain input before round 1: D[q] = K(own q, own q), from the
+// resident panels or the streaming store (step 1 and gain peeks before it).
+void ll_init_d(dsel_engine* e) {
+  const int nt = e->nt;
+  if (e->stream && e->nloc > 0 && !e->hstore && !e->hk_user && e->kbf_fd < 0)
+    throw Fail{DSEL_E_STATE, "no K loaded (streaming store)"};
+  if (e->stream && e->nloc > 0) {
+    // D[q] = K(own_q, own_q)^T = K(own_q, own_q) (symmetric), from the host store;
+    // store block is row-major, D is column-major: equal for a symmetric block
+    if (e->kbf_fd >= 0) {  // diagonal blocks (s_q, s_q) from the file
+      kbf_read_blocks(e, [&](int qq) { return e->slot_sensor[qq]; }, [&](int qq) { return e->slot_sensor[qq]; });
+      CU(cudaMemcpyAsync(e->D, e->h_kstage, sizeof(double) * (size_t)e->nloc * nt * nt, cudaMemcpyHostToDevice,
+                         e->s));
+    } else {
+      h2d_blocks(e, e->D, [&](int qq) {
+        return e->hk_user  ? user_block(e, qq, e->slot_sensor[qq])
+               : packed_host_source(e) ? hpacked_block(e, qq, qq)
+                            : e->hstore + ((size_t)(qq * e->G + e->rank) * e->nloc + qq) * nt * nt;
+      }, e->s);
+    }
+    e->h2d_bytes += (uint64_t)e->nloc * nt * nt * sizeof(double);
+  } else if (e->nloc > 0) {
+    const long long total = (long long)e->nloc * nt * nt;
+    ll_init_d_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 16), 256, 0, e->s>>>(
+        e->C, e->n, nt, e->nloc, e->G, e->rank, e->D);
+    CU(cudaGetLastError());
+    e->launches += 1;
+  }
+}
+
 void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   if (e->aborted.load()) throw Fail{DSEL_E_NCCL, "aborted: a peer rank failed (dsel_abort)"};
   if (e->finished || (int)e->chosen.size() >= e->eff_budget)
@@ -1110,28 +1155,7 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
     throw Fail{DSEL_E_STATE, "no K loaded (streaming store)"};
   // ---- gains + local argmax ----
   CU(cudaEventRecord(ev[0], e->s));
-  if (e->stream && round == 0 && e->nloc > 0) {
-    // D[q] = K(own_q, own_q)^T = K(own_q, own_q) (symmetric), from the host store;
-    // store block is row-major, D is column-major: equal for a symmetric block
-    if (e->kbf_fd >= 0) {  // diagonal blocks (s_q, s_q) from the file
-      kbf_read_blocks(e, [&](int qq) { return e->slot_sensor[qq]; }, [&](int qq) { return e->slot_sensor[qq]; });
-      CU(cudaMemcpyAsync(e->D, e->h_kstage, sizeof(double) * (size_t)e->nloc * nt * nt, cudaMemcpyHostToDevice,
-                         e->s));
-    } else {
-      h2d_blocks(e, e->D, [&](int qq) {
-        return e->hk_user  ? user_block(e, qq, e->slot_sensor[qq])
-               : packed_host_source(e) ? hpacked_block(e, qq, qq)
-                            : e->hstore + ((size_t)(qq * e->G + e->rank) * e->nloc + qq) * nt * nt;
-      }, e->s);
-    }
-    e->h2d_bytes += (uint64_t)e->nloc * nt * nt * sizeof(double);
-  } else if (e->ll && round == 0 && e->nloc > 0) {
-    const long long total = (long long)e->nloc * nt * nt;
-    ll_init_d_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 16), 256, 0, e->s>>>(
-        e->C, e->n, nt, e->nloc, e->G, e->rank, e->D);
-    CU(cudaGetLastError());
-    e->launches += 1;
-  }
+  if (e->ll && round == 0) ll_init_d(e);
   const int n_batch = e->n_cols_tab;
   // the local top-2 is folded by the gain launch itself (last block); forced
   // steps and empty batches use the separate pick / argmax kernels
@@ -1461,7 +1485,7 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       ua.n_tiles = e->sym ? e->sym_tiles : ua.n_row_tiles * ua.n_col_tiles;
       ua.n_full = ua.n_tiles;
       ua.split_s = 1;
-      launch_ws(e, ua, ws_pick(e, 0, ua.n_k, false));
+      launch_ws(e, ua, e->rl_cfg);
     } else {
       UpdateArgs ua{};
       ua.C = e->C;
@@ -1604,7 +1628,7 @@ void apply_plan(dsel_engine* e, const dsel_config* cfg, bool ll, bool stream) {
   e->full_panels = !e->packed;
   e->c_elems = (size_t)e->geom().total(e->nloc);
   e->c_pad = e->packed ? (size_t)e->n : 0;
-  e->mpad = round_up((int)e->n, ws::BR);
+  e->mpad = round_up((int)e->n, ws::ROW_PAD);
   e->hpacked = stream && e->G == 1;
 }
 
@@ -1729,8 +1753,9 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
       CU(cudaEventCreateWithFlags(&e->ev_copy[b], cudaEventDisableTiming));
       CU(cudaEventCreateWithFlags(&e->ev_scat[b], cudaEventDisableTiming));
     }
-    if (const char* wc = getenv("DSEL_WS_CFG")) e->ws_cfg = std::max(-1, std::min(2, atoi(wc)));
-    e->ws_br = e->ws_cfg == 1 ? 64 : 128;
+    if (const char* wc = getenv("DSEL_WS_CFG")) e->ws_cfg = std::max(-1, std::min(3, atoi(wc)));
+    e->rl_cfg = e->ws_cfg >= 0 ? e->ws_cfg : 0;
+    e->ws_br = cfg_br(e->rl_cfg);
     if (const char* wg = getenv("DSEL_WS_GROUP")) e->ws_group = std::max(1, atoi(wg));
     // the storage plan decides every allocation below. AUTO: K resident in
     // HBM with the requested algorithm when that fits the budget, else the
@@ -1760,7 +1785,7 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     }
     if (e->keep) e->K0 = dmalloc<double>(shard, tot);
     if (e->nt % 2 && !e->ll) e->W = dmalloc<double>((size_t)e->n * e->ldw, tot);  // odd-nt update path
-    e->mpad = round_up((int)e->n, ws::BR);
+    e->mpad = round_up((int)e->n, ws::ROW_PAD);
     if (e->ll) {
       // left-looking: no resident conditional covariance, no right-looking W
     } else if (e->nt % 2 == 0) {
@@ -2596,7 +2621,7 @@ void gen_device_stream(dsel_engine* e, int vrank, double sigma, uint64_t seed) {
   const int R = e->n_rows_tab, n_rows = R * nt;
   const size_t n2 = (size_t)nt * nt, panel = (size_t)e->n * nt;
   constexpr int kch = 512;  // rank columns per update launch
-  const int mpad = round_up(std::max(n_rows, 1), ws::BR);
+  const int mpad = round_up(std::max(n_rows, 1), ws::ROW_PAD);
   size_t free_b = 0, total_b = 0;
   CU(cudaMemGetInfo(&free_b, &total_b));
   const size_t fixed = ((size_t)mpad * kch + (size_t)e->nc * n2) * sizeof(double) + (4ull << 30);
@@ -2604,7 +2629,7 @@ void gen_device_stream(dsel_engine* e, int vrank, double sigma, uint64_t seed) {
   const int cp = (int)std::max<size_t>(1, std::min<size_t>((size_t)std::max(e->nloc, 1), room / (panel * sizeof(double))));
   DevScratch<double> chunk((size_t)cp * panel), vt((size_t)mpad * kch), packed((size_t)e->nc * n2);
   const bool sym = e->hpacked;  // the packed store keeps the block-lower half only
-  const int br = ws::BR;
+  const int br = e->ws_br;
   const int nct_max = (cp * nt + ws::BC - 1) / ws::BC;
   const int ng_max = (nct_max + e->ws_group - 1) / e->ws_group;
   std::vector<int> h_tabs(2 * (size_t)cp + nct_max + ng_max + 1);
@@ -2664,7 +2689,7 @@ void gen_device_stream(dsel_engine* e, int vrank, double sigma, uint64_t seed) {
       ua.n_tiles = sym ? sym_tiles : nrt * nct;
       ua.n_full = ua.n_tiles;
       ua.split_s = 1;
-      launch_ws(e, ua, ws_pick(e, 0, ua.n_k, false));
+      launch_ws(e, ua, gen_cfg(e, ua.n_k));
     }
     for (int h = 0; h < c; ++h) CU(store_panel_d2h(e, chunk.p + (size_t)h * panel, e->n, q0 + h, packed.p));
     CU(cudaStreamSynchronize(e->s));
@@ -2697,7 +2722,7 @@ dsel_status dsel_gen_synthetic_device(dsel_engine* e, int rank, double sigma, ui
       CU(cudaGetLastError());
     }
     constexpr int kch = 512;  // rank columns per update launch
-    const int mpad = round_up(std::max(n_rows, 1), ws::BR);
+    const int mpad = round_up(std::max(n_rows, 1), ws::ROW_PAD);
     DevScratch<double> vt_buf((size_t)mpad * kch);
     double* Vt = vt_buf.p;
     cudaError_t ce = cudaSuccess;
@@ -2730,7 +2755,7 @@ dsel_status dsel_gen_synthetic_device(dsel_engine* e, int rank, double sigma, ui
       ua.n_tiles = sym ? e->sym_tiles : ua.n_row_tiles * ua.n_col_tiles;
       ua.n_full = ua.n_tiles;
       ua.split_s = 1;
-      launch_ws(e, ua, ws_pick(e, 0, ua.n_k, false));
+      launch_ws(e, ua, gen_cfg(e, ua.n_k));
       ce = cudaGetLastError();
       gen_flops += 2.0 * kch * (sym ? 0.5 * (double)n_rows * (n_cols + nt) : (double)n_rows * n_cols);
     }
@@ -2846,6 +2871,7 @@ dsel_status dsel_run(dsel_engine* e, int* n_done) {
 dsel_status dsel_peek_gains(dsel_engine* e, double* gains_by_sensor) {
   return guard(e, [&] {
     CU(cudaSetDevice(e->dev));
+    if (e->ll && e->chosen.empty()) ll_init_d(e);
     const int n_batch = e->n_cols_tab;
     run_gain(e, e->col_slot(), n_batch);
     std::vector<double> g(n_batch);

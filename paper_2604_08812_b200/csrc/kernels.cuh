@@ -357,8 +357,14 @@ struct Cfg {
 using Big = Cfg<128, 2, 3, 1>;
 using Pair = Cfg<64, 2, 2, 2>;
 using Big4 = Cfg<128, 3, 2, 1>;
+// Big6: 192-row tiles, 12 consumer warps (3 per SM sub-partition: one warp
+// stalled on a fragment load or a barrier leaves two to keep the DMMA pipe
+// fed), 1 chunk x 3 stages; registers capped at 152 per thread
+using Big6 = Cfg<192, 1, 3, 1>;
+constexpr int ROW_PAD = 384;  // lcm of the tile heights: tiled W buffers are padded to it
 static_assert(Big::SMEM <= 232448 - 2048, "ws kernel shared memory (1 CTA/SM)");
 static_assert(Big4::SMEM <= 232448 - 2048, "ws kernel shared memory (Big4)");
+static_assert(Big6::SMEM <= 232448 - 2048, "ws kernel shared memory (Big6)");
 static_assert(2 * (Pair::SMEM + 2048) <= 233472, "ws kernel shared memory (2 CTAs/SM)");
 constexpr int THREADS = Big::THREADS;
 constexpr size_t SMEM = Big::SMEM;
@@ -2158,12 +2164,20 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 }
 
 // abort: host-mapped word set by dsel_abort when a peer rank failed, so no
-// spin-wait outlives the run it belongs to
+// spin-wait outlives the run it belongs to. It is read over PCIe, so only
+// every 4096th spin (a flood of host reads from every waiting block would
+// slow the wait itself)
+__device__ __forceinline__ bool spin_until(const unsigned long long* flag, unsigned long long v,
+                                           const volatile int* abort) {
+  unsigned it = 0;
+  while (ld_acquire_sys(flag) < v)
+    if ((++it & 4095u) == 0 && *abort) return false;
+  return true;
+}
+
 __global__ void p2p_wait_kernel(const unsigned long long* flag, unsigned long long v,
                                 const volatile int* abort) {
-  if (threadIdx.x == 0)
-    while (ld_acquire_sys(flag) < v && !*abort) {
-    }
+  if (threadIdx.x == 0) spin_until(flag, v, abort);
 }
 
 // All-gather-v fused with the scatter: element pairs (j, r, c..c+1) of the
@@ -2177,15 +2191,7 @@ __global__ void w_peer_scatter_kernel(const double* const* peer_w, unsigned long
   __shared__ int s_abort;
   if (threadIdx.x == 0) s_abort = 0;
   __syncthreads();
-  if (threadIdx.x < G) {
-    const unsigned long long* f = peer_flag[threadIdx.x];
-    while (ld_acquire_sys(f) < seq) {
-      if (*abort) {
-        s_abort = 1;
-        break;
-      }
-    }
-  }
+  if (threadIdx.x < G && !spin_until(peer_flag[threadIdx.x], seq, abort)) s_abort = 1;
   __syncthreads();
   if (s_abort) return;
   const int half = nt / 2;
