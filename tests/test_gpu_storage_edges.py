@@ -318,3 +318,31 @@ def test_packed_host_store_device_generated_k(dsel):
     for x, y in zip(rs, rh):
         assert gain_close(x["gain"], y["gain"], 1e-12)
     assert st["io_ms"] > 0
+
+
+def test_repeated_runs_bit_identical(dsel, golden_dir):
+    """Race evidence without compute-sanitizer (closed on this pool): the
+    warp-specialized mbarrier pipelines, the fused last-block argmax and the
+    split-k reductions must give bit-identical gains on every repetition. A
+    shared-memory race or a missing barrier shows up as run-to-run noise."""
+    for name, kws in (("c1.json", [dict(), dict(algorithm="left"), dict(algorithm="left", storage="stream")]),
+                      ("c3mini.json", [dict(), dict(algorithm="left")])):
+        g = golden(golden_dir, name)
+        nd, nt, rk, b = g["n_sensors"], g["n_steps"], g["rank"], g["budget"]
+        v = dsel.synthetic_v(nd, nt, rk, g["seed"])
+        for kw in kws:
+            runs = []
+            with dsel.Engine(nd, nt, b, keep_pristine=True, **kw) as eng:
+                eng.gen_synthetic(v, rk, g["sigma"])
+                for rep in range(5):
+                    if rep:
+                        eng.reset()
+                    for _ in range(b):
+                        gains = eng.peek_gains()  # every remaining candidate, then the step
+                        info = eng.step()
+                        runs.append((rep, tuple(np.nan_to_num(gains).view(np.uint64)),
+                                     info["chosen_index"], np.float64(info["gain"]).view(np.uint64)))
+            per = len(runs) // 5
+            first = [r[1:] for r in runs[:per]]
+            for rep in range(1, 5):
+                assert [r[1:] for r in runs[rep * per:(rep + 1) * per]] == first, (name, kw, rep)

@@ -33,5 +33,6 @@ print(json.dumps({"time_to_k_ms": st["time_to_k_ms"], "update_ms": st["update_ms
                   "update_tflops": st["update_flops"] / st["update_ms"] / 1e9,
                   "phase_ms": tot, "launches": st["kernel_launches"],
                   "first_rounds": [{k: round(r[k], 4) for k in ("ms_gain", "ms_exchange", "ms_panel", "ms_update")} for r in rows[:3]],
-                  "last_rounds": [{k: round(r[k], 4) for k in ("ms_gain", "ms_exchange", "ms_panel", "ms_update")} for r in rows[-3:]]}, indent=1))
+                  "last_rounds": [{k: round(r[k], 4) for k in ("ms_gain", "ms_exchange", "ms_panel", "ms_update")} for r in rows[-3:]],
+                  "update_flops_per_round": [r["update_flops"] for r in rows]}, indent=1))
 eng.close()
