@@ -151,7 +151,8 @@ T* dmalloc(size_t count, uint64_t& total) {
   return static_cast<T*>(p);
 }
 
-constexpr int kEv = 8;  // 0-4 phases; 5,6 streamed H2D start/end (copy stream); 7 GEMM end
+constexpr int kEv = 10;  // 0-4 phases; 5,6 streamed H2D start/end (copy stream); 7 GEMM end;
+                        // 8,9 look-ahead bulk start/end (bulk stream)
 
 }  // namespace
 
@@ -257,6 +258,30 @@ struct dsel_engine {
   unsigned* d_counter = nullptr;  // gain-launch ticket for the fused argmax (zero between launches)
   int* d_round = nullptr;  // per-round tables (one block, one upload): d_tab | d_sym | d_hb
   int* h_round = nullptr;  // pinned staging of the same layout
+  // look-ahead rounds (symmetric right-looking, Nt a multiple of the tile):
+  // round t's bulk update runs on s2 beside round t+1's chain (gains, argmax,
+  // W solve), which only needs the diagonal blocks (updated first) and the
+  // next chosen row/column (updated once it is known). Tables and W are
+  // double-buffered: the bulk of round t reads buffer t%2 while round t+1 fills
+  // the other one.
+  bool la = false;
+  int la_reserve = 16;         // SMs left to the chain while a bulk runs
+  int prio_least = 0;          // stream priority of the bulk stream
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t ev_wrdy[2] = {nullptr, nullptr}, ev_bulk[2] = {nullptr, nullptr};
+  bool bulk_pending[2] = {false, false};
+  int* d_round_b[2] = {nullptr, nullptr};
+  int* h_round_b[2] = {nullptr, nullptr};
+  double *Wt_b[2] = {nullptr, nullptr}, *Wnt_b[2] = {nullptr, nullptr};
+  int2 *d_lists = nullptr, *h_lists = nullptr;  // [2][list_cap] tile lists (cross | diagonal)
+  size_t list_cap = 0;
+  int rbuf = 0;                // buffer of the current round
+  bool prev_valid = false;     // the previous round's bulk is still to run
+  size_t n_tab_ints = 0, n_sym_ints = 0, n_hb_ints = 0;  // table block layout
+  int prev_R = 0, prev_Rl = 0, prev_sym_tiles = 0;
+  double prev_bulk_flops = 0.0;  // full block-lower flops of that round minus its diagonal blocks
+  unsigned long long seq2 = 0;   // panel-ready flag sequence (flag[1])
+  std::vector<char> bulk_round;  // rounds whose ev[8..9] hold a bulk span
   size_t round_ints = 0;
   int* d_tab = nullptr;  // [row_pos nc | col_slot nloc | col_g nloc]
   ArgRec *d_rec = nullptr, *d_recs = nullptr;
@@ -358,6 +383,30 @@ void build_tables(dsel_engine* e, bool upload = true) {
   if (upload)
     CU(cudaMemcpyAsync(e->d_tab, e->h_tab, sizeof(int) * (size_t)(e->nc + 2 * e->nloc),
                        cudaMemcpyHostToDevice, e->s));
+}
+
+// point the round tables (and, with look-ahead, the tiled W operands) at buffer b
+void set_round_buf(dsel_engine* e, int b) {
+  e->rbuf = b;
+  e->d_round = e->d_round_b[b];
+  e->h_round = e->h_round_b[b];
+  e->d_tab = e->d_round;
+  e->h_tab = e->h_round;
+  e->d_sym = e->h_sym = nullptr;
+  if (e->n_sym_ints) {
+    e->d_sym = e->d_round + e->n_tab_ints;
+    e->h_sym = e->h_round + e->n_tab_ints;
+  }
+  if (e->n_hb_ints) {
+    e->d_hb = e->d_round + e->n_tab_ints + e->n_sym_ints;
+    e->h_hb = e->h_round + e->n_tab_ints + e->n_sym_ints;
+    e->d_hbpos = e->d_hb + e->nc;
+    e->d_hboff = e->d_hb + 2 * (size_t)e->nc;
+  }
+  if (e->Wt_b[b]) {
+    e->Wt = e->Wt_b[b];
+    e->Wnt = e->Wnt_b[b];
+  }
 }
 
 // every per-round table (row/col, tile schedule, holder lists) in one copy
@@ -722,22 +771,26 @@ int ws_pick(const dsel_engine* e, int r_rows, int n_k, bool fixed_rows) {
   return n_k >= 16 ? 2 : 0;
 }
 
-void launch_ws(dsel_engine* e, UpdateWSArgs& ua, int cfg) {
+// sms: SMs the persistent grid may occupy (0 = all; the look-ahead bulk leaves
+// some to the next round's chain); st: stream (null = the compute stream)
+void launch_ws(dsel_engine* e, UpdateWSArgs& ua, int cfg, int sms = 0, cudaStream_t st = nullptr) {
   ua.br = cfg_br(cfg);
   const long long units = (long long)ua.n_full + (long long)(ua.n_tiles - ua.n_full) * ua.split_s;
   if (units <= 0) return;
+  if (!st) st = e->s;
+  if (sms <= 0) sms = e->n_sms;
   if (cfg == 1) {
-    const int grid = (int)std::min<long long>(2LL * e->n_sms, units);
-    schur_update_ws_kernel<ws::Pair><<<grid, ws::Pair::THREADS, ws::Pair::SMEM, e->s>>>(ua);
+    const int grid = (int)std::min<long long>(2LL * sms, units);
+    schur_update_ws_kernel<ws::Pair><<<grid, ws::Pair::THREADS, ws::Pair::SMEM, st>>>(ua);
   } else if (cfg == 2) {
-    const int grid = (int)std::min<long long>(e->n_sms, units);
-    schur_update_ws_kernel<ws::Big4><<<grid, ws::Big4::THREADS, ws::Big4::SMEM, e->s>>>(ua);
+    const int grid = (int)std::min<long long>(sms, units);
+    schur_update_ws_kernel<ws::Big4><<<grid, ws::Big4::THREADS, ws::Big4::SMEM, st>>>(ua);
   } else if (cfg == 3) {
-    const int grid = (int)std::min<long long>(e->n_sms, units);
-    schur_update_ws_kernel<ws::Big6><<<grid, ws::Big6::THREADS, ws::Big6::SMEM, e->s>>>(ua);
+    const int grid = (int)std::min<long long>(sms, units);
+    schur_update_ws_kernel<ws::Big6><<<grid, ws::Big6::THREADS, ws::Big6::SMEM, st>>>(ua);
   } else {
-    const int grid = (int)std::min<long long>(e->n_sms, units);
-    schur_update_ws_kernel<ws::Big><<<grid, ws::Big::THREADS, ws::Big::SMEM, e->s>>>(ua);
+    const int grid = (int)std::min<long long>(sms, units);
+    schur_update_ws_kernel<ws::Big><<<grid, ws::Big::THREADS, ws::Big::SMEM, st>>>(ua);
   }
   CU(cudaGetLastError());
 }
@@ -1140,6 +1193,125 @@ void ll_init_d(dsel_engine* e) {
   }
 }
 
+// The right-looking update of the current round tables and W (block-lower
+// schedule under symmetric storage).
+UpdateWSArgs round_update_args(dsel_engine* e) {
+  const int nt = e->nt, n_rows = e->n_rows_tab * nt, n_cols = e->n_cols_tab * nt;
+  UpdateWSArgs ua{};
+  ua.C = e->C;
+  ua.geom = e->geom();
+  ua.Wt = e->Wt;
+  ua.Wnt = e->Wnt;
+  ua.mpad = e->mpad;
+  ua.n_k = e->ldw / ws::KC;
+  ua.row_pos = e->row_pos();
+  ua.col_slot = e->col_slot();
+  ua.col_g = e->col_g();
+  ua.nt = nt;
+  ua.n_rows = n_rows;
+  ua.n_cols = n_cols;
+  ua.n_row_tiles = (n_rows + e->ws_br - 1) / e->ws_br;
+  ua.n_col_tiles = (n_cols + ws::BC - 1) / ws::BC;
+  ua.group = e->ws_group;
+  ua.sym = e->sym;
+  ua.first_rt = e->d_sym;
+  ua.gprefix = e->d_sym ? e->d_sym + ua.n_col_tiles : nullptr;
+  ua.n_groups = (ua.n_col_tiles + e->ws_group - 1) / e->ws_group;
+  ua.n_tiles = e->sym ? e->sym_tiles : ua.n_row_tiles * ua.n_col_tiles;
+  ua.n_full = ua.n_tiles;
+  ua.split_s = 1;
+  return ua;
+}
+
+// Look-ahead, once round t's winner (position p) is known: the bulk of round
+// t-1 (its block-lower tiles minus the diagonal blocks and the new winner's
+// row/column) goes to the bulk stream on all SMs but la_reserve; the winner's
+// row block in this rank's panels and, at the owner, its panel below the
+// diagonal are updated with W_{t-1} on the compute stream -- round t's W solve
+// reads exactly those. Uses the current (round t-1) tables and W buffer.
+void la_bulk_and_cross(dsel_engine* e, int p, int q, int owner, int round, cudaEvent_t* ev) {
+  const int nt = e->nt, R = e->n_rows_tab, Rl = e->n_cols_tab;
+  const int* rp = e->h_tab;
+  const int* cs = e->h_tab + e->nc;
+  const int* rpe = std::lower_bound(rp, rp + R, p);
+  if (rpe == rp + R || *rpe != p) throw Fail{DSEL_E_STATE, "look-ahead: the winner is not a live row"};
+  const int gk = (int)(rpe - rp);
+  int hk = -1;
+  if (owner == e->rank)
+    for (int h = 0; h < Rl; ++h)
+      if (cs[h] == q) hk = h;
+  const int pb = e->rbuf, nb = 1 - pb;
+  if (Rl > 0) {  // the bulk of round t-1 (waits for W_{t-1}, recorded after its diagonal blocks)
+    CU(cudaStreamWaitEvent(e->s2, e->ev_wrdy[pb], 0));
+    CU(cudaEventRecord(ev[8], e->s2));
+    UpdateWSArgs ua = round_update_args(e);
+    ua.la_mode = 1;
+    ua.excl_g = gk;
+    ua.excl_h = hk;
+    launch_ws(e, ua, e->rl_cfg, e->n_sms - e->la_reserve, e->s2);
+    CU(cudaEventRecord(ev[9], e->s2));
+    e->bulk_round.push_back((char)1);
+    e->launches += 1;
+  } else {
+    e->bulk_round.push_back((char)0);
+  }
+  CU(cudaEventRecord(e->ev_bulk[pb], e->s2));
+  e->bulk_pending[pb] = true;
+  // the winner's row/column: round t-2's bulk (other buffer) has finished with it
+  if (e->bulk_pending[nb]) CU(cudaStreamWaitEvent(e->s, e->ev_bulk[nb], 0));
+  const int rtpb = nt / e->ws_br, ctpb = nt / ws::BC;
+  int2* L = e->h_lists + (size_t)nb * e->list_cap;
+  int nl = 0;
+  for (int h = 0; h < Rl; ++h) {  // block (k, j) of own panels j above k
+    if (cs[h] * e->G + e->rank >= p) continue;
+    for (int a = 0; a < rtpb; ++a)
+      for (int b = 0; b < ctpb; ++b) L[nl++] = make_int2(gk * rtpb + a, h * ctpb + b);
+  }
+  if (hk >= 0)  // the owner: panel k below its diagonal block
+    for (int g = gk + 1; g < R; ++g)
+      for (int a = 0; a < rtpb; ++a)
+        for (int b = 0; b < ctpb; ++b) L[nl++] = make_int2(g * rtpb + a, hk * ctpb + b);
+  if (nl > 0) {
+    int2* dL = e->d_lists + (size_t)nb * e->list_cap;
+    CU(cudaMemcpyAsync(dL, L, sizeof(int2) * nl, cudaMemcpyHostToDevice, e->s));
+    UpdateWSArgs ua = round_update_args(e);
+    ua.sym = 0;
+    ua.la_mode = 2;
+    ua.tlist = dL;
+    ua.n_tiles = ua.n_full = nl;
+    launch_ws(e, ua, e->rl_cfg);
+    e->launches += 1;
+  }
+  e->update_flops += e->prev_bulk_flops;  // bulk + cross = round t-1 minus its diagonal blocks
+  if (e->G > 1 && e->p2p) {
+    // peers read panel k below the diagonal over NVLink in round t's W solve:
+    // the owner publishes that its strip is updated (flag word 1)
+    ++e->seq2;
+    if (owner == e->rank) {
+      p2p_signal_kernel<<<1, 32, 0, e->s>>>(e->flag + 1, e->seq2);
+      CU(cudaGetLastError());
+    }
+  }
+  (void)round;
+}
+
+// Look-ahead: finish the pending round's bulk now (diagonal blocks excluded --
+// already done), so C is the full conditional covariance (read_block_row).
+void la_flush(dsel_engine* e) {
+  if (!e->la || !e->prev_valid) return;
+  if (e->n_cols_tab > 0) {
+    CU(cudaStreamWaitEvent(e->s2, e->ev_wrdy[e->rbuf], 0));
+    UpdateWSArgs ua = round_update_args(e);
+    ua.la_mode = 1;
+    ua.excl_g = -1;
+    ua.excl_h = -1;
+    launch_ws(e, ua, e->rl_cfg, 0, e->s2);
+    e->update_flops += e->prev_bulk_flops;
+  }
+  CU(cudaStreamSynchronize(e->s2));
+  e->prev_valid = false;
+}
+
 void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   if (e->aborted.load()) throw Fail{DSEL_E_NCCL, "aborted: a peer rank failed (dsel_abort)"};
   if (e->finished || (int)e->chosen.size() >= e->eff_budget)
@@ -1245,6 +1417,12 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       bytes += (uint64_t)(e->n + nt) * nt * sizeof(double) * (uint64_t)(e->G - 1);
     }
   }
+  if (e->la) {
+    if (e->prev_valid && !last) la_bulk_and_cross(e, p, q, owner, round, ev);
+    else e->bulk_round.push_back((char)0);
+    e->prev_valid = false;
+    set_round_buf(e, 1 - e->rbuf);  // round t's tables and W go to the other buffer
+  }
   e->alive[p] = 0;
   e->n_alive -= 1;
   g_probe.mark("pre", e->s);
@@ -1340,6 +1518,10 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
     g_probe.mark("trinv", e->s);
     const bool dist_w = e->sym && e->G > 1;
     const int n_own_rows = dist_w ? (e->hb_off[e->rank + 1] - e->hb_off[e->rank]) * nt : R * nt;
+    if (dist_w && e->la && e->p2p && owner != e->rank && e->seq2 > 0) {
+      p2p_wait_kernel<<<1, 32, 0, e->s>>>(e->peer_flag[owner] + 1, e->seq2, e->d_abort);
+      CU(cudaGetLastError());
+    }
     if (dist_w && n_own_rows > 0) {
       // W rows of the blocks this rank holds, packed (row-major, ld = ldw)
       PanelArgs pa{};
@@ -1459,32 +1641,40 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   g_probe.mark("hist", e->s);
   CU(cudaEventRecord(ev[3], e->s));
   g_probe.dump(e->rank);
-  if (!last && R > 0 && Rl > 0) {
+  if (!last && R > 0 && Rl > 0 && e->la) {
+    // look-ahead: only the diagonal blocks now (the next round's gains need
+    // them); the bulk runs beside the next round's chain (la_bulk_and_cross)
+    const int* cg = e->h_tab + e->nc + e->nloc;
+    const int rtpb = nt / e->ws_br, ctpb = nt / ws::BC;
+    const int nb = e->rbuf;
+    int2* L = e->h_lists + (size_t)nb * e->list_cap + e->list_cap / 2;
+    int nl = 0;
+    for (int h = 0; h < Rl; ++h)
+      for (int a = 0; a < rtpb; ++a)
+        for (int b = 0; b < ctpb; ++b) L[nl++] = make_int2(cg[h] * rtpb + a, h * ctpb + b);
+    int2* dL = e->d_lists + (size_t)nb * e->list_cap + e->list_cap / 2;
+    CU(cudaMemcpyAsync(dL, L, sizeof(int2) * nl, cudaMemcpyHostToDevice, e->s));
+    UpdateWSArgs ua = round_update_args(e);
+    ua.sym = 0;
+    ua.la_mode = 2;
+    ua.tlist = dL;
+    ua.n_tiles = ua.n_full = nl;
+    launch_ws(e, ua, e->rl_cfg);
+    e->launches += 1;
+    CU(cudaEventRecord(e->ev_wrdy[nb], e->s));  // W_t and the round-t tables are final
+    double blocks = 0.0;
+    for (int h = 0; h < Rl; ++h) blocks += (double)(R - cg[h]);
+    const double n3 = 2.0 * (double)nt * nt * nt;
+    flops = n3 * Rl;  // the diagonal blocks; the rest is counted when the bulk runs
+    e->update_flops += flops;
+    e->prev_valid = true;
+    e->prev_bulk_flops = n3 * (blocks - Rl);
+  } else if (!last && R > 0 && Rl > 0) {
     const int n_rows = R * nt, n_cols = Rl * nt;
+    (void)n_rows;
+    (void)n_cols;
     if (nt % 2 == 0) {
-      UpdateWSArgs ua{};
-      ua.C = e->C;
-      ua.geom = e->geom();
-      ua.Wt = e->Wt;
-      ua.Wnt = e->Wnt;
-      ua.mpad = e->mpad;
-      ua.n_k = e->ldw / ws::KC;
-      ua.row_pos = e->row_pos();
-      ua.col_slot = e->col_slot();
-      ua.col_g = e->col_g();
-      ua.nt = nt;
-      ua.n_rows = n_rows;
-      ua.n_cols = n_cols;
-      ua.n_row_tiles = (n_rows + e->ws_br - 1) / e->ws_br;
-      ua.n_col_tiles = (n_cols + ws::BC - 1) / ws::BC;
-      ua.group = e->ws_group;
-      ua.sym = e->sym;
-      ua.first_rt = e->d_sym;
-      ua.gprefix = e->d_sym + ua.n_col_tiles;
-      ua.n_groups = (ua.n_col_tiles + e->ws_group - 1) / e->ws_group;
-      ua.n_tiles = e->sym ? e->sym_tiles : ua.n_row_tiles * ua.n_col_tiles;
-      ua.n_full = ua.n_tiles;
-      ua.split_s = 1;
+      UpdateWSArgs ua = round_update_args(e);
       launch_ws(e, ua, e->rl_cfg);
     } else {
       UpdateArgs ua{};
@@ -1560,18 +1750,31 @@ void destroy_impl(dsel_engine* e) {
   if (e->s) cudaStreamSynchronize(e->s);
   if (e->cs) cudaStreamSynchronize(e->cs);
   for (auto ev : e->ev) cudaEventDestroy(ev);
-  double* dptr[] = {e->cpart, e->Wown, e->Wkn, e->D, e->cbuf, e->ldiag, e->Craw, e->K0, e->W, e->Wn, e->Wt, e->Wnt, e->Pbuf, e->Lk, e->Linv, e->Lscr, e->gains, e->hist,
+  double* dptr[] = {e->cpart, e->Wown, e->Wkn, e->D, e->cbuf, e->ldiag, e->Craw, e->K0, e->W, e->Wn,
+                    e->Wt_b[0] ? e->Wt_b[0] : e->Wt, e->Wnt_b[0] ? e->Wnt_b[0] : e->Wnt, e->Pbuf, e->Lk, e->Linv, e->Lscr, e->gains, e->hist,
                     e->kgain, e->stage, e->xbuf};
   for (double* d : dptr)
     if (d) cudaFree(d);
-  int* iptr[] = {e->status, e->kstatus, e->d_pos_sensor, e->d_slot_sensor, e->d_round, e->d_iota};
+  int* iptr[] = {e->status, e->kstatus, e->d_pos_sensor, e->d_slot_sensor, e->d_round_b[0], e->d_iota};
   for (int* d : iptr)
     if (d) cudaFree(d);
   if (e->d_rec) cudaFree(e->d_rec);
   if (e->d_counter) cudaFree(e->d_counter);
   if (e->d_recs) cudaFree(e->d_recs);
   if (e->h_recs) cudaFreeHost(e->h_recs);
-  if (e->h_round) cudaFreeHost(e->h_round);
+  if (e->s2) cudaStreamSynchronize(e->s2);
+  if (e->h_round_b[0]) cudaFreeHost(e->h_round_b[0]);
+  if (e->h_round_b[1]) cudaFreeHost(e->h_round_b[1]);
+  if (e->d_round_b[1]) cudaFree(e->d_round_b[1]);
+  if (e->Wt_b[1]) cudaFree(e->Wt_b[1]);
+  if (e->Wnt_b[1]) cudaFree(e->Wnt_b[1]);
+  if (e->d_lists) cudaFree(e->d_lists);
+  if (e->h_lists) cudaFreeHost(e->h_lists);
+  for (int b = 0; b < 2; ++b) {
+    if (e->ev_wrdy[b]) cudaEventDestroy(e->ev_wrdy[b]);
+    if (e->ev_bulk[b]) cudaEventDestroy(e->ev_bulk[b]);
+  }
+  if (e->s2) cudaStreamDestroy(e->s2);
   if (e->hstore) cudaFreeHost(e->hstore);
   if (e->hk_registered) cudaHostUnregister(e->hk_registered);
   detach_kbf(e);
@@ -1617,6 +1820,13 @@ size_t round_ints(const dsel_engine* e, size_t* tab = nullptr, size_t* sym = nul
   return n_tab + n_sym + n_hb;
 }
 
+// look-ahead tile lists per round: the next chosen row/column strip (<= all
+// local blocks + all rows below) and the diagonal blocks of the local columns
+size_t la_list_cap(const dsel_engine* e) {
+  const size_t per_block = (size_t)(e->nt / e->ws_br) * (e->nt / ws::BC);
+  return per_block * ((size_t)e->nloc + e->nc + (size_t)e->nloc) + 4;
+}
+
 // Storage plan: algorithm, residency and panel layout, and everything sized
 // from them (create_impl allocates exactly what plan_bytes counts).
 void apply_plan(dsel_engine* e, const dsel_config* cfg, bool ll, bool stream) {
@@ -1630,6 +1840,8 @@ void apply_plan(dsel_engine* e, const dsel_config* cfg, bool ll, bool stream) {
   e->c_pad = e->packed ? (size_t)e->n : 0;
   e->mpad = round_up((int)e->n, ws::ROW_PAD);
   e->hpacked = stream && e->G == 1;
+  const char* la_env = getenv("DSEL_LOOKAHEAD");
+  e->la = e->sym && !ll && e->nt % e->ws_br == 0 && e->nt % ws::BC == 0 && !(la_env && atoi(la_env) == 0);
 }
 
 uint64_t plan_bytes(const dsel_engine* e, const dsel_config* cfg) {
@@ -1664,6 +1876,12 @@ uint64_t plan_bytes(const dsel_engine* e, const dsel_config* cfg) {
     add(nloc1, 4);
   }
   add(round_ints(e), 4);
+  if (e->la) {  // second table buffer, second W buffers, tile lists
+    add(round_ints(e), 4);
+    add((uint64_t)e->mpad * ldw, 8);
+    add((uint64_t)e->mpad * ldw, 8);
+    add(2 * la_list_cap(e), 8);
+  }
   if (e->sym && e->G > 1) {
     add(n * ldw, 8);
     add(n * ldw, 8);
@@ -1744,7 +1962,12 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     CU(cudaSetDevice(e->dev));
     set_smem_limits(e->dev);
     CU(cudaDeviceGetAttribute(&e->n_sms, cudaDevAttrMultiProcessorCount, e->dev));
-    CU(cudaStreamCreateWithFlags(&e->s, cudaStreamNonBlocking));
+    // the round chain's stream outranks the look-ahead bulk stream: when both
+    // have work pending, the chain's CTAs get the SMs first
+    int prio_least = 0, prio_greatest = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest));
+    e->prio_least = prio_least;
+    CU(cudaStreamCreateWithPriority(&e->s, cudaStreamNonBlocking, prio_greatest));
     CU(cudaStreamCreateWithFlags(&e->cs, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&e->ts, cudaStreamNonBlocking));
     CU(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
@@ -1830,18 +2053,31 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     }
     e->d_round = dmalloc<int>(e->round_ints, tot);
     CU(ds_malloc_host(&e->h_round, sizeof(int) * e->round_ints));
-    e->d_tab = e->d_round;
-    e->h_tab = e->h_round;
-    if (n_sym) {
-      e->d_sym = e->d_round + n_tab;
-      e->h_sym = e->h_round + n_tab;
+    e->d_round_b[0] = e->d_round;
+    e->h_round_b[0] = e->h_round;
+    if (e->la) {
+      e->d_round_b[1] = dmalloc<int>(e->round_ints, tot);
+      CU(ds_malloc_host(&e->h_round_b[1], sizeof(int) * e->round_ints));
+      e->Wt_b[0] = e->Wt;
+      e->Wnt_b[0] = e->Wnt;
+      e->Wt_b[1] = dmalloc<double>((size_t)e->mpad * e->ldw, tot);
+      e->Wnt_b[1] = dmalloc<double>((size_t)e->mpad * e->ldw, tot);
+      CU(cudaMemsetAsync(e->Wt_b[1], 0, sizeof(double) * (size_t)e->mpad * e->ldw, e->s));
+      CU(cudaMemsetAsync(e->Wnt_b[1], 0, sizeof(double) * (size_t)e->mpad * e->ldw, e->s));
+      e->list_cap = la_list_cap(e);
+      e->d_lists = reinterpret_cast<int2*>(dmalloc<double>(2 * e->list_cap, tot));
+      CU(ds_malloc_host(&e->h_lists, sizeof(int2) * 2 * e->list_cap));
+      CU(cudaStreamCreateWithPriority(&e->s2, cudaStreamNonBlocking, e->prio_least));
+      for (int b = 0; b < 2; ++b) {
+        CU(cudaEventCreateWithFlags(&e->ev_wrdy[b], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&e->ev_bulk[b], cudaEventDisableTiming));
+      }
+      if (const char* rs = getenv("DSEL_LA_RESERVE")) e->la_reserve = std::max(0, std::min(e->n_sms - 8, atoi(rs)));
     }
-    if (n_hb) {
-      e->d_hb = e->d_round + n_tab + n_sym;
-      e->h_hb = e->h_round + n_tab + n_sym;
-      e->d_hbpos = e->d_hb + e->nc;
-      e->d_hboff = e->d_hb + 2 * (size_t)e->nc;
-    }
+    e->n_tab_ints = n_tab;
+    e->n_sym_ints = n_sym;
+    e->n_hb_ints = n_hb;
+    set_round_buf(e, 0);
     e->Lk = dmalloc<double>((size_t)e->nt * e->nt, tot);
     e->Linv = dmalloc<double>((size_t)e->ldw * e->ldw, tot);
     e->Lscr = dmalloc<double>((size_t)std::max(e->nloc, 1) * e->nt * e->nt, tot);
@@ -2263,6 +2499,7 @@ dsel_status dsel_sync(dsel_engine* e) {
   return guard(e, [&] {
     CU(cudaSetDevice(e->dev));
     CU(cudaStreamSynchronize(e->s));
+    if (e->s2) CU(cudaStreamSynchronize(e->s2));
   });
 }
 
@@ -2491,6 +2728,7 @@ dsel_status dsel_read_block_row(dsel_engine* e, int j, double* host_row) {
     if (p < 0 || p % e->G != e->rank) throw Fail{DSEL_E_RANGE, "block row not owned by this rank"};
     const int q = p / e->G;
     const size_t elems = (size_t)e->nd * e->nt * e->nt;
+    la_flush(e);
     if (e->stream) {  // K itself, from the pinned host store
       const size_t n2 = (size_t)e->nt * e->nt;
       std::memset(host_row, 0, elems * sizeof(double));
@@ -2891,6 +3129,7 @@ int dsel_get_trace(dsel_engine* e, dsel_step_info* rows, int max_rows) {
   try {
     CU(cudaSetDevice(e->dev));
     CU(cudaStreamSynchronize(e->s));
+    if (e->s2) CU(cudaStreamSynchronize(e->s2));
     const int n = std::min<int>((int)e->trace.size(), max_rows);
     for (int i = 0; i < n; ++i) {
       dsel_step_info r = e->trace[i];
@@ -2905,6 +3144,11 @@ int dsel_get_trace(dsel_engine* e, dsel_step_info* rows, int max_rows) {
       r.ms_exchange = b;
       r.ms_panel = c;
       r.ms_update = d;
+      if ((size_t)i < e->bulk_round.size() && e->bulk_round[i]) {  // the look-ahead bulk run in this step
+        float bk = 0;
+        CU(cudaEventElapsedTime(&bk, ev[8], ev[9]));
+        r.ms_update += bk;
+      }
       r.ms_round = tot;
       r.ms_io = 0.0;
       if (std::find(e->streamed_round.begin(), e->streamed_round.end(), i) != e->streamed_round.end()) {
@@ -2923,6 +3167,11 @@ int dsel_get_trace(dsel_engine* e, dsel_step_info* rows, int max_rows) {
 
 // selection state back to "nothing chosen" (the store is handled by the caller)
 static void reset_state(dsel_engine* e) {
+  if (e->s2) cudaStreamSynchronize(e->s2);
+  e->prev_valid = false;
+  e->bulk_pending[0] = e->bulk_pending[1] = false;
+  e->bulk_round.clear();
+  if (e->la) set_round_buf(e, 0);
   e->alive.assign(e->nc, 1);
   e->n_alive = e->nc;
   e->chosen.clear();
@@ -2940,6 +3189,7 @@ dsel_status dsel_reset(dsel_engine* e) {
   return guard(e, [&] {
     if (!e->keep && !e->ll) throw Fail{DSEL_E_STATE, "dsel_reset requires keep_pristine"};
     CU(cudaSetDevice(e->dev));
+    if (e->s2) CU(cudaStreamSynchronize(e->s2));  // no bulk may still write C
     if (!e->ll)  // the left-looking store is K itself and is never modified
       CU(cudaMemcpyAsync(e->C, e->K0, sizeof(double) * e->c_elems, cudaMemcpyDeviceToDevice, e->s));
     reset_state(e);
@@ -2952,6 +3202,7 @@ dsel_status dsel_get_stats(dsel_engine* e, dsel_stats* st) {
     if (!st) throw Fail{DSEL_E_INVALID, "null stats"};
     CU(cudaSetDevice(e->dev));
     CU(cudaStreamSynchronize(e->s));
+    if (e->s2) CU(cudaStreamSynchronize(e->s2));
     dsel_stats r{};
     r.rounds = (int)e->trace.size();
     r.kernel_launches = e->launches;
@@ -2977,6 +3228,10 @@ dsel_status dsel_get_stats(dsel_engine* e, dsel_stats* st) {
         float u = 0;
         CU(cudaEventElapsedTime(&u, e->ev[(size_t)i * kEv + 3], e->ev[(size_t)i * kEv + 4]));
         upd += u;
+        if ((size_t)i < e->bulk_round.size() && e->bulk_round[i]) {
+          CU(cudaEventElapsedTime(&u, e->ev[(size_t)i * kEv + 8], e->ev[(size_t)i * kEv + 9]));
+          upd += u;
+        }
       }
       r.update_ms = upd;
     }

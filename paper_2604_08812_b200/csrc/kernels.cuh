@@ -412,6 +412,15 @@ struct UpdateWSArgs {
   double* part;
   long long part_stride;
   int br;  // tile height of the launched configuration (128 or 64)
+  // look-ahead rounds (Nt a multiple of the tile sizes, so every tile lies in
+  // one block row and one block column): la_mode 1 = the block-lower schedule
+  // minus the diagonal blocks, the row block of compact block excl_g and the
+  // local column block excl_h (the bulk of a round, run beside the next
+  // round's chain); 2 = an explicit tile list tlist[n_tiles] of (row tile,
+  // column tile) (the diagonal blocks, or the next chosen row/column)
+  int la_mode;
+  int excl_g, excl_h;
+  const int2* tlist;
 };
 
 // unit -> (tile, split z, k-chunk range)
@@ -435,6 +444,12 @@ __device__ __forceinline__ void ws_unit(const UpdateWSArgs& a, int unit, int& ti
 // fr / gp: first_rt and gprefix staged in shared memory (binary search).
 __device__ __forceinline__ bool ws_tile(const UpdateWSArgs& a, const int* fr, const int* gp, int id,
                                         int& r0, int& c0) {
+  if (a.la_mode == 2) {
+    const int2 t = a.tlist[id];
+    r0 = t.x * a.br;
+    c0 = t.y * 64;
+    return true;
+  }
   if (!a.sym) {
     const int gsz = a.group * a.n_row_tiles;
     const int grp = id / gsz;
@@ -458,7 +473,12 @@ __device__ __forceinline__ bool ws_tile(const UpdateWSArgs& a, const int* fr, co
   const int ct = ct0 + local % gw;
   r0 = rt * a.br;
   c0 = ct * 64;
-  return rt >= fr[ct];
+  if (rt < fr[ct]) return false;
+  if (a.la_mode == 1) {
+    const int gr = r0 / a.nt, hc = c0 / a.nt;
+    if (gr == a.excl_g || hc == a.excl_h || gr == a.col_g[hc]) return false;
+  }
+  return true;
 }
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {

@@ -108,6 +108,36 @@ if which == "replay":
     print(f"rank {rank}/{world} replay: {'OK' if not bad else 'MISMATCH'}", flush=True)
     dist.destroy_process_group()
     sys.exit(1 if bad else 0)
+if which == "lookahead":
+    # look-ahead rounds (Nt = 128) at world size > 1: the winner's panel strip
+    # is read over NVLink after the owner's flag; gains bit-identical to the
+    # plain schedule and to one GPU
+    from oracle import oracle as O  # checker only
+    nd, nt, b = 16, 128, 8
+    k = O.random_hessian(nd, nt, 1.0, 1800, 4)
+    want = O.greedy_select(k, nd, nt, b)
+    res = {}
+    for la in ("1", "0"):
+        os.environ["DSEL_LOOKAHEAD"] = la
+        cid = [d.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(cid, src=0)
+        with d.Engine(nd, nt, b, device=local, world_size=world, rank=rank, nccl_id=cid[0]) as eng:
+            eng.load_k(k)
+            eng.run()
+            res[la] = [(r["chosen_index"], r["gain"]) for r in eng.trace()]
+    os.environ["DSEL_LOOKAHEAD"] = "1"
+    one = None
+    if rank == 0:
+        with d.Engine(nd, nt, b, device=local) as eng:
+            eng.load_k(k)
+            eng.run()
+            one = [(r["chosen_index"], r["gain"]) for r in eng.trace()]
+    box = [one]
+    dist.broadcast_object_list(box, src=0)
+    ok = (res["1"] == res["0"] == box[0] and [c for c, _ in res["1"]] == list(want.chosen))
+    print(f"rank {rank}/{world} lookahead: {'OK' if ok else 'MISMATCH'}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
 if which == "device":
     # K formed on every rank by the update kernel from the device Philox V; the
     # sequence must match the oracle on the same K (numpy V) at any world size

@@ -346,3 +346,40 @@ def test_repeated_runs_bit_identical(dsel, golden_dir):
             first = [r[1:] for r in runs[:per]]
             for rep in range(1, 5):
                 assert [r[1:] for r in runs[rep * per:(rep + 1) * per]] == first, (name, kw, rep)
+
+
+def test_lookahead_rounds_bit_identical_and_exact(dsel, O, monkeypatch):
+    """Look-ahead (Nt a multiple of the tile: the bulk of round t runs beside
+    round t+1's chain): every gain bit-identical to the plain schedule (same
+    per-element operation order), the reference sequence, and the resident C
+    after a flush equals K - K[:,S] K_SS^-1 K[S,:]."""
+    nd, nt, b = 12, 128, 6
+    k = O.random_hessian(nd, nt, 1.0, 1400, 9)
+    want = O.greedy_select(k, nd, nt, b)
+    runs = {}
+    for la in ("1", "0"):
+        monkeypatch.setenv("DSEL_LOOKAHEAD", la)
+        with dsel.Engine(nd, nt, b) as eng:
+            eng.load_k(k)
+            rows = [eng.step() for _ in range(b)]
+            st = eng.stats()
+        runs[la] = [(r["chosen_index"], np.float64(r["gain"]).view(np.uint64)) for r in rows]
+        assert [r["chosen_index"] for r in rows] == want.chosen
+        assert st["update_flops"] > 0
+    assert runs["1"] == runs["0"]
+    monkeypatch.setenv("DSEL_LOOKAHEAD", "1")
+    dense = O.blocks_to_dense(k, nd, nt)
+    with dsel.Engine(nd, nt, b) as eng:
+        eng.load_k(k)
+        S = []
+        for t in range(4):
+            S.append(eng.step()["chosen_index"])
+            if t % 2:  # read back every other round (the flush path), keep stepping after it
+                idx = np.concatenate([np.arange(s * nt, (s + 1) * nt) for s in S])
+                cond = dense - dense[:, idx] @ np.linalg.solve(dense[np.ix_(idx, idx)], dense[idx, :])
+                for j in [x for x in range(nd) if x not in S][:3]:
+                    got = eng.read_block_row(j).reshape(nd, nt, nt)
+                    for i in [x for x in range(nd) if x not in S]:
+                        ref = cond[j * nt:(j + 1) * nt, i * nt:(i + 1) * nt]
+                        np.testing.assert_allclose(got[i], ref, rtol=1e-9, atol=1e-9 * np.abs(dense).max())
+        assert S == want.chosen[:4]
