@@ -19,7 +19,9 @@ from oracle import oracle as O  # noqa: E402
 
 
 def dump(name, obj):
-    with open(os.path.join(HERE, name), "w") as f:
+    out = os.environ.get("GOLDEN_OUT", HERE)  # e.g. gpurun_out/ when generated on a GPU box's host
+    os.makedirs(out, exist_ok=True)
+    with open(os.path.join(out, name), "w") as f:
         json.dump(obj, f, indent=1)
     print("wrote", name)
 
@@ -47,6 +49,7 @@ def synthetic_case(name, nd, nt, rank, sigma, seed, budget, workers=8, replay=Fa
     ts = time.time() - t0
     path = f"/tmp/{name}.kbf"
     O.ref_write_kbf(k, nd, nt, path)
+    print(f"{name}: K {tk:.1f} s, selection {ts:.1f} s", flush=True)
     sha = hashlib.sha256(open(path, "rb").read()).hexdigest()
     os.remove(path)
     src = ("reference run_parallel_greedy<double> (oracle/_ref) on "
