@@ -254,10 +254,16 @@ def time_device(eng, args, world, clock_dev=None):
             upd_ms.append(st["update_ms"])
             upd_fl.append(st["update_flops"])
             launches.append(st["kernel_launches"])
-        chosen = [r["chosen_index"] for r in eng.trace()]
+        rows = eng.trace()
+        chosen = [r["chosen_index"] for r in rows]
     if clk:
         clk.__exit__()
-    out = {"value": sum(times) / len(times), "chosen": chosen,
+    gaps = [((r["gain"] - r["runner_up_gain"]) / max(abs(r["gain"]), 1.0), r["k"]) for r in rows
+            if r["runner_up"] >= 0]
+    near = {"tau": 1e-9, "flagged_rounds": [r["k"] for r in rows if r["near_tie"]],
+            "min_rel_top2_gap": min(gaps)[0] if gaps else None,
+            "at_round": min(gaps)[1] if gaps else None}
+    out = {"value": sum(times) / len(times), "chosen": chosen, "near_ties": near,
            "launches": int(sum(launches) / len(launches)),
            "clocks": clk.summary() if clk else None}
     upd_t = sum(upd_ms) / 1e3
@@ -419,6 +425,7 @@ def our_arm(args, world, rank, local):
                                       f"(x{tr['traffic_over_algorithmic']})") if tr else
                                      "no ncu --set full capture of this configuration committed"},
         "e2e": e2e,
+        "near_ties": prim["near_ties"],
         "gpu_launches": int(sum(launches) / len(launches)) if launches else 0,
         "clocks": clocks,
         "setup": {"v_host_s": round(t_v, 2), "k_gen_device_s": round(t_gen, 2)},

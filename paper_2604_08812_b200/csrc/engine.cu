@@ -31,6 +31,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "dsel.h"
 #include "kernels.cuh"
 #include "lti.h"
@@ -103,6 +105,19 @@ struct DevScratch {
   DevScratch(const DevScratch&) = delete;
   DevScratch& operator=(const DevScratch&) = delete;
 };
+// NVTX ranges (header-only nvtx3): one per C-ABI call that does device work and
+// one per phase of a round, so a timeline shows the host side of every round
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  void next(const char* name) {
+    nvtxRangePop();
+    nvtxRangePushA(name);
+  }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
+
 // DEBUG probes (DSEL_PROBE=1): GPU events + host times at named points of a round
 struct Probe {
   bool on = getenv("DSEL_PROBE") != nullptr;
@@ -1313,6 +1328,8 @@ void la_flush(dsel_engine* e) {
 }
 
 void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
+  Nvtx nv_step("dsel_step");
+  Nvtx nv("gains");
   if (e->aborted.load()) throw Fail{DSEL_E_NCCL, "aborted: a peer rank failed (dsel_abort)"};
   if (e->finished || (int)e->chosen.size() >= e->eff_budget)
     throw Fail{DSEL_E_STATE, "selection already finished"};
@@ -1343,6 +1360,7 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   CU(cudaEventRecord(ev[1], e->s));
 
   // ---- cross-rank argmax: 32 B per rank ----
+  nv.next("argmax exchange");
   uint64_t bytes = 0;
   if (e->G > 1) {
     NC(ncclAllGather(e->d_rec, e->d_recs, sizeof(ArgRec), ncclUint8, e->comm, e->s));
@@ -1385,6 +1403,7 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   const int p = e->sensor_pos[s1];
   const int owner = p % e->G;
   const int q = p / e->G;
+  nv.next("panel: L_k^-1, W");
 
   // ---- panel: broadcast C[:,k] and L_k = chol(C_kk) from the owner ----
   // The owner's gain kernel already factored C_kk (scratch slot bidx); every
@@ -1640,6 +1659,7 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
   }
   g_probe.mark("hist", e->s);
   CU(cudaEventRecord(ev[3], e->s));
+  nv.next("update");
   g_probe.dump(e->rank);
   if (!last && R > 0 && Rl > 0 && e->la) {
     // look-ahead: only the diagonal blocks now (the next round's gains need
@@ -1907,6 +1927,7 @@ uint64_t plan_bytes(const dsel_engine* e, const dsel_config* cfg) {
 void connect_impl(dsel_engine* e);
 
 void create_impl(const dsel_config* cfg, dsel_engine** out) {
+  Nvtx nv("dsel_create");
   if (!cfg || !out) throw Fail{DSEL_E_INVALID, "null argument"};
   if (cfg->n_sensors < 1 || cfg->n_steps < 1) throw Fail{DSEL_E_INVALID, "n_sensors and n_steps must be >= 1"};
   if (cfg->budget < 0) throw Fail{DSEL_E_INVALID, "budget must be nonnegative"};
@@ -2584,6 +2605,7 @@ dsel_status dsel_load_k(dsel_engine* e, const double* host_k) {
 namespace {
 
 void load_kbf_impl(dsel_engine* e, const char* path, bool exact_columns, int threads) {
+  Nvtx nv("dsel_load_kbf");
   const std::string ps(path ? path : "");
   const int fd = ::open(ps.c_str(), O_RDONLY);
   if (fd < 0) throw Fail{DSEL_E_IO, "cannot open " + ps + ": " + std::strerror(errno)};
@@ -2853,6 +2875,7 @@ static void reset_state(dsel_engine* e);
 // and copied to the pinned store -- the packed store needs only the
 // block-lower tiles. K never has to fit in HBM (north star (1) at C5 scale).
 void gen_device_stream(dsel_engine* e, int vrank, double sigma, uint64_t seed) {
+  Nvtx nv("gen_synthetic_device (host store)");
   const int nt = e->nt;
   reset_state(e);  // every candidate live: compact row index = position
   ensure_hstore(e);
