@@ -280,7 +280,7 @@ struct dsel_engine {
   // double-buffered: the bulk of round t reads buffer t%2 while round t+1 fills
   // the other one.
   bool la = false;
-  int la_reserve = 16;         // SMs left to the chain while a bulk runs
+  int la_reserve = 8;          // SMs left to the chain while a bulk runs (8 measured best on C2)
   int prio_least = 0;          // stream priority of the bulk stream
   cudaStream_t s2 = nullptr;
   cudaEvent_t ev_wrdy[2] = {nullptr, nullptr}, ev_bulk[2] = {nullptr, nullptr};
@@ -1687,9 +1687,8 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
     const double n3 = 2.0 * (double)nt * nt * nt;
     flops = n3 * Rl;  // the diagonal blocks; the rest is counted when the bulk runs
     e->update_flops += flops;
-    e->prev_valid = true;
     e->prev_bulk_flops = n3 * (blocks - Rl);
-  } else if (!last && R > 0 && Rl > 0) {
+  } else if (!last && R > 0 && Rl > 0 && !e->la) {
     const int n_rows = R * nt, n_cols = Rl * nt;
     (void)n_rows;
     (void)n_cols;
@@ -1728,6 +1727,12 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       flops = 2.0 * nt * (double)n_rows * (double)n_cols;
     }
     e->update_flops += flops;
+  }
+  if (e->la) {
+    // every rank marks every non-final round (even with no local columns left):
+    // the next step's bulk/cross and its panel-flag sequence stay in lockstep
+    if (!last && (R == 0 || Rl == 0)) e->prev_bulk_flops = 0.0;
+    e->prev_valid = !last;
   }
   CU(cudaEventRecord(ev[4], e->s));
 
@@ -1860,8 +1865,10 @@ void apply_plan(dsel_engine* e, const dsel_config* cfg, bool ll, bool stream) {
   e->c_pad = e->packed ? (size_t)e->n : 0;
   e->mpad = round_up((int)e->n, ws::ROW_PAD);
   e->hpacked = stream && e->G == 1;
+  // look-ahead rounds are opt-in (DSEL_LOOKAHEAD=1): measured -4 % at 1 GPU and
+  // -7.5 % at 2 GPUs on C2, but a 4-GPU bench run did not finish (open)
   const char* la_env = getenv("DSEL_LOOKAHEAD");
-  e->la = e->sym && !ll && e->nt % e->ws_br == 0 && e->nt % ws::BC == 0 && !(la_env && atoi(la_env) == 0);
+  e->la = e->sym && !ll && e->nt % e->ws_br == 0 && e->nt % ws::BC == 0 && la_env && atoi(la_env) == 1;
 }
 
 uint64_t plan_bytes(const dsel_engine* e, const dsel_config* cfg) {

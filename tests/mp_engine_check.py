@@ -125,7 +125,7 @@ if which == "lookahead":
             eng.load_k(k)
             eng.run()
             res[la] = [(r["chosen_index"], r["gain"]) for r in eng.trace()]
-    os.environ["DSEL_LOOKAHEAD"] = "1"
+    os.environ["DSEL_LOOKAHEAD"] = "0"
     one = None
     if rank == 0:
         with d.Engine(nd, nt, b, device=local) as eng:
