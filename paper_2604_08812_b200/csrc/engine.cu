@@ -1667,12 +1667,12 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
     const int* cg = e->h_tab + e->nc + e->nloc;
     const int rtpb = nt / e->ws_br, ctpb = nt / ws::BC;
     const int nb = e->rbuf;
-    int2* L = e->h_lists + (size_t)nb * e->list_cap + e->list_cap / 2;
+    int2* L = e->h_lists + (size_t)nb * e->list_cap + la_diag_off(e);
     int nl = 0;
     for (int h = 0; h < Rl; ++h)
       for (int a = 0; a < rtpb; ++a)
         for (int b = 0; b < ctpb; ++b) L[nl++] = make_int2(cg[h] * rtpb + a, h * ctpb + b);
-    int2* dL = e->d_lists + (size_t)nb * e->list_cap + e->list_cap / 2;
+    int2* dL = e->d_lists + (size_t)nb * e->list_cap + la_diag_off(e);
     CU(cudaMemcpyAsync(dL, L, sizeof(int2) * nl, cudaMemcpyHostToDevice, e->s));
     UpdateWSArgs ua = round_update_args(e);
     ua.sym = 0;
@@ -1847,9 +1847,14 @@ size_t round_ints(const dsel_engine* e, size_t* tab = nullptr, size_t* sym = nul
 
 // look-ahead tile lists per round: the next chosen row/column strip (<= all
 // local blocks + all rows below) and the diagonal blocks of the local columns
+size_t la_diag_off(const dsel_engine* e);
 size_t la_list_cap(const dsel_engine* e) {
-  const size_t per_block = (size_t)(e->nt / e->ws_br) * (e->nt / ws::BC);
-  return per_block * ((size_t)e->nloc + e->nc + (size_t)e->nloc) + 4;
+  return la_diag_off(e) + (size_t)(e->nt / e->ws_br) * (e->nt / ws::BC) * e->nloc + 2;
+}
+// the cross list (row strip over own panels <= nloc blocks, the owner's column
+// <= nc blocks) first, then the diagonal-block list
+size_t la_diag_off(const dsel_engine* e) {
+  return (size_t)(e->nt / e->ws_br) * (e->nt / ws::BC) * ((size_t)e->nloc + e->nc) + 2;
 }
 
 // Storage plan: algorithm, residency and panel layout, and everything sized
