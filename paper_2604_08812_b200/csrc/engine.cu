@@ -1210,6 +1210,16 @@ void ll_init_d(dsel_engine* e) {
 
 // The right-looking update of the current round tables and W (block-lower
 // schedule under symmetric storage).
+// look-ahead tile lists per round: the cross list (row strip over own panels
+// <= nloc blocks, the owner's column <= nc blocks) first, then the
+// diagonal-block list (<= nloc blocks)
+size_t la_diag_off(const dsel_engine* e) {
+  return (size_t)(e->nt / e->ws_br) * (e->nt / ws::BC) * ((size_t)e->nloc + e->nc) + 2;
+}
+size_t la_list_cap(const dsel_engine* e) {
+  return la_diag_off(e) + (size_t)(e->nt / e->ws_br) * (e->nt / ws::BC) * e->nloc + 2;
+}
+
 UpdateWSArgs round_update_args(dsel_engine* e) {
   const int nt = e->nt, n_rows = e->n_rows_tab * nt, n_cols = e->n_cols_tab * nt;
   UpdateWSArgs ua{};
@@ -1847,15 +1857,7 @@ size_t round_ints(const dsel_engine* e, size_t* tab = nullptr, size_t* sym = nul
 
 // look-ahead tile lists per round: the next chosen row/column strip (<= all
 // local blocks + all rows below) and the diagonal blocks of the local columns
-size_t la_diag_off(const dsel_engine* e);
-size_t la_list_cap(const dsel_engine* e) {
-  return la_diag_off(e) + (size_t)(e->nt / e->ws_br) * (e->nt / ws::BC) * e->nloc + 2;
-}
-// the cross list (row strip over own panels <= nloc blocks, the owner's column
-// <= nc blocks) first, then the diagonal-block list
-size_t la_diag_off(const dsel_engine* e) {
-  return (size_t)(e->nt / e->ws_br) * (e->nt / ws::BC) * ((size_t)e->nloc + e->nc) + 2;
-}
+
 
 // Storage plan: algorithm, residency and panel layout, and everything sized
 // from them (create_impl allocates exactly what plan_bytes counts).
