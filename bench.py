@@ -41,6 +41,9 @@ CONFIGS = {
     "c1": dict(nd=64, nt=32, rank=2048, budget=16),
     "c2": dict(nd=200, nt=128, rank=8192, budget=50),
     "c3": dict(nd=75, nt=420, rank=24576, budget=50),  # nd scaled by N
+    # BASELINE configs[3]: K = 508 GB, formed on the devices (device Philox V,
+    # rank 81,920 -- V alone is 165 GB, never on a host); needs >= 2 GPUs
+    "c4": dict(nd=600, nt=420, rank=81920, budget=175),
 }
 SIGMA, SEED = 1.0, 2024
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -307,9 +310,65 @@ def time_e2e(eng, args, world, host_rows, mine, chosen, attach=None):
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
 
+def c4_arm(args, world, rank, local):
+    """C4 (600 x Nt=420, select 175): the packed block-lower panels hold K in HBM
+    from 2 GPUs (127 GB/GPU at 2). K is formed on the devices before every step
+    (outside the timed region; there is no room for a pristine copy), so a step
+    costs ~1-2 min of setup: use --steps 1 --warmup 0 by hand. No e2e (the host
+    cannot hold K) and no CPU baseline (hours of reference work per round)."""
+    import paper_2604_08812_b200 as d
+
+    w = workload("c4", world)
+    nd, nt, vrank, budget = w["nd"], w["nt"], w["rank"], w["budget"]
+    peaks = measure_fp64_peaks(d, local)
+    peaks_min = {k: allreduce_min(x, world) for k, x in peaks.items()}
+    nid = broadcast_bytes(d.nccl_unique_id() if (world > 1 and rank == 0) else None, world)
+    eng = d.Engine(nd, nt, budget, device=local, world_size=world, rank=rank, nccl_id=nid,
+                   storage="hbm")
+    times, upd, fl, t_gen, launches = [], [], [], 0.0, 0
+    for it in range(args.warmup + args.steps):
+        barrier(world)
+        t0 = time.time()
+        eng.gen_synthetic_device(vrank, SIGMA, SEED)
+        t_gen = max(t_gen, allreduce_max(time.time() - t0, world))
+        barrier(world)
+        eng.run()
+        st = eng.stats()
+        if it >= args.warmup:
+            times.append(allreduce_max(st["time_to_k_ms"] / 1e3, world))
+            upd.append(st["update_ms"])
+            fl.append(st["update_flops"])
+            launches = st["kernel_launches"]
+    rows = eng.trace()
+    dev_gb = eng.device_bytes / 1e9
+    eng.close()
+    value = sum(times) / len(times)
+    upd_tf = sum(fl) / (sum(upd) / 1e3) / 1e12
+    line = {"metric": "time-to-k-sensors (s)", "value": round(value, 3), "unit": "s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(value * 1e3, 1),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: K = sigma^2 I + V V^T with V from the device Philox stream "
+                    "(rank 81,920; not the reference RNG stream -- V is 165 GB)",
+            "config": {**workload_config("c4", nd, nt, budget, vrank, world),
+                       "chosen_first": [r["chosen_index"] for r in rows[:8]],
+                       "objective": rows[-1]["objective"], "device_gb_per_gpu": round(dev_gb, 1),
+                       "k_formation_s": round(t_gen, 1)},
+            "roofline": {"bound": "tensor", "kernel": "schur_update_ws_kernel (DMMA.8x8x4, TMA bulk)",
+                         "achieved": round(upd_tf, 3), "peak": peaks_min["dmma_tflops"],
+                         "unit": "TFLOP/s", "frac": round(upd_tf / peaks_min["dmma_tflops"], 4),
+                         "peak_cublas_dgemm": peaks_min["cublas_dgemm_tflops"], "traffic": None},
+            "e2e": None, "e2e_note": "K (508 GB) does not fit any host here",
+            "gpu_launches": int(launches)}
+    if rank == 0:
+        emit(line)
+
+
 def our_arm(args, world, rank, local):
     import paper_2604_08812_b200 as d
 
+    if args.config == "c4":
+        c4_arm(args, world, rank, local)
+        return
     w = workload(args.config, world)
     nd, nt, vrank, budget = w["nd"], w["nt"], w["rank"], w["budget"]
     t0 = time.time()
