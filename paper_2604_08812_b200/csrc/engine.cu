@@ -1446,8 +1446,10 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
       bytes += (uint64_t)(e->n + nt) * nt * sizeof(double) * (uint64_t)(e->G - 1);
     }
   }
+  bool crossed = false;  // this round updated the winner's strip (peers wait on the owner's flag)
   if (e->la) {
-    if (e->prev_valid && !last) la_bulk_and_cross(e, p, q, owner, round, ev);
+    crossed = e->prev_valid && !last;
+    if (crossed) la_bulk_and_cross(e, p, q, owner, round, ev);
     else e->bulk_round.push_back((char)0);
     e->prev_valid = false;
     set_round_buf(e, 1 - e->rbuf);  // round t's tables and W go to the other buffer
@@ -1547,7 +1549,9 @@ void step_impl(dsel_engine* e, int forced, dsel_step_info* info) {
     g_probe.mark("trinv", e->s);
     const bool dist_w = e->sym && e->G > 1;
     const int n_own_rows = dist_w ? (e->hb_off[e->rank + 1] - e->hb_off[e->rank]) * nt : R * nt;
-    if (dist_w && e->la && e->p2p && owner != e->rank && e->seq2 > 0) {
+    // only when the owner updated its strip this round: in a round without it
+    // (round 1, after a flush) the owner's flag holds an older sequence
+    if (dist_w && crossed && e->p2p && owner != e->rank) {
       p2p_wait_kernel<<<1, 32, 0, e->s>>>(e->peer_flag[owner] + 1, e->seq2, e->d_abort);
       CU(cudaGetLastError());
     }
