@@ -121,10 +121,15 @@ if which == "lookahead":
         os.environ["DSEL_LOOKAHEAD"] = la
         cid = [d.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(cid, src=0)
-        with d.Engine(nd, nt, b, device=local, world_size=world, rank=rank, nccl_id=cid[0]) as eng:
+        with d.Engine(nd, nt, b, device=local, world_size=world, rank=rank, nccl_id=cid[0],
+                      keep_pristine=True) as eng:
             eng.load_k(k)
-            eng.run()
-            res[la] = [(r["chosen_index"], r["gain"]) for r in eng.trace()]
+            runs = []
+            for _ in range(3):  # reruns after dsel_reset: the flag sequences carry over
+                eng.reset()
+                eng.run()
+                runs.append([(r["chosen_index"], r["gain"]) for r in eng.trace()])
+            res[la] = runs[0] if runs[0] == runs[1] == runs[2] else None
     os.environ["DSEL_LOOKAHEAD"] = "0"
     one = None
     if rank == 0:
