@@ -398,16 +398,32 @@ def our_arm(args, world, rank, local):
                 hv[idx * row_elems:(idx + 1) * row_elems] = src.read_block_row(j)
         host_rows = [host[idx * row_elems:(idx + 1) * row_elems] for idx in range(len(mine))]
     engines, t_gen = {}, 0.0
-    for a in algos:  # every engine gets the same bit-exact K, then V is released
+    # the right-looking update under the look-ahead schedule (default when Nt is a
+    # multiple of the tile) and, beside it, the plain schedule: the same kernel on
+    # every SM, which is where the roofline of the update kernel is read
+    la_ok = nt % 128 == 0 and os.environ.get("DSEL_LOOKAHEAD", "1") != "0"
+    builds = list(algos) + (["plain"] if la_ok and "right" in algos else [])
+    for a in builds:  # every engine gets the same bit-exact K, then V is released
         nid = broadcast_bytes(d.nccl_unique_id() if (world > 1 and rank == 0) else None, world)
+        prev_la = os.environ.get("DSEL_LOOKAHEAD")
+        os.environ["DSEL_LOOKAHEAD"] = "0" if a == "plain" else (prev_la or "1")
         engines[a] = d.Engine(nd, nt, budget, device=local, world_size=world, rank=rank,
-                              nccl_id=nid, keep_pristine=True, export_factor=True, algorithm=a)
+                              nccl_id=nid, keep_pristine=True, export_factor=True,
+                              algorithm="right" if a == "plain" else a)
+        if prev_la is None:
+            del os.environ["DSEL_LOOKAHEAD"]
+        else:
+            os.environ["DSEL_LOOKAHEAD"] = prev_la
         t0 = time.time()
         engines[a].gen_synthetic(v, vrank, SIGMA)
         t_gen = max(t_gen, time.time() - t0)
     del v
     res = {a: time_device(engines[a], args, world, local if a == args.algorithm else None)
-           for a in algos}
+           for a in builds}
+    if "plain" in res:
+        if res["plain"]["chosen"] != res["right"]["chosen"]:
+            raise RuntimeError("look-ahead and plain schedules give different sequences")
+        engines.pop("plain").close()
     if len(algos) > 1 and res[algos[0]]["chosen"] != res[algos[1]]["chosen"]:
         raise RuntimeError("right- and left-looking sequences differ")
     for a in algos:
@@ -433,7 +449,9 @@ def our_arm(args, world, rank, local):
     prim = res[algos[0]]
     other = res[algos[1]] if len(algos) > 1 else None
     value, chosen, clocks = prim["value"], prim["chosen"], prim["clocks"]
-    upd_tf, upd_tf_all = prim["upd_tf"], prim["upd_tf_max"]
+    plain = res.get("plain")
+    kern = plain if (plain is not None and args.algorithm == "right") else prim
+    upd_tf, upd_tf_all = kern["upd_tf"], kern["upd_tf_max"]
     tot_flops, tot_flops_all = prim["flops_rank"], prim["flops_all"]
     e2e_tf = tot_flops_all / value / 1e12
     e2e, launches = prim["e2e"], [prim["launches"]]
@@ -461,6 +479,14 @@ def our_arm(args, world, rank, local):
         "config": {**workload_config(args.config, nd, nt, budget, vrank, world),
                    "chosen_first": chosen[:8]},
         "algorithm": ALGO_DESC[args.algorithm],
+        "schedule": ({"primary": "look-ahead rounds (the bulk of round t beside round t+1's gains, "
+                                 "argmax and W solve; 8 SMs reserved for that chain)",
+                      "plain_schedule_value": round(plain["value"], 6),
+                      "roofline_from": "the plain schedule (the same update kernel on all 148 SMs; "
+                                       "under look-ahead it shares the GPU with the chain)",
+                      "lookahead_update_tflops_per_gpu": round(prim["upd_tf"], 3)}
+                     if plain is not None and args.algorithm == "right" else
+                     {"primary": "plain rounds"}),
         "schur_update": {"flops_per_step_per_rank": tot_flops,
                          "flops_per_step_all_ranks": tot_flops_all,
                          "kernel_tflops_per_gpu": round(upd_tf, 3),

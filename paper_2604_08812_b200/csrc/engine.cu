@@ -1876,10 +1876,9 @@ void apply_plan(dsel_engine* e, const dsel_config* cfg, bool ll, bool stream) {
   e->c_pad = e->packed ? (size_t)e->n : 0;
   e->mpad = round_up((int)e->n, ws::ROW_PAD);
   e->hpacked = stream && e->G == 1;
-  // look-ahead rounds are opt-in (DSEL_LOOKAHEAD=1): measured -4 % at 1 GPU and
-  // -7.5 % at 2 GPUs on C2, but a 4-GPU bench run did not finish (open)
+  // look-ahead rounds (DSEL_LOOKAHEAD=0 turns them off)
   const char* la_env = getenv("DSEL_LOOKAHEAD");
-  e->la = e->sym && !ll && e->nt % e->ws_br == 0 && e->nt % ws::BC == 0 && la_env && atoi(la_env) == 1;
+  e->la = e->sym && !ll && e->nt % e->ws_br == 0 && e->nt % ws::BC == 0 && !(la_env && atoi(la_env) == 0);
 }
 
 uint64_t plan_bytes(const dsel_engine* e, const dsel_config* cfg) {
