@@ -216,13 +216,14 @@ def test_packed_and_full_panels_bitwise_identical(dsel, golden_dir):
 @pytest.mark.parametrize("kw", [dict(), dict(algorithm="left"),
                                 dict(algorithm="left", storage="stream")],
                          ids=["right", "left", "stream"])
-@pytest.mark.parametrize("name", ["c3.json", "c3_b20.json", "c4s.json", "c4s_b40.json"])
+@pytest.mark.parametrize("name", ["c3.json", "c4s.json", "c4s_b40.json"])
 def test_baseline_sizes_against_reference_golden(dsel, golden_dir, name, kw):
     """C3 at G = 1 (75 x Nt=420, rank 24,576, select 50: the weak-scaling unit)
     and a scaled C4 (600 candidates x Nt=64, rank 8192, select 100), K from the
     bit-exact generator, sequences identical and gains within 1e-9 of the
-    reference's run_parallel_greedy. The *_b20 / *_b40 goldens are the first 20 /
-    40 rounds of the same selections (the reference needs hours for all)."""
+    reference's run_parallel_greedy. c4s_b40 is the first 40 rounds of the scaled-C4
+    selection (the reference needs hours for all 100; C3's 50 rounds took 2.8 h on
+    8 cores)."""
     g = golden(golden_dir, name)
     nd, nt, rk, b = g["n_sensors"], g["n_steps"], g["rank"], g["budget"]
     v = dsel.synthetic_v(nd, nt, rk, g["seed"])

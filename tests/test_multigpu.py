@@ -29,8 +29,8 @@ def free_port():
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not gpu_available() or ngpu() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("which", ["c1", "replay", "lookahead", "wave", "c2", "c3mini", "c3", "c3_b20",
-                                   "c4s", "c4s_b40", "random", "device", "lti", "attach"])
+@pytest.mark.parametrize("which", ["c1", "replay", "lookahead", "wave", "c2", "c3mini", "c3", "c4s",
+                                   "c4s_b40", "random", "device", "lti", "attach"])
 def test_multi_gpu_matches_reference(which):
     if which.startswith(("c3", "c4s")) and which != "c3mini" and not os.path.exists(
             os.path.join(ROOT, "tests", "golden", f"{which}.json")):

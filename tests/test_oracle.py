@@ -214,3 +214,17 @@ def test_edge_golden_is_reference_output(golden_dir):
         t = O.greedy_select(k, c["n_sensors"], c["n_steps"], c["budget"])
         assert t.chosen == c["chosen"] and t.gains == c["gains"], c["name"]
         assert t.n_infeasible[:len(c["chosen"])] == c["n_infeasible"], c["name"]
+
+
+def test_c3_golden_is_a_complete_reference_run(golden_dir):
+    """tests/golden/c3.json: BASELINE configs[2] at G = 1 (75 x Nt=420, rank
+    24,576, select 50), the reference's own run_parallel_greedy on 8 workers."""
+    path = os.path.join(golden_dir, "c3.json")
+    if not os.path.exists(path):
+        pytest.skip("c3 golden not generated")
+    g = json.load(open(path))
+    assert (g["n_sensors"], g["n_steps"], g["rank"], g["budget"]) == (75, 420, 24576, 50)
+    assert len(g["chosen"]) == 50 == len(set(g["chosen"]))
+    assert all(b > a for a, b in zip(g["objectives"], g["objectives"][1:]))
+    assert g["n_evaluated"] == list(range(75, 25, -1))
+    assert "reference run_parallel_greedy" in g["source"]
