@@ -338,17 +338,22 @@ constexpr long long kNoCol = (-9223372036854775807LL - 1);
 // Big: 128-row tiles, 8 consumer warps, 1 CTA/SM. Pair: 64-row tiles, 4
 // consumer warps, 2 CTAs/SM -- the two CTAs drift apart, so one's tile
 // prologue/epilogue (C tile in, results out) overlaps the other's DMMA loop.
-template <int BRT, int SCT, int STG, int MINBT>
+// TSV: the finished tile goes to a shared-memory buffer and a storer warp
+// writes it back with bulk (TMA) copies, so the consumers start the next
+// tile's DMMA loop instead of waiting on 64 KB of global stores.
+template <int BRT, int SCT, int STG, int MINBT, int TSV = 0>
 struct Cfg {
   static constexpr int BR = BRT, SC = SCT, STAGES = STG, MINB = MINBT;
+  static constexpr bool TS = TSV != 0;
   static constexpr int RG = BRT / 32;  // warp rows
-  static constexpr int CONSUMERS = RG * 2 * 32, THREADS = CONSUMERS + 32;
+  static constexpr int CONSUMERS = RG * 2 * 32, THREADS = CONSUMERS + (TS ? 64 : 32);
   static constexpr int CP = BRT + 8;  // C tile column pitch (doubles): conflict-free LDS.128
   static constexpr size_t OFF_R = 0;
   static constexpr size_t OFF_C = OFF_R + (size_t)STAGES * SC * BR * KC * 8;
   static constexpr size_t OFF_CT = OFF_C + (size_t)STAGES * SC * BC * KC * 8;
-  static constexpr size_t OFF_MAPS = OFF_CT + (size_t)BC * CP * 8;  // 2 x {colbase, rowphys, cshift, colstart}
-  static constexpr size_t MAPS_BYTES = (size_t)BC * 8 + BR * 4 + BC * 4 + BC * 4;
+  static constexpr size_t OFF_OUT = OFF_CT + (size_t)BC * CP * 8;  // TS: the outgoing tile
+  static constexpr size_t OFF_MAPS = OFF_OUT + (TS ? (size_t)BC * CP * 8 : 0);  // 2 x {colbase, rowphys, cshift, colstart[, row runs]}
+  static constexpr size_t MAPS_BYTES = (size_t)BC * 8 + BR * 4 + BC * 4 + BC * 4 + (TS ? (BR + 2) * 4 : 0);
   static constexpr size_t OFF_RUNS = OFF_MAPS + 2 * MAPS_BYTES;     // producer scratch
   static constexpr size_t OFF_BAR = OFF_RUNS + (size_t)(2 * BC + BR + 8) * 8;
   static constexpr size_t OFF_SYM = OFF_BAR + 16 * 8;
@@ -361,10 +366,14 @@ using Big4 = Cfg<128, 3, 2, 1>;
 // stalled on a fragment load or a barrier leaves two to keep the DMMA pipe
 // fed), 1 chunk x 3 stages; registers capped at 152 per thread
 using Big6 = Cfg<192, 1, 3, 1>;
+// BigT: Big's tiles with the bulk-store epilogue (1 chunk x 3 stages to make
+// room for the outgoing tile)
+using BigT = Cfg<128, 1, 3, 1, 1>;
 constexpr int ROW_PAD = 384;  // lcm of the tile heights: tiled W buffers are padded to it
 static_assert(Big::SMEM <= 232448 - 2048, "ws kernel shared memory (1 CTA/SM)");
 static_assert(Big4::SMEM <= 232448 - 2048, "ws kernel shared memory (Big4)");
 static_assert(Big6::SMEM <= 232448 - 2048, "ws kernel shared memory (Big6)");
+static_assert(BigT::SMEM <= 232448 - 2048, "ws kernel shared memory (BigT)");
 static_assert(2 * (Pair::SMEM + 2048) <= 233472, "ws kernel shared memory (2 CTAs/SM)");
 constexpr int THREADS = Big::THREADS;
 constexpr size_t SMEM = Big::SMEM;
@@ -514,6 +523,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+
 // One 16-deep k-chunk of the consumer mainloop. The tiled layout rotates a
 // row's 4-double groups by (buffer row % 4). r-side smem rows are buffer rows
 // r0 + i (r0 % 4 == 0), so their rotation is (k4 + g). A c-side smem row i
@@ -560,6 +575,10 @@ __global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(
   uint64_t* tfull = bars + 2 * STAGES;    // [2]       maps + C tile landed (per map buffer)
   uint64_t* mempty = bars + 2 * STAGES + 2;  // [2]    consumers finished the tile's epilogue
   uint64_t* cempty = bars + 2 * STAGES + 4;  // [1]    consumers copied the C tile to registers
+  uint64_t* ofull = bars + 2 * STAGES + 5;   // [1]    TS: consumers wrote the outgoing tile
+  uint64_t* oempty = bars + 2 * STAGES + 6;  // [1]    TS: the bulk stores finished reading it
+  double* sOut = reinterpret_cast<double*>(smem_raw + Cf::OFF_OUT);
+  __shared__ int s_nrr[2];    // TS: row runs of the tile per map buffer
   __shared__ int s_tflag[2];  // per map buffer: 1 = a tile is ready, 0 = no more tiles
   __shared__ int s_tile_r0[2], s_tile_c0[2];  // tile origin per map buffer (left-looking output)
   __shared__ int s_cshift[2];                  // per map buffer: some c-side row has a rotation delta
@@ -575,6 +594,9 @@ __global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(
   };
   auto colstart_of = [&](int b) {  // first stored physical row of each column (packed store)
     return reinterpret_cast<int*>(smem_raw + OFF_MAPS + b * MAPS_BYTES + BC * 8 + BR * 4 + BC * 4);
+  };
+  auto rrun_of = [&](int b) {  // TS: the tile's row-run starts (then the end)
+    return reinterpret_cast<int*>(smem_raw + OFF_MAPS + b * MAPS_BYTES + BC * 8 + BR * 4 + 2 * BC * 4);
   };
   int* cw = reinterpret_cast<int*>(smem_raw + OFF_RUNS);        // [BC] W row of each c column
   int* runs = cw + BC;                                          // row runs: start,len pairs
@@ -600,9 +622,13 @@ __global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&mempty[b], CONSUMERS / 32);
+      mbar_init(&mempty[b], CONSUMERS / 32 + (Cf::TS ? 1 : 0));  // TS: + the storer
     }
     mbar_init(cempty, CONSUMERS / 32);
+    if (Cf::TS) {
+      mbar_init(ofull, CONSUMERS / 32);
+      mbar_init(oempty, 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -717,6 +743,12 @@ __global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(
       nrr = __shfl_sync(0xffffffffu, nrr, 0);
       ncr = __shfl_sync(0xffffffffu, ncr, 0);
       __syncwarp();
+      if (Cf::TS) {  // the storer needs this tile's row runs after the producer moved on
+        int* rr_b = rrun_of(b);
+        for (int q = lane; q <= nrr; q += 32) rr_b[q] = rrun[q];
+        if (lane == 0) s_nrr[b] = nrr;
+        __syncwarp();
+      }
       // C tile -> sCt once consumers copied the previous tile to registers
       if (it >= 1) mbar_wait(cempty, (it - 1) & 1);
       if (!cinit) {  // accumulate from zero (streaming left-looking: K added afterwards)
@@ -765,6 +797,49 @@ __global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(
         mbar_arrive(&tfull[b]);
       }
     }
+    return;
+  }
+
+  if (Cf::TS && warp == CONSUMERS / 32 + 1) {
+    // ================================ storer ================================
+    // walks the producer's tile sequence; per finished tile, bulk copies of
+    // each column's row runs from sOut to C (rows above a packed panel's first
+    // stored row clipped), then releases sOut and the tile's maps
+    int it = 0;
+    for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
+      int r0, c0, tile, uz, kb_lo, kb_hi;
+      ws_unit(a, unit, tile, uz, kb_lo, kb_hi);
+      if (!ws_tile(a, fr, gp, tile, r0, c0)) continue;
+      const int b = it & 1;
+      mbar_wait(ofull, it & 1);
+      const long long* colbase = colbase_of(b);
+      const int* rowphys = rowphys_of(b);
+      const int* cst = colstart_of(b);
+      const int* rr_b = rrun_of(b);
+      const int nrr = s_nrr[b];
+      const int ncv = min(BC, a.n_cols - c0);
+      for (int p = lane; p < ncv * nrr; p += 32) {
+        const int c = p / nrr, q = p - c * nrr;
+        int i0 = rr_b[q], len = rr_b[q + 1] - i0;
+        const int first = rowphys[i0], c_lo = cst[c];
+        if (first < c_lo) {
+          const int skip = c_lo - first;
+          i0 += skip;
+          len -= skip;
+        }
+        if (len <= 0) continue;
+        bulk_s2g(a.C + colbase[c] + rowphys[i0], sOut + c * CP + i0, (unsigned)len * 8u);
+      }
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(oempty);
+        mbar_arrive(&mempty[b]);
+      }
+      ++it;
+    }
+    asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // writes landed before exit
     return;
   }
 
@@ -839,6 +914,18 @@ __global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(
           if (rowphys[rl + 1] >= 0) out[(size_t)(r0o + rl + 1) * a.ldo + crow] = acc[i][j][1];
         }
       }
+    } else if (Cf::TS) {
+      // the finished tile into sOut (the storer writes it back with bulk copies)
+      if (it >= 1) mbar_wait(oempty, (it - 1) & 1);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          *reinterpret_cast<double2*>(sOut + (wc + i * 8 + g) * CP + wr + j * 8 + 2 * t) =
+              make_double2(acc[i][j][0], acc[i][j][1]);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ofull);
     } else {
       // packed store: rows above the column's diagonal block are not stored
       // (their slots hold the previous column's data) -- never written
