@@ -254,7 +254,7 @@ struct dsel_engine {
   const double** d_peer_wsend = nullptr;
   unsigned long long** d_peer_flag = nullptr;
   int ws_br = 128;  // tile height of the right-looking update configuration (rl_cfg)
-  int ws_cfg = -1;   // DSEL_WS_CFG: -1 auto, 0 ws::Big, 1 ws::Pair, 2 ws::Big4, 3 ws::Big6, 4 ws::BigT
+  int ws_cfg = -1;   // DSEL_WS_CFG: -1 auto, 0 ws::Big, 1 ws::Pair, 2 ws::Big4, 3 ws::Big6, 4 ws::BigT, 5 ws::BigR
   int rl_cfg = 0;    // configuration of the right-looking update and K formation
   int ws_group = kWsGroupDefault;  // column tiles per rasterization group
   double gen_flops = 0.0;  // last dsel_gen_synthetic_device (K formation on the update kernel)
@@ -624,6 +624,7 @@ void set_smem_limits(int dev) {
   allow_smem(schur_update_ws_kernel<ws::Big4>, optin);
   allow_smem(schur_update_ws_kernel<ws::Big6>, optin);
   allow_smem(schur_update_ws_kernel<ws::BigT>, optin);
+  allow_smem(schur_update_ws_kernel<ws::BigR>, optin);
   CU(cudaFuncSetAttribute(schur_update_ws_kernel<ws::Pair>, cudaFuncAttributePreferredSharedMemoryCarveout,
                           (int)cudaSharedmemCarveoutMaxShared));
   allow_smem(ll_gemm_kernel, optin);
@@ -807,6 +808,9 @@ void launch_ws(dsel_engine* e, UpdateWSArgs& ua, int cfg, int sms = 0, cudaStrea
   } else if (cfg == 4) {
     const int grid = (int)std::min<long long>(sms, units);
     schur_update_ws_kernel<ws::BigT><<<grid, ws::BigT::THREADS, ws::BigT::SMEM, st>>>(ua);
+  } else if (cfg == 5) {
+    const int grid = (int)std::min<long long>(sms, units);
+    schur_update_ws_kernel<ws::BigR><<<grid, ws::BigR::THREADS, ws::BigR::SMEM, st>>>(ua);
   } else {
     const int grid = (int)std::min<long long>(sms, units);
     schur_update_ws_kernel<ws::Big><<<grid, ws::Big::THREADS, ws::Big::SMEM, st>>>(ua);
@@ -2018,7 +2022,7 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
       CU(cudaEventCreateWithFlags(&e->ev_copy[b], cudaEventDisableTiming));
       CU(cudaEventCreateWithFlags(&e->ev_scat[b], cudaEventDisableTiming));
     }
-    if (const char* wc = getenv("DSEL_WS_CFG")) e->ws_cfg = std::max(-1, std::min(4, atoi(wc)));
+    if (const char* wc = getenv("DSEL_WS_CFG")) e->ws_cfg = std::max(-1, std::min(5, atoi(wc)));
     e->rl_cfg = e->ws_cfg >= 0 ? e->ws_cfg : 0;
     e->ws_br = cfg_br(e->rl_cfg);
     if (const char* wg = getenv("DSEL_WS_GROUP")) e->ws_group = std::max(1, atoi(wg));

@@ -341,18 +341,21 @@ constexpr long long kNoCol = (-9223372036854775807LL - 1);
 // TSV: the finished tile goes to a shared-memory buffer and a storer warp
 // writes it back with bulk (TMA) copies, so the consumers start the next
 // tile's DMMA loop instead of waiting on 64 KB of global stores.
+// TSV = 2 (reduce): the DMMA loop starts from zero, no C tile is loaded, and
+// the storer adds the finished tile into C with bulk reduce-adds
+// (cp.reduce.async.bulk .add.f64); the outgoing tile reuses the C tile buffer.
 template <int BRT, int SCT, int STG, int MINBT, int TSV = 0>
 struct Cfg {
   static constexpr int BR = BRT, SC = SCT, STAGES = STG, MINB = MINBT;
-  static constexpr bool TS = TSV != 0;
+  static constexpr bool TS = TSV != 0, RED = TSV == 2;
   static constexpr int RG = BRT / 32;  // warp rows
   static constexpr int CONSUMERS = RG * 2 * 32, THREADS = CONSUMERS + (TS ? 64 : 32);
   static constexpr int CP = BRT + 8;  // C tile column pitch (doubles): conflict-free LDS.128
   static constexpr size_t OFF_R = 0;
   static constexpr size_t OFF_C = OFF_R + (size_t)STAGES * SC * BR * KC * 8;
   static constexpr size_t OFF_CT = OFF_C + (size_t)STAGES * SC * BC * KC * 8;
-  static constexpr size_t OFF_OUT = OFF_CT + (size_t)BC * CP * 8;  // TS: the outgoing tile
-  static constexpr size_t OFF_MAPS = OFF_OUT + (TS ? (size_t)BC * CP * 8 : 0);  // 2 x {colbase, rowphys, cshift, colstart[, row runs]}
+  static constexpr size_t OFF_OUT = RED ? OFF_CT : OFF_CT + (size_t)BC * CP * 8;  // TS: the outgoing tile
+  static constexpr size_t OFF_MAPS = OFF_CT + (size_t)BC * CP * 8 + (TS && !RED ? (size_t)BC * CP * 8 : 0);  // 2 x {colbase, rowphys, cshift, colstart[, row runs]}
   static constexpr size_t MAPS_BYTES = (size_t)BC * 8 + BR * 4 + BC * 4 + BC * 4 + (TS ? (BR + 2) * 4 : 0);
   static constexpr size_t OFF_RUNS = OFF_MAPS + 2 * MAPS_BYTES;     // producer scratch
   static constexpr size_t OFF_BAR = OFF_RUNS + (size_t)(2 * BC + BR + 8) * 8;
@@ -369,11 +372,14 @@ using Big6 = Cfg<192, 1, 3, 1>;
 // BigT: Big's tiles with the bulk-store epilogue (1 chunk x 3 stages to make
 // room for the outgoing tile)
 using BigT = Cfg<128, 1, 3, 1, 1>;
+// BigR: Big's tiles and stages, DMMA from zero, bulk reduce-add write-back
+using BigR = Cfg<128, 2, 3, 1, 2>;
 constexpr int ROW_PAD = 384;  // lcm of the tile heights: tiled W buffers are padded to it
 static_assert(Big::SMEM <= 232448 - 2048, "ws kernel shared memory (1 CTA/SM)");
 static_assert(Big4::SMEM <= 232448 - 2048, "ws kernel shared memory (Big4)");
 static_assert(Big6::SMEM <= 232448 - 2048, "ws kernel shared memory (Big6)");
 static_assert(BigT::SMEM <= 232448 - 2048, "ws kernel shared memory (BigT)");
+static_assert(BigR::SMEM <= 232448 - 2048, "ws kernel shared memory (BigR)");
 static_assert(2 * (Pair::SMEM + 2048) <= 233472, "ws kernel shared memory (2 CTAs/SM)");
 constexpr int THREADS = Big::THREADS;
 constexpr size_t SMEM = Big::SMEM;
@@ -529,6 +535,12 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned by
                : "memory");
 }
 
+__device__ __forceinline__ void bulk_s2g_add(double* dst, const double* src, unsigned bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;\n" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+
 // One 16-deep k-chunk of the consumer mainloop. The tiled layout rotates a
 // row's 4-double groups by (buffer row % 4). r-side smem rows are buffer rows
 // r0 + i (r0 % 4 == 0), so their rotation is (k4 + g). A c-side smem row i
@@ -645,7 +657,7 @@ __global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(
       int r0, c0, tile, uz, kb_lo, kb_hi;
       ws_unit(a, unit, tile, uz, kb_lo, kb_hi);
       if (!ws_tile(a, fr, gp, tile, r0, c0)) continue;
-      const bool cinit = a.C && uz <= 0;  // split units > 0 start from zero
+      const bool cinit = a.C && uz <= 0 && !Cf::RED;  // split units > 0 (and RED) start from zero
       const int nrv = min(BR, a.n_rows - r0);  // valid rows of the tile
       const int ncv = min(BC, a.n_cols - c0);  // valid columns
       const int b = it & 1;
@@ -828,7 +840,10 @@ __global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(
           len -= skip;
         }
         if (len <= 0) continue;
-        bulk_s2g(a.C + colbase[c] + rowphys[i0], sOut + c * CP + i0, (unsigned)len * 8u);
+        if (Cf::RED)
+          bulk_s2g_add(a.C + colbase[c] + rowphys[i0], sOut + c * CP + i0, (unsigned)len * 8u);
+        else
+          bulk_s2g(a.C + colbase[c] + rowphys[i0], sOut + c * CP + i0, (unsigned)len * 8u);
       }
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
@@ -856,7 +871,7 @@ __global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(
     if (!s_tflag[b]) break;  // the producer has no more tiles for this CTA
     double acc[4][4][2];
     const int uz = s_tile_z[b], unk = s_tile_nk[b];
-    const bool cz = a.C == nullptr || uz > 0;
+    const bool cz = a.C == nullptr || uz > 0 || Cf::RED;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
