@@ -255,7 +255,7 @@ struct dsel_engine {
   unsigned long long** d_peer_flag = nullptr;
   int ws_br = 128;  // tile height of the right-looking update configuration (rl_cfg)
   int ws_cfg = -1;   // DSEL_WS_CFG: -1 auto, 0 ws::Big, 1 ws::Pair, 2 ws::Big4, 3 ws::Big6, 4 ws::BigT, 5 ws::BigR
-  int rl_cfg = 0;    // configuration of the right-looking update and K formation
+  int rl_cfg = 5;    // configuration of the right-looking update (BigR by default)
   int ws_group = kWsGroupDefault;  // column tiles per rasterization group
   double gen_flops = 0.0;  // last dsel_gen_synthetic_device (K formation on the update kernel)
   bool keep = false, export_factor = false;
@@ -2023,7 +2023,7 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
       CU(cudaEventCreateWithFlags(&e->ev_scat[b], cudaEventDisableTiming));
     }
     if (const char* wc = getenv("DSEL_WS_CFG")) e->ws_cfg = std::max(-1, std::min(5, atoi(wc)));
-    e->rl_cfg = e->ws_cfg >= 0 ? e->ws_cfg : 0;
+    e->rl_cfg = e->ws_cfg >= 0 ? e->ws_cfg : 5;  // BigR: DMMA from zero + bulk reduce-add write-back
     e->ws_br = cfg_br(e->rl_cfg);
     if (const char* wg = getenv("DSEL_WS_GROUP")) e->ws_group = std::max(1, atoi(wg));
     // the storage plan decides every allocation below. AUTO: K resident in
