@@ -625,6 +625,7 @@ void set_smem_limits(int dev) {
   allow_smem(schur_update_ws_kernel<ws::Big6>, optin);
   allow_smem(schur_update_ws_kernel<ws::BigT>, optin);
   allow_smem(schur_update_ws_kernel<ws::BigR>, optin);
+  allow_smem(schur_update_ws_kernel<ws::BigR4>, optin);
   CU(cudaFuncSetAttribute(schur_update_ws_kernel<ws::Pair>, cudaFuncAttributePreferredSharedMemoryCarveout,
                           (int)cudaSharedmemCarveoutMaxShared));
   allow_smem(ll_gemm_kernel, optin);
@@ -768,7 +769,7 @@ void setup_p2p(dsel_engine* e) {
 // short ones (Nt = 128 right-looking); 64-row tiles (Pair) when the r-side row
 // count pads badly to 128 (left-looking r-side = Nt rows: 420 -> 82 % of 4 x
 // 128 tiles, 94 % of 7 x 64). -1 = auto.
-int cfg_br(int cfg) { return cfg == 1 ? 64 : cfg == 3 ? 192 : 128; }
+int cfg_br(int cfg) { return cfg == 1 ? 64 : cfg == 3 ? 192 : 128; }  // 0,2,4,5,6: 128
 int ws_pick(const dsel_engine* e, int r_rows, int n_k, bool fixed_rows);
 // K formation on the update kernel: its tile schedule uses ws_br, so the tile
 // height must match the right-looking configuration's
@@ -811,6 +812,9 @@ void launch_ws(dsel_engine* e, UpdateWSArgs& ua, int cfg, int sms = 0, cudaStrea
   } else if (cfg == 5) {
     const int grid = (int)std::min<long long>(sms, units);
     schur_update_ws_kernel<ws::BigR><<<grid, ws::BigR::THREADS, ws::BigR::SMEM, st>>>(ua);
+  } else if (cfg == 6) {
+    const int grid = (int)std::min<long long>(sms, units);
+    schur_update_ws_kernel<ws::BigR4><<<grid, ws::BigR4::THREADS, ws::BigR4::SMEM, st>>>(ua);
   } else {
     const int grid = (int)std::min<long long>(sms, units);
     schur_update_ws_kernel<ws::Big><<<grid, ws::Big::THREADS, ws::Big::SMEM, st>>>(ua);
@@ -2022,8 +2026,10 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
       CU(cudaEventCreateWithFlags(&e->ev_copy[b], cudaEventDisableTiming));
       CU(cudaEventCreateWithFlags(&e->ev_scat[b], cudaEventDisableTiming));
     }
-    if (const char* wc = getenv("DSEL_WS_CFG")) e->ws_cfg = std::max(-1, std::min(5, atoi(wc)));
-    e->rl_cfg = e->ws_cfg >= 0 ? e->ws_cfg : 5;  // BigR: DMMA from zero + bulk reduce-add write-back
+    if (const char* wc = getenv("DSEL_WS_CFG")) e->ws_cfg = std::max(-1, std::min(6, atoi(wc)));
+    // BigR: DMMA from zero + bulk reduce-add write-back; its 3 x 2 stage
+    // variant from 16 k-chunks (Nt = 420), like Big4 for the plain kernel
+    e->rl_cfg = e->ws_cfg >= 0 ? e->ws_cfg : (e->ldw / ws::KC >= 16 ? 6 : 5);
     e->ws_br = cfg_br(e->rl_cfg);
     if (const char* wg = getenv("DSEL_WS_GROUP")) e->ws_group = std::max(1, atoi(wg));
     // the storage plan decides every allocation below. AUTO: K resident in

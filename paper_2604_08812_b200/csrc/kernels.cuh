@@ -374,12 +374,14 @@ using Big6 = Cfg<192, 1, 3, 1>;
 using BigT = Cfg<128, 1, 3, 1, 1>;
 // BigR: Big's tiles and stages, DMMA from zero, bulk reduce-add write-back
 using BigR = Cfg<128, 2, 3, 1, 2>;
+using BigR4 = Cfg<128, 3, 2, 1, 2>;  // BigR with Big4's stages (long k)
 constexpr int ROW_PAD = 384;  // lcm of the tile heights: tiled W buffers are padded to it
 static_assert(Big::SMEM <= 232448 - 2048, "ws kernel shared memory (1 CTA/SM)");
 static_assert(Big4::SMEM <= 232448 - 2048, "ws kernel shared memory (Big4)");
 static_assert(Big6::SMEM <= 232448 - 2048, "ws kernel shared memory (Big6)");
 static_assert(BigT::SMEM <= 232448 - 2048, "ws kernel shared memory (BigT)");
 static_assert(BigR::SMEM <= 232448 - 2048, "ws kernel shared memory (BigR)");
+static_assert(BigR4::SMEM <= 232448 - 2048, "ws kernel shared memory (BigR4)");
 static_assert(2 * (Pair::SMEM + 2048) <= 233472, "ws kernel shared memory (2 CTAs/SM)");
 constexpr int THREADS = Big::THREADS;
 constexpr size_t SMEM = Big::SMEM;
