@@ -27,6 +27,18 @@ def free_port():
     return p
 
 
+def torchrun(n, args, env=None, timeout=900):
+    """torchrun on 127.0.0.1; a fresh port and another try when the one picked
+    was taken between free_port() and the rendezvous (EADDRINUSE)."""
+    for _ in range(3):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+               "--master-addr", "127.0.0.1", "--master-port", str(free_port()), *args]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env)
+        if r.returncode == 0 or "EADDRINUSE" not in r.stderr + r.stdout:
+            return r
+    return r
+
+
 @pytest.mark.gpu
 @pytest.mark.skipif(not gpu_available() or ngpu() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("which", ["c1", "replay", "lookahead", "wave", "c2", "c3mini", "c3", "c4s",
@@ -35,11 +47,7 @@ def test_multi_gpu_matches_reference(which):
     if which.startswith(("c3", "c4s")) and which != "c3mini" and not os.path.exists(
             os.path.join(ROOT, "tests", "golden", f"{which}.json")):
         pytest.skip(f"{which} golden not generated")
-    n = min(ngpu(), 8)
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
-           os.path.join(ROOT, "tests", "mp_engine_check.py"), which]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    r = torchrun(min(ngpu(), 8), [os.path.join(ROOT, "tests", "mp_engine_check.py"), which])
     print(r.stdout[-3000:])
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
@@ -50,12 +58,8 @@ def test_multi_gpu_matches_reference(which):
 def test_multi_gpu_nccl_exchange_fallback(which):
     """DSEL_P2P=0: the W / W_k exchange over NCCL broadcasts instead of NVLink
     peer memory gives the same results."""
-    n = min(ngpu(), 8)
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
-           os.path.join(ROOT, "tests", "mp_engine_check.py"), which]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900,
-                       env=dict(os.environ, DSEL_P2P="0"))
+    r = torchrun(min(ngpu(), 8), [os.path.join(ROOT, "tests", "mp_engine_check.py"), which],
+                 env=dict(os.environ, DSEL_P2P="0"))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
