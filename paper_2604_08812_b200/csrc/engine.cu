@@ -545,6 +545,11 @@ int chol_mp(int nt) {
   return mp;
 }
 
+// staged gain kernel (one 16-warp CTA per candidate, chunked L stream): on when the
+// batch fits one wave; DSEL_CHOL_STAGE=0 selects chol_logdet_kernel instead
+bool g_chol_stage = true;
+size_t g_chol_stage_max = 0;  // dynamic smem the staged kernel may use (opt-in - static)
+
 void launch_chol(const CholArgs& a, int n_batch, cudaStream_t s, int n_sms) {
   const int nb = chol_nb(a.nt);
   const size_t smem = ((size_t)nb * a.mp + a.nt) * sizeof(double);
@@ -557,6 +562,8 @@ void launch_chol(const CholArgs& a, int n_batch, cudaStream_t s, int n_sms) {
       chol_logdet_tri_kernel<2><<<n_batch, 256, ts, s>>>(a);
     else
       chol_logdet_tri_kernel<1><<<n_batch, 256, ts, s>>>(a);
+  } else if (nb == 32 && !two && g_chol_stage && cst::smem_bytes(a.nt, a.mp) <= g_chol_stage_max) {
+    chol_logdet_stage_kernel<12><<<n_batch, 384, cst::smem_bytes(a.nt, a.mp), s>>>(a);
   } else if (nb == 32) {
     if (two)
       chol_logdet_kernel<32, 2><<<n_batch, 256, smem, s>>>(a);
@@ -613,6 +620,14 @@ void set_smem_limits(int dev) {
   allow_smem(chol_logdet_kernel<32, 1>, optin);
   allow_smem(chol_logdet_kernel<32, 2>, optin);
   allow_smem(chol_logdet_kernel<8, 1>, optin);
+  {
+    cudaFuncAttributes fa{};
+    CU(cudaFuncGetAttributes(&fa, chol_logdet_stage_kernel<12>));
+    g_chol_stage_max = (size_t)optin - fa.sharedSizeBytes;
+    allow_smem(chol_logdet_stage_kernel<12>, optin);
+    const char* cs = getenv("DSEL_CHOL_STAGE");
+    g_chol_stage = !(cs && cs[0] == '0');
+  }
   allow_smem(chol_logdet_tri_kernel<1>, optin);
   allow_smem(chol_logdet_tri_kernel<2>, optin);
   allow_smem(schur_update_kernel<2>, optin);
@@ -3204,6 +3219,14 @@ int dsel_get_trace(dsel_engine* e, dsel_step_info* rows, int max_rows) {
         r.ms_update += bk;
       }
       r.ms_round = tot;
+      if (getenv("DSEL_TIMELINE")) {  // diagnostics: event offsets from round 1's start, ms
+        float o[7] = {0, 0, 0, 0, 0, -1, -1};
+        const int ids[7] = {0, 1, 2, 3, 4, 8, 9};
+        const bool bulk = (size_t)i < e->bulk_round.size() && e->bulk_round[i];
+        for (int j = 0; j < (bulk ? 7 : 5); ++j) CU(cudaEventElapsedTime(&o[j], e->ev[0], ev[ids[j]]));
+        fprintf(stderr, "[tl] %d %d %.4f %.4f %.4f %.4f %.4f %.4f %.4f\n", e->rank, i, o[0], o[1], o[2], o[3],
+                o[4], o[5], o[6]);
+      }
       r.ms_io = 0.0;
       if (std::find(e->streamed_round.begin(), e->streamed_round.end(), i) != e->streamed_round.end()) {
         float io = 0;

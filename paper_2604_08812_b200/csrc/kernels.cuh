@@ -1524,21 +1524,24 @@ __device__ __forceinline__ void block_argmax(const double* gain, const int* stat
                                              ArgRec* out) {
   __shared__ double sg1[256], sg2[256];
   __shared__ int ss1[256], ss2[256], sinf[256];
+  // blocks wider than 256 threads: the extra threads only take part in the barriers
   const int tid = threadIdx.x;
   double g1 = -INFINITY, g2 = -INFINITY;
   int s1 = -1, s2 = -1, ninf = 0;
-  for (int i = tid; i < n; i += 256) {
-    if (__ldcg(status + i) >= 0) {
-      ++ninf;
-      continue;
+  if (tid < 256) {
+    for (int i = tid; i < n; i += 256) {
+      if (__ldcg(status + i) >= 0) {
+        ++ninf;
+        continue;
+      }
+      top2_insert(__ldcg(gain + i), sensor[i], g1, s1, g2, s2);
     }
-    top2_insert(__ldcg(gain + i), sensor[i], g1, s1, g2, s2);
+    sg1[tid] = g1;
+    sg2[tid] = g2;
+    ss1[tid] = s1;
+    ss2[tid] = s2;
+    sinf[tid] = ninf;
   }
-  sg1[tid] = g1;
-  sg2[tid] = g2;
-  ss1[tid] = s1;
-  ss2[tid] = s2;
-  sinf[tid] = ninf;
   __syncthreads();
   for (int w = 128; w > 0; w >>= 1) {
     if (tid < w) {
@@ -1855,6 +1858,236 @@ __global__ void __launch_bounds__(256, MINB) chol_logdet_kernel(CholArgs a) {
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
       g_tend[b] = t1;
 #endif
+    }
+  }
+  gain_epilogue(a);
+}
+
+// ------------------------------------------------------------------------ //
+// Gain kernel, 128 < Nt <= ~430 with fewer candidates than SMs (C3: 75       //
+// candidates of Nt = 420 on 148 SMs): one CTA of NW warps per candidate owns //
+// a whole SM. The left-looking panel update streams the earlier factor       //
+// columns L[J0:, kk:kk+16] from the block's L2-resident scratch into two     //
+// shared-memory chunk buffers with cp.async (the next chunk in flight while  //
+// DMMA runs on this one; the first two chunks of the next panel are fetched  //
+// during this panel's diagonal factorization and row solve), instead of one  //
+// L2 round trip per 32 columns per row tile from registers. Each warp owns   //
+// fixed row tiles and keeps their accumulators across chunks. The DMMA order //
+// on every accumulator, the diagonal block, the row solve and the log-det    //
+// reduction are those of chol_logdet_kernel<32, *>: the gains are bitwise    //
+// identical to it.                                                           //
+// ------------------------------------------------------------------------ //
+namespace cst {
+constexpr int NB = 32;   // panel width
+constexpr int CW = 16;   // chunk width (columns of L per stage)
+__host__ __device__ constexpr size_t smem_bytes(int nt, int mp) {
+  return ((size_t)(NB + 2 * CW) * mp + nt) * sizeof(double);
+}
+}  // namespace cst
+
+__device__ __forceinline__ void cp_async_wait_dyn(int n) {
+  if (n <= 0) cp_async_wait<0>();
+  else if (n == 1) cp_async_wait<1>();
+  else if (n == 2) cp_async_wait<2>();
+  else cp_async_wait<3>();
+}
+
+// one CW-column chunk into the accumulators of a warp's NU row tiles
+// (tiles warp, warp + NW, ...); ch points at chunk element (t, g)
+template <int NU, int MAXT, int NW>
+__device__ __forceinline__ void stage_chunk_mma(double (&acc)[MAXT][4][2], const double* ch, int mp, int warp) {
+#pragma unroll
+  for (int k4 = 0; k4 < cst::CW / 4; ++k4) {
+    const double* col = ch + k4 * 4 * mp;
+    double bv[4];
+#pragma unroll
+    for (int n8 = 0; n8 < 4; ++n8) bv[n8] = col[n8 * 8];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      const double av = col[(warp + u * NW) * 8];
+#pragma unroll
+      for (int n8 = 0; n8 < 4; ++n8) dmma884(acc[u][n8], av, bv[n8]);
+    }
+  }
+}
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1) chol_logdet_stage_kernel(CholArgs a) {
+  constexpr int NB = cst::NB, CW = cst::CW, NT = NW * 32;
+  constexpr int MAXT = (448 / 8 + NW - 1) / NW;  // row tiles per warp (nt <= 448)
+  static_assert(MAXT <= 5, "stage_chunk_mma dispatch covers 1..5 tiles");
+  static_assert(448 <= 2 * NT, "one 16-byte chunk copy per column per thread");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int b = blockIdx.x;
+  if (b >= a.n) return;
+  const int nt = a.nt, mp = a.mp;
+  double* S = reinterpret_cast<double*>(smem_raw);  // [NB][mp] current panel
+  double* CH = S + NB * mp;                          // [2][CW][mp] chunks of earlier L columns
+  double* diagv = CH + 2 * CW * mp;                  // [nt]
+  __shared__ double rdiag[NB];
+  __shared__ __align__(16) double s_colbuf[64];
+  __shared__ int s_fail;
+  __shared__ double s_red[8];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const double* src = a.src + a.src_off[b];
+  const long long lds = a.src_ld[b];
+  double* L = a.L + (size_t)b * a.l_stride;  // column-major nt x nt
+  const bool vec = ((nt & 1) == 0) && ((a.l_stride & 1) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(a.L) & 15) == 0);
+  if (tid == 0) s_fail = -1;
+  // cp.async group bookkeeping (uniform across the block): n_commit groups so far,
+  // and the group index holding each chunk buffer / the panel
+  // (two named slots, not arrays: no local memory)
+  int n_commit = 0, g_buf0 = -1, g_buf1 = -1, g_ch0 = -1, g_ch1 = -1;
+  auto issue_chunk = [&](int J0, int c) {  // L[J0:, c*CW : c*CW+CW] -> CH[c & 1]
+    double* dst = CH + (c & 1) * CW * mp;
+    const int m = nt - J0;
+    // no integer division in the issue loops (m <= 2 * NT: one 16-byte copy
+    // per column per thread, or at most two 8-byte ones)
+    const double* srcc = L + (size_t)(c * CW) * nt + J0;
+    if (vec) {  // m is even when nt is
+      const int i = 2 * tid;
+      if (i < m) {
+#pragma unroll
+        for (int j = 0; j < CW; ++j) cp_async16(dst + j * mp + i, srcc + (size_t)j * nt + i, true);
+      }
+    } else {
+#pragma unroll 4
+      for (int j = 0; j < CW; ++j)
+        for (int i = tid; i < m; i += NT) cp_async8(dst + j * mp + i, srcc + (size_t)j * nt + i, true);
+    }
+    cp_async_commit();
+    if (c & 1) {
+      g_buf1 = n_commit++;
+      g_ch1 = c;
+    } else {
+      g_buf0 = n_commit++;
+      g_ch0 = c;
+    }
+  };
+  auto chunk_in = [&](int c) { return ((c & 1) ? g_ch1 : g_ch0) == c; };
+  for (int J0 = 0; J0 < nt; J0 += NB) {
+    const int nb = min(NB, nt - J0);
+    const int m = nt - J0;
+    const int nch = J0 / CW;
+    __syncthreads();  // previous panel's readers of S are done, its L columns stored
+    for (int j = 0; j < nb; ++j)
+      for (int i = tid; i < m; i += NT) cp_async8(S + j * mp + i, src + (size_t)(J0 + j) * lds + J0 + i, true);
+    cp_async_commit();
+    const int g_s = n_commit++;
+    double acc[MAXT][4][2];
+#pragma unroll
+    for (int u = 0; u < MAXT; ++u)
+#pragma unroll
+      for (int n8 = 0; n8 < 4; ++n8) acc[u][n8][0] = acc[u][n8][1] = 0.0;
+    const int mt_n = (m + 7) >> 3;
+    const int n_u = warp < mt_n ? (mt_n - warp + NW - 1) / NW : 0;  // row tiles of this warp
+    for (int c = 0; c < nch; ++c) {
+      if (!chunk_in(c)) issue_chunk(J0, c);  // not prefetched
+      if (c + 1 < nch && !chunk_in(c + 1)) issue_chunk(J0, c + 1);
+      cp_async_wait_dyn(n_commit - 1 - ((c & 1) ? g_buf1 : g_buf0));
+      __syncthreads();
+      const double* ch = CH + (c & 1) * CW * mp + t * mp + g;
+      // this warp's tile count as a compile-time loop bound: a predicated-off
+      // DMMA still occupies the pipe, so no tile slot may be issued empty
+      switch (n_u) {
+        case 5: stage_chunk_mma<5, MAXT, NW>(acc, ch, mp, warp); break;
+        case 4: stage_chunk_mma<4, MAXT, NW>(acc, ch, mp, warp); break;
+        case 3: stage_chunk_mma<3, MAXT, NW>(acc, ch, mp, warp); break;
+        case 2: stage_chunk_mma<2, MAXT, NW>(acc, ch, mp, warp); break;
+        case 1: stage_chunk_mma<1, MAXT, NW>(acc, ch, mp, warp); break;
+        default: break;
+      }
+      __syncthreads();  // buffer c & 1 may be refilled
+      if (c & 1) g_ch1 = -1;
+      else g_ch0 = -1;
+    }
+    cp_async_wait_dyn(n_commit - 1 - g_s);
+    __syncthreads();
+    if (nch > 0) {
+#pragma unroll
+      for (int u = 0; u < MAXT; ++u) {
+        const int i = (warp + u * NW) * 8 + g;
+        if (i < m) {
+#pragma unroll
+          for (int n8 = 0; n8 < 4; ++n8) {
+            const int j0 = n8 * 8 + 2 * t;
+            if (j0 < nb) S[j0 * mp + i] -= acc[u][n8][0];
+            if (j0 + 1 < nb) S[(j0 + 1) * mp + i] -= acc[u][n8][1];
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // prefetch the next panel's first chunks (columns of panels already stored)
+    const int J1 = J0 + NB;
+    if (J1 < nt) {
+      const int nch1 = J1 / CW;
+      for (int c = 0; c < 2 && c < nch1 && (c + 1) * CW <= J0; ++c) issue_chunk(J1, c);
+    }
+    if (warp == 0) {  // diagonal block: one warp, lane l owns row l
+      double r[NB];
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        r[c] = (lane < nb && c < nb) ? (c <= lane ? S[c * mp + lane] : 0.0) : (c == lane ? 1.0 : 0.0);
+      int fail = -1;
+      diag_step<0, NB>(r, lane, nb, diagv + J0, rdiag, fail, s_colbuf, r[0]);
+      if (lane < nb) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+          if (c <= lane) S[c * mp + lane] = r[c];
+      }
+      if (lane == 0 && fail >= 0) s_fail = J0 + fail;
+    }
+    __syncthreads();
+    if (s_fail >= 0) break;
+#pragma unroll 1
+    for (int i = NB + tid; i < m; i += NT) {  // rows below: x L_dd^T = s
+#pragma unroll
+      for (int jb = 0; jb < NB; jb += 8) {
+        double s8[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) s8[c] = S[(jb + c) * mp + i];
+        trsm_step<0, 8>(s8, S + jb * mp + jb, mp, rdiag + jb);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) S[(jb + c) * mp + i] = s8[c];
+#pragma unroll 4
+        for (int c = jb + 8; c < NB; ++c) {
+          const double* lc = S + c;
+          double v = S[c * mp + i];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v -= s8[j] * lc[(jb + j) * mp];
+          S[c * mp + i] = v;
+        }
+      }
+    }
+    __syncthreads();
+    for (int j = 0; j < nb; ++j)
+      for (int i = tid; i < m; i += NT) L[(size_t)(J0 + j) * nt + J0 + i] = S[j * mp + i];
+  }
+  cp_async_wait<0>();  // a prefetch issued before a failing pivot
+  __syncthreads();
+  if (s_fail >= 0) {
+    if (tid == 0) {
+      a.status[b] = s_fail;
+      a.gain[b] = -INFINITY;
+    }
+  } else {
+    // the reduction of chol_logdet_kernel (256 threads, 8 warps): same bits
+    double part = 0.0;
+    if (tid < 256)
+      for (int j = tid; j < nt; j += 256) part += log(diagv[j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
+    if (lane == 0 && warp < 8) s_red[warp] = part;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < 8; ++w) s += s_red[w];
+      a.status[b] = -1;
+      a.gain[b] = 2.0 * s;
     }
   }
   gain_epilogue(a);

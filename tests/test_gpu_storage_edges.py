@@ -261,6 +261,42 @@ def test_batched_logdet_against_numpy(dsel):
         assert st[2] == m // 2 and ld[2] == -np.inf, (m, st[2], ld[2])
 
 
+def test_staged_gain_kernel_bitwise(dsel, monkeypatch):
+    """chol_logdet_stage_kernel (one 12-warp CTA per candidate streaming the
+    earlier factor columns through shared-memory chunks; taken when
+    128 < Nt <= ~424 and the batch fits one wave) returns the same bits as
+    chol_logdet_kernel (DSEL_CHOL_STAGE=0): batched log-dets at even and odd
+    m, an infeasible pivot, and a whole Nt = 420 selection."""
+    import torch
+
+    rng = np.random.default_rng(11)
+
+    def both(fn):
+        monkeypatch.setenv("DSEL_CHOL_STAGE", "0")
+        ref = fn()
+        monkeypatch.delenv("DSEL_CHOL_STAGE")
+        return ref, fn()
+
+    for m in (129, 200, 301, 420, 424):
+        a = rng.standard_normal((6, m, m + 5)) / np.sqrt(m)
+        mats = a @ a.transpose(0, 2, 1) + 0.5 * np.eye(m)
+        mats[5, m - 40, :] = 0.0
+        mats[5, :, m - 40] = 0.0
+        t = torch.tensor(mats, device="cuda")
+        (l0, s0), (l1, s1) = both(lambda: dsel.batched_logdet(t))
+        assert torch.equal(s0, s1) and int(s1[5]) == m - 40, (m, s0, s1)
+        assert torch.equal(l0, l1), (m, (l0 - l1).abs().max().item())
+
+    def select():
+        with dsel.Engine(24, 420, 4) as eng:
+            eng.gen_synthetic_device(4096, 1.0, 7)
+            eng.run()
+            return [(r["chosen_index"], r["gain"], r["runner_up_gain"]) for r in eng.trace()]
+
+    r0, r1 = both(select)
+    assert r0 == r1, (r0, r1)
+
+
 # ---- out-of-HBM stores (north star (1)) ----------------------------------- #
 def test_file_backed_store_matches_reference(dsel, O, golden_dir, tmp_path):
     """dsel_attach_kbf: K stays in the KBF file; every round preads the chosen
