@@ -280,7 +280,7 @@ struct dsel_engine {
   // double-buffered: the bulk of round t reads buffer t%2 while round t+1 fills
   // the other one.
   bool la = false;
-  int la_reserve = 8;          // SMs left to the chain while a bulk runs (8 measured best on C2)
+  int la_reserve = 8;          // SMs left to the chain while a bulk runs (set per world size at create)
   int prio_least = 0;          // stream priority of the bulk stream
   cudaStream_t s2 = nullptr;
   cudaEvent_t ev_wrdy[2] = {nullptr, nullptr}, ev_bulk[2] = {nullptr, nullptr};
@@ -2139,6 +2139,11 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
         CU(cudaEventCreateWithFlags(&e->ev_wrdy[b], cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&e->ev_bulk[b], cudaEventDisableTiming));
       }
+      // the chain's share grows as the per-GPU bulk shrinks: C2 sweeps
+      // (profiles/r02_la_reserve_c2.json) put the best at 8 / 12 / 16 SMs for
+      // 1 / 2 / 4 GPUs; 16 from 4 GPUs up (8 GPUs: 25 candidates per rank, the
+      // gain kernel's CTAs fit 16 SMs in one wave)
+      e->la_reserve = e->G == 1 ? 8 : e->G == 2 ? 12 : 16;
       if (const char* rs = getenv("DSEL_LA_RESERVE")) e->la_reserve = std::max(0, std::min(e->n_sms - 8, atoi(rs)));
     }
     e->n_tab_ints = n_tab;
