@@ -545,9 +545,10 @@ int chol_mp(int nt) {
   return mp;
 }
 
-// staged gain kernel (one 16-warp CTA per candidate, chunked L stream): on when the
-// batch fits one wave; DSEL_CHOL_STAGE=0 selects chol_logdet_kernel instead
-bool g_chol_stage = true;
+// staged gain kernels (one 12-warp CTA per candidate, chunked L stream) when the
+// batch fits one wave: 2 (default) the look-ahead version, 1 the plain staged
+// one, DSEL_CHOL_STAGE=0 chol_logdet_kernel -- all three give the same bits
+int g_chol_stage = 2;
 size_t g_chol_stage_max = 0;  // dynamic smem the staged kernel may use (opt-in - static)
 
 void launch_chol(const CholArgs& a, int n_batch, cudaStream_t s, int n_sms) {
@@ -562,8 +563,11 @@ void launch_chol(const CholArgs& a, int n_batch, cudaStream_t s, int n_sms) {
       chol_logdet_tri_kernel<2><<<n_batch, 256, ts, s>>>(a);
     else
       chol_logdet_tri_kernel<1><<<n_batch, 256, ts, s>>>(a);
-  } else if (nb == 32 && !two && g_chol_stage && cst::smem_bytes(a.nt, a.mp) <= g_chol_stage_max) {
-    chol_logdet_stage_kernel<12><<<n_batch, 384, cst::smem_bytes(a.nt, a.mp), s>>>(a);
+  } else if (nb == 32 && !two && g_chol_stage > 0 && cst::smem_bytes(a.nt, a.mp) <= g_chol_stage_max) {
+    if (g_chol_stage == 2 && a.nt <= cla::MAX_NT)
+      chol_logdet_la_kernel<<<n_batch, cla::NW * 32, cst::smem_bytes(a.nt, a.mp), s>>>(a);
+    else
+      chol_logdet_stage_kernel<12><<<n_batch, 384, cst::smem_bytes(a.nt, a.mp), s>>>(a);
   } else if (nb == 32) {
     if (two)
       chol_logdet_kernel<32, 2><<<n_batch, 256, smem, s>>>(a);
@@ -621,12 +625,14 @@ void set_smem_limits(int dev) {
   allow_smem(chol_logdet_kernel<32, 2>, optin);
   allow_smem(chol_logdet_kernel<8, 1>, optin);
   {
-    cudaFuncAttributes fa{};
+    cudaFuncAttributes fa{}, fb{};
     CU(cudaFuncGetAttributes(&fa, chol_logdet_stage_kernel<12>));
-    g_chol_stage_max = (size_t)optin - fa.sharedSizeBytes;
+    CU(cudaFuncGetAttributes(&fb, chol_logdet_la_kernel));
+    g_chol_stage_max = (size_t)optin - std::max(fa.sharedSizeBytes, fb.sharedSizeBytes);
     allow_smem(chol_logdet_stage_kernel<12>, optin);
+    allow_smem(chol_logdet_la_kernel, optin);
     const char* cs = getenv("DSEL_CHOL_STAGE");
-    g_chol_stage = !(cs && cs[0] == '0');
+    g_chol_stage = cs ? std::max(0, std::min(2, atoi(cs))) : 2;
   }
   allow_smem(chol_logdet_tri_kernel<1>, optin);
   allow_smem(chol_logdet_tri_kernel<2>, optin);

@@ -1894,10 +1894,10 @@ __device__ __forceinline__ void cp_async_wait_dyn(int n) {
 
 // one CW-column chunk into the accumulators of a warp's NU row tiles
 // (tiles warp, warp + NW, ...); ch points at chunk element (t, g)
-template <int NU, int MAXT, int NW>
+template <int NU, int MAXT, int NW, int K4 = cst::CW / 4>
 __device__ __forceinline__ void stage_chunk_mma(double (&acc)[MAXT][4][2], const double* ch, int mp, int warp) {
 #pragma unroll
-  for (int k4 = 0; k4 < cst::CW / 4; ++k4) {
+  for (int k4 = 0; k4 < K4; ++k4) {
     const double* col = ch + k4 * 4 * mp;
     double bv[4];
 #pragma unroll
@@ -2068,6 +2068,253 @@ __global__ void __launch_bounds__(NW * 32, 1) chol_logdet_stage_kernel(CholArgs 
       for (int i = tid; i < m; i += NT) L[(size_t)(J0 + j) * nt + J0 + i] = S[j * mp + i];
   }
   cp_async_wait<0>();  // a prefetch issued before a failing pivot
+  __syncthreads();
+  if (s_fail >= 0) {
+    if (tid == 0) {
+      a.status[b] = s_fail;
+      a.gain[b] = -INFINITY;
+    }
+  } else {
+    // the reduction of chol_logdet_kernel (256 threads, 8 warps): same bits
+    double part = 0.0;
+    if (tid < 256)
+      for (int j = tid; j < nt; j += 256) part += log(diagv[j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
+    if (lane == 0 && warp < 8) s_red[warp] = part;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < 8; ++w) s += s_red[w];
+      a.status[b] = -1;
+      a.gain[b] = 2.0 * s;
+    }
+  }
+  gain_epilogue(a);
+}
+
+// ------------------------------------------------------------------------ //
+// Look-ahead version of the staged gain kernel (same shapes, the default):   //
+// warp 0 factors panel q's diagonal block while warps 1..11 already stream   //
+// panel q+1's update over the columns finished before panel q (its chunks    //
+// staged in the other of two [32][mp] buffers); then all warps solve panel   //
+// q's rows, warps 1..11 add panel q's own columns to panel q+1's             //
+// accumulators straight from shared memory and form S(q+1) = K - acc in the  //
+// buffer the chunks used, while warp 0 stores panel q's factor columns.      //
+// The accumulation per element is the same chain (k ascending in chunks of   //
+// 16, DMMA k4 steps), so the gains are bitwise those of chol_logdet_kernel.  //
+// ------------------------------------------------------------------------ //
+namespace cla {
+constexpr int NW = 12;        // warps per CTA: warp 0 diagonal, 1..11 update
+constexpr int NWU = NW - 1;   // update warps
+constexpr int MAXT = 5;       // row tiles per update warp: nt - 32 <= 8 * 5 * 11
+constexpr int MAX_NT = 32 + 8 * MAXT * NWU;  // 472
+constexpr int CW = 16;        // chunk width: the next panel's 32-column buffer = 2 slots
+constexpr int SLOTS = 2;      // (8-column chunks in 4 slots measured slower: 496 vs 469 us)
+}  // namespace cla
+
+template <int MAXT, int NWU, int K4>
+__device__ __forceinline__ void la_chunk_mma(int n_u, double (&acc)[MAXT][4][2], const double* ch, int mp,
+                                             int wu) {
+  switch (n_u) {
+    case 5: stage_chunk_mma<5, MAXT, NWU, K4>(acc, ch, mp, wu); break;
+    case 4: stage_chunk_mma<4, MAXT, NWU, K4>(acc, ch, mp, wu); break;
+    case 3: stage_chunk_mma<3, MAXT, NWU, K4>(acc, ch, mp, wu); break;
+    case 2: stage_chunk_mma<2, MAXT, NWU, K4>(acc, ch, mp, wu); break;
+    case 1: stage_chunk_mma<1, MAXT, NWU, K4>(acc, ch, mp, wu); break;
+    default: break;
+  }
+}
+
+__device__ __forceinline__ void bar_named(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+// rows below a panel's diagonal block: x L_dd^T = s, one row per thread
+// (tid0/nthr: this thread's slot in the threads sharing the rows)
+__device__ __forceinline__ void panel_row_solve(double* S, int mp, int m, const double* rdiag, int tid0,
+                                                int nthr) {
+  constexpr int NB = cst::NB;
+#pragma unroll 1
+  for (int i = NB + tid0; i < m; i += nthr) {
+#pragma unroll
+    for (int jb = 0; jb < NB; jb += 8) {
+      double s8[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) s8[c] = S[(jb + c) * mp + i];
+      trsm_step<0, 8>(s8, S + jb * mp + jb, mp, rdiag + jb);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) S[(jb + c) * mp + i] = s8[c];
+#pragma unroll 4
+      for (int c = jb + 8; c < NB; ++c) {
+        const double* lc = S + c;
+        double v = S[c * mp + i];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v -= s8[j] * lc[(jb + j) * mp];
+        S[c * mp + i] = v;
+      }
+    }
+  }
+}
+
+// panel q's factor columns to the L2-resident scratch by every thread of the
+// CTA (16-byte stores when nt is even: 8-byte aligned panels of even height)
+__device__ __forceinline__ void la_store_panel(double* L, const double* S, int nt, int J0, int nb, int m, int mp,
+                                               int tid, int nthr) {
+  if ((nt & 1) == 0 && (reinterpret_cast<uintptr_t>(L) & 15) == 0) {
+    const int h = m >> 1;
+    for (int j = 0; j < nb; ++j)
+      for (int i2 = tid; i2 < h; i2 += nthr)
+        *reinterpret_cast<double2*>(L + (size_t)(J0 + j) * nt + J0 + 2 * i2) =
+            *reinterpret_cast<const double2*>(S + j * mp + 2 * i2);
+  } else {
+    for (int j = 0; j < nb; ++j)
+      for (int i = tid; i < m; i += nthr) L[(size_t)(J0 + j) * nt + J0 + i] = S[j * mp + i];
+  }
+}
+
+// Warp 0 and the update warps run separate loops (the same barrier sequence:
+// three __syncthreads per panel), so the update warps' accumulators are never
+// live across the diagonal factorization's registers.
+__global__ void __launch_bounds__(cla::NW * 32, 1) chol_logdet_la_kernel(CholArgs a) {
+  constexpr int NB = cst::NB, CW = cla::CW, NT = cla::NW * 32, NWU = cla::NWU, MAXT = cla::MAXT;
+  constexpr int NTU = NWU * 32;  // update-group threads
+  static_assert(cla::MAX_NT <= 2 * NTU, "one 16-byte chunk copy per column per update thread");
+  static_assert(CW * cla::SLOTS == NB, "the chunk slots tile the next panel's buffer");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int b = blockIdx.x;
+  if (b >= a.n) return;
+  const int nt = a.nt, mp = a.mp;
+  double* BUF = reinterpret_cast<double*>(smem_raw);  // [2][NB][mp]: S(q) in BUF[q & 1]
+  double* diagv = BUF + 2 * NB * mp;                  // [nt]
+  __shared__ double rdiag[NB];
+  __shared__ __align__(16) double s_colbuf[64];
+  __shared__ int s_fail;
+  __shared__ double s_red[8];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const double* src = a.src + a.src_off[b];
+  const long long lds = a.src_ld[b];
+  double* L = a.L + (size_t)b * a.l_stride;  // column-major nt x nt
+  const int np = (nt + NB - 1) / NB;
+  if (tid == 0) s_fail = -1;
+  // S(0): panel 0 of the candidate's block
+  for (int j = 0; j < min(NB, nt); ++j)
+    for (int i = tid; i < nt; i += NT) cp_async8(BUF + j * mp + i, src + (size_t)j * lds + i, true);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  if (warp == 0) {
+    // ============ diagonal blocks, their share of the row solve, stores ============
+    for (int q = 0; q < np; ++q) {
+      const int J0 = q * NB, nb = min(NB, nt - J0), m = nt - J0;
+      double* S = BUF + (q & 1) * NB * mp;
+      {
+        double r[NB];
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+          r[c] = (lane < nb && c < nb) ? (c <= lane ? S[c * mp + lane] : 0.0) : (c == lane ? 1.0 : 0.0);
+        int fail = -1;
+        diag_step<0, NB>(r, lane, nb, diagv + J0, rdiag, fail, s_colbuf, r[0]);
+        if (lane < nb) {
+#pragma unroll
+          for (int c = 0; c < NB; ++c)
+            if (c <= lane) S[c * mp + lane] = r[c];
+        }
+        if (lane == 0 && fail >= 0) s_fail = J0 + fail;
+      }
+      __syncthreads();  // (1) diagonal block done
+      if (s_fail >= 0) break;
+      panel_row_solve(S, mp, m, rdiag, tid, NT);
+      __syncthreads();  // (2) panel q solved
+      la_store_panel(L, S, nt, J0, nb, m, mp, tid, NT);
+      __syncthreads();  // (3) S(q+1) formed
+    }
+  } else {
+    // ============ update warps: panel q+1 while panel q is factored ============
+    const int g = lane >> 2, t = lane & 3;
+    const int wu = warp - 1, tu = tid - 32;
+    const bool vec = ((nt & 1) == 0) && ((a.l_stride & 1) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(a.L) & 15) == 0);
+    double acc[MAXT][4][2];
+    for (int q = 0; q < np; ++q) {
+      const int J0 = q * NB, m = nt - J0;
+      double* S = BUF + (q & 1) * NB * mp;
+      double* N = BUF + ((q + 1) & 1) * NB * mp;  // panel q+1: chunk slots, then S(q+1)
+      const bool next = q + 1 < np;
+      const int J1 = J0 + NB, m1 = nt - J1, nb1 = next ? min(NB, nt - J1) : 0;
+      const int mt_n1 = next ? (m1 + 7) >> 3 : 0;
+      const int n_u = wu < mt_n1 ? (mt_n1 - wu + NWU - 1) / NWU : 0;
+#pragma unroll
+      for (int u = 0; u < MAXT; ++u)
+#pragma unroll
+        for (int n8 = 0; n8 < 4; ++n8) acc[u][n8][0] = acc[u][n8][1] = 0.0;
+      // phase A: L[J1:, 0:J0] in chunks of 16 columns through N's two slots
+      const int nch = next ? J0 / CW : 0;
+      auto issue = [&](int c) {
+        double* dst = N + (c % cla::SLOTS) * CW * mp;
+        const double* sc = L + (size_t)(c * CW) * nt + J1;
+        if (vec) {
+          const int i = 2 * tu;
+          if (i < m1) {
+#pragma unroll
+            for (int j = 0; j < CW; ++j) cp_async16(dst + j * mp + i, sc + (size_t)j * nt + i, true);
+          }
+        } else {
+#pragma unroll 4
+          for (int j = 0; j < CW; ++j)
+            for (int i = tu; i < m1; i += NTU) cp_async8(dst + j * mp + i, sc + (size_t)j * nt + i, true);
+        }
+        cp_async_commit();
+      };
+      for (int c = 0; c < min(nch, cla::SLOTS - 1); ++c) issue(c);
+      for (int c = 0; c < nch; ++c) {
+        // chunk c landed (chunks up to c + SLOTS - 2 may still be in flight)
+        cp_async_wait_dyn(min(nch, c + cla::SLOTS - 1) - c - 1);
+        bar_named(1, NTU);  // ... for every thread, and chunk c - 1's slot is free
+        if (c + cla::SLOTS - 1 < nch) issue(c + cla::SLOTS - 1);
+        la_chunk_mma<MAXT, NWU, CW / 4>(n_u, acc, N + (c % cla::SLOTS) * CW * mp + t * mp + g, mp, wu);
+      }
+      // K's panel q+1 into N while warp 0 still factors (every slot consumed first)
+      if (next) {
+        bar_named(1, NTU);
+        for (int j = 0; j < nb1; ++j)
+          for (int i = tu; i < m1; i += NTU) cp_async8(N + j * mp + i, src + (size_t)(J1 + j) * lds + J1 + i, true);
+        cp_async_commit();
+      }
+      __syncthreads();  // (1)
+      if (s_fail >= 0) break;
+      // phase B: the row solve
+      panel_row_solve(S, mp, m, rdiag, tid, NT);
+      __syncthreads();  // (2)
+      // phase C: panel q's own columns (chunks 2q, 2q+1 of the same chain) from
+      // shared memory, then S(q+1) = K - acc in N
+      if (next) {
+        const double* Lq = S + NB + t * mp + g;  // rows J1.. of panel q's columns
+        la_chunk_mma<MAXT, NWU, 4>(n_u, acc, Lq, mp, wu);
+        la_chunk_mma<MAXT, NWU, 4>(n_u, acc, Lq + 16 * mp, mp, wu);
+        cp_async_wait<0>();
+        bar_named(1, NTU);  // K's panel q+1 landed for every update thread
+#pragma unroll
+        for (int u = 0; u < MAXT; ++u) {
+          if (u < n_u) {
+            const int i = (wu + u * NWU) * 8 + g;
+            if (i < m1) {
+#pragma unroll
+              for (int n8 = 0; n8 < 4; ++n8) {
+                const int j0 = n8 * 8 + 2 * t;
+                if (j0 < nb1) N[j0 * mp + i] -= acc[u][n8][0];
+                if (j0 + 1 < nb1) N[(j0 + 1) * mp + i] -= acc[u][n8][1];
+              }
+            }
+          }
+        }
+      }
+      la_store_panel(L, S, nt, J0, min(NB, nt - J0), m, mp, tid, NT);
+      __syncthreads();  // (3)
+    }
+  }
+  cp_async_wait<0>();
   __syncthreads();
   if (s_fail >= 0) {
     if (tid == 0) {

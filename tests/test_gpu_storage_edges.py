@@ -262,20 +262,30 @@ def test_batched_logdet_against_numpy(dsel):
 
 
 def test_staged_gain_kernel_bitwise(dsel, monkeypatch):
-    """chol_logdet_stage_kernel (one 12-warp CTA per candidate streaming the
+    """The staged gain kernels (one 12-warp CTA per candidate streaming the
     earlier factor columns through shared-memory chunks; taken when
-    128 < Nt <= ~424 and the batch fits one wave) returns the same bits as
+    128 < Nt <= ~424 and the batch fits one wave) -- the default look-ahead
+    version (next panel's stream beside the diagonal factorization) and the
+    plain one (DSEL_CHOL_STAGE=1) -- return the same bits as
     chol_logdet_kernel (DSEL_CHOL_STAGE=0): batched log-dets at even and odd
     m, an infeasible pivot, and a whole Nt = 420 selection."""
     import torch
 
     rng = np.random.default_rng(11)
 
-    def both(fn):
+    def both(fn):  # chol_logdet_kernel vs the default (look-ahead staged kernel)
         monkeypatch.setenv("DSEL_CHOL_STAGE", "0")
         ref = fn()
+        monkeypatch.setenv("DSEL_CHOL_STAGE", "1")  # the plain staged kernel: same bits too
+        assert_same(ref, fn())
         monkeypatch.delenv("DSEL_CHOL_STAGE")
         return ref, fn()
+
+    def assert_same(x, y):
+        if isinstance(x, tuple) and hasattr(x[0], "cpu"):
+            assert all(torch.equal(u, v) for u, v in zip(x, y))
+        else:
+            assert x == y
 
     for m in (129, 200, 301, 420, 424):
         a = rng.standard_normal((6, m, m + 5)) / np.sqrt(m)
