@@ -375,6 +375,9 @@ using BigT = Cfg<128, 1, 3, 1, 1>;
 // BigR: Big's tiles and stages, DMMA from zero, bulk reduce-add write-back
 using BigR = Cfg<128, 2, 3, 1, 2>;
 using BigR4 = Cfg<128, 3, 2, 1, 2>;  // BigR with Big4's stages (long k)
+// PairR: Pair's 64-row tiles on 2 CTAs/SM with BigR's zero start and bulk
+// reduce-add write-back -- the two CTAs' tile transitions drift apart
+using PairR = Cfg<64, 2, 2, 2, 2>;
 constexpr int ROW_PAD = 384;  // lcm of the tile heights: tiled W buffers are padded to it
 static_assert(Big::SMEM <= 232448 - 2048, "ws kernel shared memory (1 CTA/SM)");
 static_assert(Big4::SMEM <= 232448 - 2048, "ws kernel shared memory (Big4)");
@@ -383,6 +386,7 @@ static_assert(BigT::SMEM <= 232448 - 2048, "ws kernel shared memory (BigT)");
 static_assert(BigR::SMEM <= 232448 - 2048, "ws kernel shared memory (BigR)");
 static_assert(BigR4::SMEM <= 232448 - 2048, "ws kernel shared memory (BigR4)");
 static_assert(2 * (Pair::SMEM + 2048) <= 233472, "ws kernel shared memory (2 CTAs/SM)");
+static_assert(2 * (PairR::SMEM + 2048) <= 233472, "ws kernel shared memory (PairR, 2 CTAs/SM)");
 constexpr int THREADS = Big::THREADS;
 constexpr size_t SMEM = Big::SMEM;
 }  // namespace ws
