@@ -254,7 +254,7 @@ struct dsel_engine {
   const double** d_peer_wsend = nullptr;
   unsigned long long** d_peer_flag = nullptr;
   int ws_br = 128;  // tile height of the right-looking update configuration (rl_cfg)
-  int ws_cfg = -1;   // DSEL_WS_CFG: -1 auto, 0 Big, 1 Pair, 2 Big4, 3 Big6, 4 BigT, 5 BigR, 6 BigR4, 7 PairR
+  int ws_cfg = -1;   // DSEL_WS_CFG: -1 auto, 0 Big, 1 Pair, 2 Big4, 3 Big6, 4 BigT, 5 BigR, 6 BigR4, 7 PairR, 8 BigR6
   int rl_cfg = 5;    // configuration of the right-looking update (BigR by default)
   int ws_group = kWsGroupDefault;  // column tiles per rasterization group
   double gen_flops = 0.0;  // last dsel_gen_synthetic_device (K formation on the update kernel)
@@ -648,6 +648,7 @@ void set_smem_limits(int dev) {
   allow_smem(schur_update_ws_kernel<ws::BigR>, optin);
   allow_smem(schur_update_ws_kernel<ws::BigR4>, optin);
   allow_smem(schur_update_ws_kernel<ws::PairR>, optin);
+  allow_smem(schur_update_ws_kernel<ws::BigR6>, optin);
   CU(cudaFuncSetAttribute(schur_update_ws_kernel<ws::Pair>, cudaFuncAttributePreferredSharedMemoryCarveout,
                           (int)cudaSharedmemCarveoutMaxShared));
   CU(cudaFuncSetAttribute(schur_update_ws_kernel<ws::PairR>, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -839,6 +840,9 @@ void launch_ws(dsel_engine* e, UpdateWSArgs& ua, int cfg, int sms = 0, cudaStrea
   } else if (cfg == 6) {
     const int grid = (int)std::min<long long>(sms, units);
     schur_update_ws_kernel<ws::BigR4><<<grid, ws::BigR4::THREADS, ws::BigR4::SMEM, st>>>(ua);
+  } else if (cfg == 8) {
+    const int grid = (int)std::min<long long>(sms, units);
+    schur_update_ws_kernel<ws::BigR6><<<grid, ws::BigR6::THREADS, ws::BigR6::SMEM, st>>>(ua);
   } else if (cfg == 7) {
     const int grid = (int)std::min<long long>(2LL * sms, units);
     schur_update_ws_kernel<ws::PairR><<<grid, ws::PairR::THREADS, ws::PairR::SMEM, st>>>(ua);
@@ -2053,7 +2057,7 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
       CU(cudaEventCreateWithFlags(&e->ev_copy[b], cudaEventDisableTiming));
       CU(cudaEventCreateWithFlags(&e->ev_scat[b], cudaEventDisableTiming));
     }
-    if (const char* wc = getenv("DSEL_WS_CFG")) e->ws_cfg = std::max(-1, std::min(7, atoi(wc)));
+    if (const char* wc = getenv("DSEL_WS_CFG")) e->ws_cfg = std::max(-1, std::min(8, atoi(wc)));
     // BigR: DMMA from zero + bulk reduce-add write-back; its 3 x 2 stage
     // variant from 16 k-chunks (Nt = 420), like Big4 for the plain kernel
     e->rl_cfg = e->ws_cfg >= 0 ? e->ws_cfg : (e->ldw / ws::KC >= 16 ? 6 : 5);

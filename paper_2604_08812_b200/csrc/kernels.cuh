@@ -378,6 +378,7 @@ using BigR4 = Cfg<128, 3, 2, 1, 2>;  // BigR with Big4's stages (long k)
 // PairR: Pair's 64-row tiles on 2 CTAs/SM with BigR's zero start and bulk
 // reduce-add write-back -- the two CTAs' tile transitions drift apart
 using PairR = Cfg<64, 2, 2, 2, 2>;
+using BigR6 = Cfg<128, 1, 6, 1, 2>;  // BigR with one chunk per stage, six stages (experiment)
 constexpr int ROW_PAD = 384;  // lcm of the tile heights: tiled W buffers are padded to it
 static_assert(Big::SMEM <= 232448 - 2048, "ws kernel shared memory (1 CTA/SM)");
 static_assert(Big4::SMEM <= 232448 - 2048, "ws kernel shared memory (Big4)");
@@ -385,6 +386,7 @@ static_assert(Big6::SMEM <= 232448 - 2048, "ws kernel shared memory (Big6)");
 static_assert(BigT::SMEM <= 232448 - 2048, "ws kernel shared memory (BigT)");
 static_assert(BigR::SMEM <= 232448 - 2048, "ws kernel shared memory (BigR)");
 static_assert(BigR4::SMEM <= 232448 - 2048, "ws kernel shared memory (BigR4)");
+static_assert(BigR6::SMEM <= 232448 - 2048, "ws kernel shared memory (BigR6)");
 static_assert(2 * (Pair::SMEM + 2048) <= 233472, "ws kernel shared memory (2 CTAs/SM)");
 static_assert(2 * (PairR::SMEM + 2048) <= 233472, "ws kernel shared memory (PairR, 2 CTAs/SM)");
 constexpr int THREADS = Big::THREADS;
