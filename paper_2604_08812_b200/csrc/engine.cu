@@ -271,6 +271,9 @@ struct dsel_engine {
   int *status = nullptr, *kstatus = nullptr;
   int *d_pos_sensor = nullptr, *d_slot_sensor = nullptr;
   unsigned* d_counter = nullptr;  // gain-launch ticket for the fused argmax (zero between launches)
+  unsigned long long* ws_ctr = nullptr;       // update-kernel claim counters (compute / bulk stream), in d_counter's block
+  unsigned long long ws_ctr_base[2] = {0, 0};  // their values at the next launch
+  bool ws_dynamic = true;                      // DSEL_WS_DYNAMIC=0: static round-robin tile schedule
   int* d_round = nullptr;  // per-round tables (one block, one upload): d_tab | d_sym | d_hb
   int* h_round = nullptr;  // pinned staging of the same layout
   // look-ahead rounds (symmetric right-looking, Nt a multiple of the tile):
@@ -822,6 +825,13 @@ void launch_ws(dsel_engine* e, UpdateWSArgs& ua, int cfg, int sms = 0, cudaStrea
   if (units <= 0) return;
   if (!st) st = e->s;
   if (sms <= 0) sms = e->n_sms;
+  // dynamic schedule: one claim counter per stream (launches on a stream run
+  // one after another); every launch advances it by units + grid claims
+  const int ci = st == e->s2 ? 1 : 0;
+  const int grid_ws = (int)std::min<long long>(((cfg == 1 || cfg == 7) ? 2LL : 1LL) * sms, units);
+  ua.ctr = e->ws_dynamic ? e->ws_ctr + ci : nullptr;
+  ua.ctr_base = e->ws_ctr_base[ci];
+  if (e->ws_dynamic) e->ws_ctr_base[ci] += (unsigned long long)units + (unsigned long long)grid_ws;
   if (cfg == 1) {
     const int grid = (int)std::min<long long>(2LL * sms, units);
     schur_update_ws_kernel<ws::Pair><<<grid, ws::Pair::THREADS, ws::Pair::SMEM, st>>>(ua);
@@ -1978,7 +1988,7 @@ uint64_t plan_bytes(const dsel_engine* e, const dsel_config* cfg) {
   add(e->nc, 4);
   add(e->nloc + 1, 4);
   add(1, sizeof(ArgRec));
-  add(1, 4);
+  add(3, 8);  // gain ticket + update-kernel claim counters
   add(e->G, sizeof(ArgRec));
   if (e->stream) add(nloc1 * nt * nt, 8);
   return b;
@@ -2180,8 +2190,14 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
     e->d_pos_sensor = dmalloc<int>(e->nc, tot);
     e->d_slot_sensor = dmalloc<int>(e->nloc + 1, tot);
     e->d_rec = dmalloc<ArgRec>(1, tot);
-    e->d_counter = reinterpret_cast<unsigned*>(dmalloc<int>(1, tot));
-    CU(cudaMemsetAsync(e->d_counter, 0, sizeof(unsigned), e->s));
+    {  // [0]: the gain ticket (low word); [1], [2]: update-kernel claim counters
+      unsigned long long* blk = dmalloc<unsigned long long>(3, tot);
+      CU(cudaMemsetAsync(blk, 0, 3 * sizeof(unsigned long long), e->s));
+      e->d_counter = reinterpret_cast<unsigned*>(blk);
+      e->ws_ctr = blk + 1;
+      const char* wd = getenv("DSEL_WS_DYNAMIC");
+      e->ws_dynamic = !(wd && wd[0] == '0');
+    }
     e->d_recs = dmalloc<ArgRec>(e->G, tot);
     CU(ds_malloc_host(&e->h_recs, sizeof(ArgRec) * e->G));
     if (e->W) CU(cudaMemsetAsync(e->W, 0, sizeof(double) * (size_t)e->n * e->ldw, e->s));

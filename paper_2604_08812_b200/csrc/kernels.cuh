@@ -444,6 +444,12 @@ struct UpdateWSArgs {
   int la_mode;
   int excl_g, excl_h;
   const int2* tlist;
+  // dynamic tile schedule: non-null -> each CTA's producer claims units from
+  // this per-stream counter (value - ctr_base = unit), so a CTA that starts
+  // late (its SM busy with another stream's kernel) takes fewer tiles; null ->
+  // static round robin (unit = blockIdx.x + i * gridDim.x)
+  unsigned long long* ctr;
+  unsigned long long ctr_base;
 };
 
 // unit -> (tile, split z, k-chunk range)
@@ -661,7 +667,14 @@ __global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(
     int stage = 0;
     unsigned ephase = 0;
     int it = 0;
-    for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
+    auto claim = [&](int prev) -> int {
+      if (!a.ctr) return prev < 0 ? (int)blockIdx.x : prev + (int)gridDim.x;
+      unsigned long long v = 0;
+      if (lane == 0) v = atomicAdd(a.ctr, 1ull);
+      v = __shfl_sync(0xffffffffu, v, 0);
+      return (int)min(v - a.ctr_base, (unsigned long long)n_units);
+    };
+    for (int unit = claim(-1); unit < n_units; unit = claim(unit)) {
       int r0, c0, tile, uz, kb_lo, kb_hi;
       ws_unit(a, unit, tile, uz, kb_lo, kb_hi);
       if (!ws_tile(a, fr, gp, tile, r0, c0)) continue;
@@ -825,12 +838,14 @@ __global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(
     // walks the producer's tile sequence; per finished tile, bulk copies of
     // each column's row runs from sOut to C (rows above a packed panel's first
     // stored row clipped), then releases sOut and the tile's maps
-    int it = 0;
-    for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
-      int r0, c0, tile, uz, kb_lo, kb_hi;
-      ws_unit(a, unit, tile, uz, kb_lo, kb_hi);
-      if (!ws_tile(a, fr, gp, tile, r0, c0)) continue;
+    // follows the producer's tile sequence through the map buffers (the same
+    // tfull barriers the consumers wait on), so it also works with the
+    // dynamic schedule
+    for (int it = 0;; ++it) {
       const int b = it & 1;
+      mbar_wait(&tfull[b], (it >> 1) & 1);
+      if (!s_tflag[b]) break;
+      const int c0 = s_tile_c0[b];
       mbar_wait(ofull, it & 1);
       const long long* colbase = colbase_of(b);
       const int* rowphys = rowphys_of(b);
@@ -860,7 +875,6 @@ __global__ void __launch_bounds__(Cf::THREADS, Cf::MINB) schur_update_ws_kernel(
         mbar_arrive(oempty);
         mbar_arrive(&mempty[b]);
       }
-      ++it;
     }
     asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // writes landed before exit
     return;
