@@ -460,6 +460,8 @@ def our_arm(args, world, rank, local):
         cpu = cpu_reference(hv, nd, nt, budget, chosen)
 
     tr = ncu_traffic(os.path.join(ROOT, "profiles"), args.algorithm, args.config, world)
+    if tr and "dynamic_schedule" in tr and os.environ.get("DSEL_WS_DYNAMIC", "1") != "0":
+        tr = dict(tr, **tr["dynamic_schedule"])  # the capture of the schedule this run uses
     traffic = tr.get("traffic_bytes_per_launch") if tr else None
     peak = peaks_min["dmma_tflops"]
     line = {
