@@ -482,7 +482,8 @@ def our_arm(args, world, rank, local):
                    "chosen_first": chosen[:8]},
         "algorithm": ALGO_DESC[args.algorithm],
         "schedule": ({"primary": "look-ahead rounds (the bulk of round t beside round t+1's gains, "
-                                 "argmax and W solve; 8 SMs reserved for that chain)",
+                                 "argmax and W solve; %s SMs reserved for that chain)"
+                                 % os.environ.get("DSEL_LA_RESERVE", "12" if world <= 2 else "16"),
                       "plain_schedule_value": round(plain["value"], 6),
                       "roofline_from": "the plain schedule (the same update kernel on all 148 SMs; "
                                        "under look-ahead it shares the GPU with the chain)",

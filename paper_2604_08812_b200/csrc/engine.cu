@@ -2165,11 +2165,11 @@ void create_impl(const dsel_config* cfg, dsel_engine** out) {
         CU(cudaEventCreateWithFlags(&e->ev_wrdy[b], cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&e->ev_bulk[b], cudaEventDisableTiming));
       }
-      // the chain's share grows as the per-GPU bulk shrinks: C2 sweeps
-      // (profiles/r02_la_reserve_c2.json) put the best at 8 / 12 / 16 SMs for
-      // 1 / 2 / 4 GPUs; 16 from 4 GPUs up (8 GPUs: 25 candidates per rank, the
-      // gain kernel's CTAs fit 16 SMs in one wave)
-      e->la_reserve = e->G == 1 ? 8 : e->G == 2 ? 12 : 16;
+      // C2 sweeps (profiles/r02_la_reserve_c2.json): 12 SMs at 1 GPU (with the
+      // dynamic tile schedule; 8 with the static one), 12 at 2, 16 from 4 GPUs
+      // up (8 GPUs: 25 candidates per rank, the gain kernel's CTAs fit 16 SMs
+      // in one wave)
+      e->la_reserve = e->G <= 2 ? 12 : 16;
       if (const char* rs = getenv("DSEL_LA_RESERVE")) e->la_reserve = std::max(0, std::min(e->n_sms - 8, atoi(rs)));
     }
     e->n_tab_ints = n_tab;
